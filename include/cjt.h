@@ -1,0 +1,140 @@
+/*
+ * cjt.h - C ABI of the B200 Chebyshev-Jacobi transform library (libcjt_b200.so).
+ *
+ * Plain C types only: pointers, sizes, int status codes.  Every entry point
+ * returns 0 on success and a nonzero CJT_E* code on failure; the message of
+ * the last failure on the calling thread is returned by cjt_last_error().
+ *
+ * Which reference interface each entry point replaces (reference package
+ * `chebjac`, /root/reference/pkg/src/chebjac):
+ *
+ *   cjt_plan_create / cjt_plan_destroy   engine.plan (engine.py:96-130): the
+ *        host builds the reference plan (partition, tables, weights) and
+ *        hands the arrays over; the library uploads them once and derives the
+ *        device work lists (recurrence checkpoints, chirp-z tables).
+ *   cjt_execute          engine.forward (engine.py:153-186) / engine.inverse
+ *        (engine.py:189-227), batched: device pointers in and out.
+ *   cjt_execute_host     the same, host buffers in and out (H2D + execute +
+ *        D2H on the given stream), i.e. what a drop-in caller of
+ *        forward()/inverse() with NumPy arrays sees.
+ *   cjt_clenshaw_points        backend plugin `clenshaw_points`
+ *        (_kernels_cy.pyx:83-122, _kernels_np.py:22-57), same 12 arrays,
+ *        host pointers, overwrites out.
+ *   cjt_transpose_accumulate   backend plugin `transpose_accumulate`
+ *        (_kernels_cy.pyx:201-237, _kernels_np.py:60-97), same 12 arrays,
+ *        host pointers, accumulates into out.
+ *   cjt_host_angles      the libm cos / half-angle evaluation the reference
+ *        kernel performs per point (_kernels_cy.pyx:27,58-64), exposed so
+ *        plans carry bit-identical x and x -+ 1 values.
+ */
+#ifndef CJT_B200_H
+#define CJT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CJT_OK 0
+#define CJT_EINVAL 1   /* bad argument (maps to ValueError) */
+#define CJT_ECUDA 2    /* CUDA runtime failure */
+#define CJT_ENOMEM 3   /* device allocation failed */
+#define CJT_ENODEV 4   /* no CUDA device */
+
+#define CJT_FORWARD 0
+#define CJT_INVERSE 1
+
+/* One batched chirp-z product with fused diagonals (see planner.py ChirpZ):
+ *   out[b, q0+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
+ *   z_{b,m}[s] = sum_t exp(i pi (p0+t)(q0+s)/G) pre[m, t] x[b, p0+t].
+ * Complex arrays are interleaved (re, im) float64. */
+typedef struct {
+    int64_t p0, width;      /* input index range */
+    int64_t q0, count;      /* output index range */
+    int64_t length;         /* power-of-two Bluestein length >= width+count-1 */
+    int32_t m_count;        /* number of summed terms */
+    int32_t accumulate;     /* 1: out +=, 0: out = */
+    const double* pre;      /* [m_count][width] complex */
+    const double* post;     /* [m_count][count] complex */
+    const double* kernel_hat; /* [length] complex, natural order, 1/length folded in */
+} cjt_chirpz_desc;
+
+typedef struct {
+    int32_t direction;      /* CJT_FORWARD or CJT_INVERSE */
+    int32_t m_terms;
+    int64_t n;              /* degree N of the coefficient vectors */
+    int64_t grid_n;         /* G = N (forward) or 2N (inverse) */
+    /* recurrence region, one entry per grid row 0..G */
+    const double* x;        /* cos(theta_i) (libm) */
+    const double* xm;       /* x - x0 via half angles for regions +-1, unused for 0 */
+    const int8_t* regions;  /* 0 interior, 1 near +1, -1 near -1 */
+    const int64_t* cuts;    /* recurrence degrees at row i are 0..cuts[i]-1 (already capped) */
+    /* recurrence tables, length table_len (>= max cut + 1) */
+    int64_t table_len;
+    const double* A;
+    const double* B;
+    const double* C;
+    const double* rf_plus;
+    const double* rf_minus;
+    const double* rf_plus_inv;
+    const double* rf_minus_inv;
+    /* asymptotic blocks */
+    int32_t n_blocks;
+    const cjt_chirpz_desc* blocks;
+    /* forward: Chebyshev analysis; inverse: weighted Chebyshev synthesis */
+    cjt_chirpz_desc edge;
+    /* inverse: 1/A_n for n = 0..N (NULL for forward) */
+    const double* scalings;
+} cjt_plan_desc;
+
+typedef struct cjt_plan cjt_plan;
+
+typedef struct {
+    int64_t launches_per_execute;   /* kernels one cjt_execute launches (batch-independent) */
+    int64_t rec_steps;              /* sum over rows of recurrence degrees */
+    int64_t checkpoint_bytes;
+    int64_t workspace_bytes;
+    int64_t reserved_batch;
+    double rec_flops_per_vector;    /* 2 flop per (row, degree) contraction */
+    double fft_points_per_vector;   /* sum of Bluestein lengths x log2(length) x 2 */
+} cjt_plan_stats;
+
+int cjt_version(void);
+const char* cjt_last_error(void);
+int cjt_device_count(int* count);
+
+int cjt_plan_create(const cjt_plan_desc* desc, cjt_plan** out);
+int cjt_plan_destroy(cjt_plan* plan);
+int cjt_plan_reserve(cjt_plan* plan, int64_t max_batch);
+int cjt_plan_stats_get(const cjt_plan* plan, cjt_plan_stats* stats);
+
+/* in: [batch][N+1] float64, out: [batch][N+1] float64, device pointers.
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+int cjt_execute(cjt_plan* plan, const double* in, double* out, int64_t batch, void* stream);
+/* Same with host buffers; copies happen on `stream`, returns after D2H completes. */
+int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host,
+                     int64_t batch, void* stream);
+
+/* Reference backend-plugin signatures, host arrays (see header comment). */
+int cjt_clenshaw_points(const double* A, const double* B, const double* C,
+                        const double* rb_plus, const double* rb_minus,
+                        const double* rb_plus_inv, const double* rb_minus_inv,
+                        const double* coeffs, int64_t n_coeffs,
+                        const double* thetas, const int64_t* cuts,
+                        const int8_t* regions, double* out, int64_t n_points);
+int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
+                             const double* rf_plus, const double* rf_minus,
+                             const double* rf_plus_inv, const double* rf_minus_inv,
+                             const double* wv, const double* thetas,
+                             const int64_t* cuts, const int8_t* regions,
+                             double* out, int64_t n_out, int64_t n_points,
+                             int64_t table_len);
+
+int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n,
+                    double* x, double* xm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CJT_B200_H */

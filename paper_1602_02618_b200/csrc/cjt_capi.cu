@@ -1,0 +1,650 @@
+// C ABI (include/cjt.h): plan upload, work-list construction, batched
+// execution of the forward / inverse transform, and the reference
+// backend-plugin entry points.
+//
+// Execution order (one stream, no host synchronisation inside cjt_execute):
+//   forward (engine.py:153-186)
+//     1. K1 recurrence contraction (split-K items)      -> partials
+//     2. fixed-order partial reduction                   -> values[b][0..G]
+//     3. per asymptotic block: chirp-z, summed over m    -> values += ...
+//     4. Chebyshev analysis chirp-z                      -> out[b][0..N]
+//   inverse (engine.py:189-227)
+//     1. weighted Chebyshev synthesis chirp-z            -> wv[b][0..G]
+//     2. per asymptotic block (degrees <= N only)        -> acc[b][0..N]
+//     3. K2 recurrence contraction (degrees <= N only)   -> partials
+//     4. fixed-order reduction, + acc, * 1/A_n           -> out[b][0..N]
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "cjt_internal.cuh"
+
+namespace cjt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+}  // namespace cjt
+
+using namespace cjt;
+
+struct cjt_plan {
+  int device = 0;
+  int direction = 0;
+  int m_terms = 0;
+  int64_t n = 0, G = 0, nrows = 0;
+  std::vector<void*> allocs;
+
+  RecRowsDev rows{};
+  RecTablesDev tab{};
+  std::vector<int64_t> h_cut;
+  int64_t* ck_off = nullptr;
+  double2* ck = nullptr;
+  int64_t ck_count = 0;
+  int64_t rec_steps = 0;
+
+  std::vector<ChirpZDev> blocks;
+  ChirpZDev edge{};
+  bool has_edge = false;
+  double2* tw8192 = nullptr;
+  double* scal = nullptr;
+  int64_t scratch_elems_per_vec = 0;  // complex elements of multipass scratch per vector
+  double fft_points = 0.0;
+
+  // batch-dependent state (cjt_plan_reserve)
+  int64_t reserved = 0;
+  std::vector<void*> ws_allocs;
+  FwdItem* fitems = nullptr;
+  int64_t n_fitems = 0;
+  int32_t* tile_slot0 = nullptr;
+  int32_t* tile_nslot = nullptr;
+  int64_t n_fslots = 0;
+  InvItem* iitems = nullptr;
+  int64_t n_iitems = 0;
+  int32_t* tile_ids = nullptr;
+  int32_t* dt_slot0 = nullptr;
+  int32_t* dt_nslot = nullptr;
+  int64_t n_islots = 0;
+  double* part = nullptr;
+  double* vals = nullptr;    // forward values / inverse wv, [B][G+1]
+  double* yacc = nullptr;    // inverse block accumulator [B][N+1]
+  double2* scratch = nullptr;
+  double* io_in = nullptr;
+  double* io_out = nullptr;
+  int64_t workspace_bytes = 0;
+  int64_t last_launches = 0;
+
+  ~cjt_plan() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    for (void* p : ws_allocs) cudaFree(p);
+    for (void* p : allocs) cudaFree(p);
+    cudaSetDevice(cur);
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int dalloc(std::vector<void*>& list, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CJT_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) +
+                                ") failed: " + cudaGetErrorString(e));
+  }
+  list.push_back(*p);
+  return CJT_OK;
+}
+
+template <typename T>
+int upload(std::vector<void*>& list, T** dst, const T* src, size_t count) {
+  void* p = nullptr;
+  if (int rc = dalloc(list, &p, count * sizeof(T))) return rc;
+  *dst = static_cast<T*>(p);
+  if (count) CJT_CUDA_TRY(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  return CJT_OK;
+}
+
+// exp(-2 pi i num / den), long-double accurate
+inline void unit_root(int64_t num, int64_t den, double* re, double* im) {
+  num %= den;
+  if (num < 0) num += den;
+  if (2 * num > den) num -= den;
+  const long double ang = -2.0L * 3.14159265358979323846264338327950288L * (long double)num / (long double)den;
+  *re = (double)cosl(ang);
+  *im = (double)sinl(ang);
+}
+
+int log2_exact(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return ((int64_t(1) << l) == v) ? l : -1;
+}
+
+int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
+  ChirpZDev cz{};
+  cz.p0 = d.p0;
+  cz.width = d.width;
+  cz.q0 = d.q0;
+  cz.count = d.count;
+  cz.length = d.length;
+  cz.m_count = d.m_count;
+  cz.accumulate = d.accumulate;
+  const int lg = log2_exact(d.length);
+  if (lg < 4 || lg > 26) return fail(CJT_EINVAL, "chirp-z length must be a power of two in [16, 2^26]");
+  if (d.width < 1 || d.count < 1 || d.width + d.count - 1 > d.length || d.m_count < 1)
+    return fail(CJT_EINVAL, "inconsistent chirp-z descriptor");
+  cz.log2len = lg;
+  const size_t nm = (size_t)d.m_count;
+  if (int rc = upload(P->allocs, const_cast<double2**>(&cz.pre),
+                      reinterpret_cast<const double2*>(d.pre), nm * d.width)) return rc;
+  if (int rc = upload(P->allocs, const_cast<double2**>(&cz.post),
+                      reinterpret_cast<const double2*>(d.post), nm * d.count)) return rc;
+  const double2* kh = reinterpret_cast<const double2*>(d.kernel_hat);
+  if (lg <= 13) {
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, (size_t)d.length)) return rc;
+  } else {
+    const int l2 = std::min(13, (lg + 1) / 2);
+    const int l1 = lg - l2;
+    cz.log1 = l1;
+    cz.log2 = l2;
+    const int64_t L1 = int64_t(1) << l1, L2 = int64_t(1) << l2;
+    std::vector<double2> perm((size_t)d.length);
+    for (int64_t k1 = 0; k1 < L1; ++k1)
+      for (int64_t k2 = 0; k2 < L2; ++k2) perm[(size_t)(k1 * L2 + k2)] = kh[k1 + L1 * k2];
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
+    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
+    std::vector<double2> hi((size_t)nhi), lo(4096);
+    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
+    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
+    P->scratch_elems_per_vec = std::max<int64_t>(P->scratch_elems_per_vec, d.length * d.m_count);
+  }
+  P->fft_points += 2.0 * d.m_count * (double)d.length * lg;
+  *out = cz;
+  return CJT_OK;
+}
+
+// Work lists depend on the batch size (split-K is sized to fill the GPU).
+int build_items(cjt_plan* P, int64_t batch) {
+  const int64_t nrows = P->nrows;
+  const int64_t ntiles = (nrows + FWD_ROWS - 1) / FWD_ROWS;
+  std::vector<int64_t> tile_max((size_t)ntiles, 0);
+  for (int64_t i = 0; i < nrows; ++i) {
+    const int64_t t = i / FWD_ROWS;
+    tile_max[t] = std::max(tile_max[t], P->h_cut[i]);
+  }
+  const int64_t target = 8 * 148;
+  if (P->direction == CJT_FORWARD) {
+    const int64_t nbt = (batch + FWD_VT - 1) / FWD_VT;
+    double total = 0.0;
+    int64_t mx = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+      total += (double)tile_max[t];
+      mx = std::max(mx, tile_max[t]);
+    }
+    int64_t seg = (int64_t)std::ceil(total * nbt / target);
+    seg = std::max<int64_t>(256, ((seg + CK - 1) / CK) * CK);
+    std::vector<FwdItem> items;
+    std::vector<int32_t> s0((size_t)ntiles), ns((size_t)ntiles);
+    int32_t slot = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+      s0[t] = slot;
+      const int64_t top = ((tile_max[t] + FWD_CH - 1) / FWD_CH) * FWD_CH;
+      int32_t cnt = 0;
+      for (int64_t nb = 0; nb < top; nb += seg) {
+        FwdItem it{};
+        it.row0 = (int32_t)(t * FWD_ROWS);
+        it.nrows = (int32_t)std::min<int64_t>(FWD_ROWS, nrows - t * FWD_ROWS);
+        it.n_begin = (int32_t)nb;
+        it.n_end = (int32_t)std::min(top, nb + seg);
+        it.slot = slot++;
+        items.push_back(it);
+        ++cnt;
+      }
+      ns[t] = cnt;
+    }
+    // heaviest items first so the tail of the grid is short
+    std::stable_sort(items.begin(), items.end(), [](const FwdItem& a, const FwdItem& b) {
+      return (a.n_end - a.n_begin) > (b.n_end - b.n_begin);
+    });
+    void* p;
+    if (int rc = dalloc(P->ws_allocs, &p, items.size() * sizeof(FwdItem))) return rc;
+    P->fitems = (FwdItem*)p;
+    CJT_CUDA_TRY(cudaMemcpy(p, items.data(), items.size() * sizeof(FwdItem), cudaMemcpyHostToDevice));
+    if (int rc = dalloc(P->ws_allocs, &p, s0.size() * 4)) return rc;
+    P->tile_slot0 = (int32_t*)p;
+    CJT_CUDA_TRY(cudaMemcpy(p, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = dalloc(P->ws_allocs, &p, ns.size() * 4)) return rc;
+    P->tile_nslot = (int32_t*)p;
+    CJT_CUDA_TRY(cudaMemcpy(p, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice));
+    P->n_fitems = (int64_t)items.size();
+    P->n_fslots = slot;
+  } else {
+    const int64_t ndeg = P->n + 1;
+    const int64_t nd = (ndeg + INV_DT - 1) / INV_DT;
+    const int64_t nbt = (batch + INV_VT - 1) / INV_VT;
+    std::vector<std::vector<int32_t>> active((size_t)nd);
+    int64_t total_active = 0;
+    for (int64_t d = 0; d < nd; ++d) {
+      for (int64_t t = 0; t < ntiles; ++t)
+        if (tile_max[t] > d * INV_DT) active[d].push_back((int32_t)t);
+      total_active += (int64_t)active[d].size();
+    }
+    int64_t cs = INT64_MAX;
+    if (nd * nbt < target) cs = std::max<int64_t>(1, (int64_t)std::ceil((double)total_active * nbt / target));
+    std::vector<InvItem> items;
+    std::vector<int32_t> ids, s0((size_t)nd), ns((size_t)nd);
+    int32_t slot = 0;
+    for (int64_t d = 0; d < nd; ++d) {
+      s0[d] = slot;
+      const int64_t na = (int64_t)active[d].size();
+      int32_t cnt = 0;
+      for (int64_t a = 0; a < na; a += cs) {
+        InvItem it{};
+        it.n0 = (int32_t)(d * INV_DT);
+        it.t_begin = (int32_t)ids.size();
+        const int64_t take = std::min(cs, na - a);
+        for (int64_t q = 0; q < take; ++q) ids.push_back(active[d][a + q]);
+        it.t_count = (int32_t)take;
+        it.slot = slot++;
+        items.push_back(it);
+        ++cnt;
+      }
+      ns[d] = cnt;
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const InvItem& a, const InvItem& b) { return a.t_count > b.t_count; });
+    void* p;
+    if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, items.size()) * sizeof(InvItem))) return rc;
+    P->iitems = (InvItem*)p;
+    if (!items.empty())
+      CJT_CUDA_TRY(cudaMemcpy(p, items.data(), items.size() * sizeof(InvItem), cudaMemcpyHostToDevice));
+    if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, ids.size()) * 4)) return rc;
+    P->tile_ids = (int32_t*)p;
+    if (!ids.empty()) CJT_CUDA_TRY(cudaMemcpy(p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = dalloc(P->ws_allocs, &p, s0.size() * 4)) return rc;
+    P->dt_slot0 = (int32_t*)p;
+    CJT_CUDA_TRY(cudaMemcpy(p, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = dalloc(P->ws_allocs, &p, ns.size() * 4)) return rc;
+    P->dt_nslot = (int32_t*)p;
+    CJT_CUDA_TRY(cudaMemcpy(p, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice));
+    P->n_iitems = (int64_t)items.size();
+    P->n_islots = slot;
+  }
+  return CJT_OK;
+}
+
+void free_workspace(cjt_plan* P) {
+  for (void* p : P->ws_allocs) cudaFree(p);
+  P->ws_allocs.clear();
+  P->reserved = 0;
+  P->workspace_bytes = 0;
+}
+
+int reserve(cjt_plan* P, int64_t batch) {
+  if (batch <= P->reserved) return CJT_OK;
+  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  free_workspace(P);
+  if (int rc = build_items(P, batch)) return rc;
+  void* p;
+  const int64_t G1 = P->G + 1, N1 = P->n + 1;
+  int64_t bytes = 0;
+  const int64_t part_elems = (P->direction == CJT_FORWARD) ? P->n_fslots * FWD_ROWS : P->n_islots * INV_DT;
+  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
+  P->part = (double*)p;
+  bytes += part_elems * batch * 8;
+  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
+  P->vals = (double*)p;
+  bytes += G1 * batch * 8;
+  if (P->direction == CJT_INVERSE && !P->blocks.empty()) {
+    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+    P->yacc = (double*)p;
+    bytes += N1 * batch * 8;
+  } else {
+    P->yacc = nullptr;
+  }
+  if (P->scratch_elems_per_vec > 0) {
+    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(P->scratch_elems_per_vec * batch) * 16)) return rc;
+    P->scratch = (double2*)p;
+    bytes += P->scratch_elems_per_vec * batch * 16;
+  }
+  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+  P->io_in = (double*)p;
+  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+  P->io_out = (double*)p;
+  bytes += 2 * N1 * batch * 8;
+  P->workspace_bytes = bytes;
+  P->reserved = batch;
+  return CJT_OK;
+}
+
+int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStream_t st) {
+  int launches = 0;
+  const int64_t N1 = P->n + 1, G1 = P->G + 1;
+  if (P->direction == CJT_FORWARD) {
+    if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
+                                    N1, batch, P->part, st)) return rc;
+    if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, P->part, P->vals,
+                                           G1, batch, st)) return rc;
+    launches += 2;
+    for (const ChirpZDev& cz : P->blocks)
+      if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+        return rc;
+    if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, st, &launches))
+      return rc;
+  } else {
+    if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+      return rc;
+    if (!P->blocks.empty()) {
+      CJT_CUDA_TRY(cudaMemsetAsync(P->yacc, 0, (size_t)(N1 * batch) * 8, st));
+      for (const ChirpZDev& cz : P->blocks)
+        if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, st, &launches))
+          return rc;
+    }
+    if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
+                                    P->vals, G1, batch, P->part, st)) return rc;
+    if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
+                                       batch, st)) return rc;
+    launches += 2;
+  }
+  P->last_launches = launches;
+  return CJT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cjt_version(void) { return 1; }
+
+const char* cjt_last_error(void) { return cjt::g_last_error.c_str(); }
+
+int cjt_device_count(int* count) {
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(CJT_ENODEV, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  return CJT_OK;
+}
+
+int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
+  if (!d || !out) return fail(CJT_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->direction != CJT_FORWARD && d->direction != CJT_INVERSE) return fail(CJT_EINVAL, "bad direction");
+  if (d->n < 1) return fail(CJT_EINVAL, "N must be >= 1");
+  const int64_t G = d->grid_n;
+  if (G != (d->direction == CJT_FORWARD ? d->n : 2 * d->n)) return fail(CJT_EINVAL, "grid_n inconsistent with direction");
+  int ndev = 0;
+  if (cjt_device_count(&ndev) || ndev == 0) return fail(CJT_ENODEV, "no CUDA device visible");
+  std::unique_ptr<cjt_plan> P(new cjt_plan());
+  CJT_CUDA_TRY(cudaGetDevice(&P->device));
+  P->direction = d->direction;
+  P->m_terms = d->m_terms;
+  P->n = d->n;
+  P->G = G;
+  P->nrows = G + 1;
+  const int64_t nr = P->nrows;
+
+  P->h_cut.assign(d->cuts, d->cuts + nr);
+  int64_t maxcut = 0;
+  for (int64_t i = 0; i < nr; ++i) {
+    if (P->h_cut[i] < 0) return fail(CJT_EINVAL, "negative cut");
+    maxcut = std::max(maxcut, P->h_cut[i]);
+    P->rec_steps += P->h_cut[i];
+  }
+  if (d->table_len < maxcut + 1) return fail(CJT_EINVAL, "recurrence tables shorter than max cut + 1");
+
+  auto& A = P->allocs;
+  double *x, *xm;
+  int8_t* reg;
+  int64_t* cut;
+  if (int rc = upload(A, &x, d->x, nr)) return rc;
+  if (int rc = upload(A, &xm, d->xm, nr)) return rc;
+  if (int rc = upload(A, &reg, d->regions, nr)) return rc;
+  if (int rc = upload(A, &cut, d->cuts, nr)) return rc;
+  P->rows = RecRowsDev{x, xm, reg, cut, nr};
+  const size_t tl = (size_t)d->table_len;
+  double* t[7];
+  const double* src[7] = {d->A, d->B, d->C, d->rf_plus, d->rf_minus, d->rf_plus_inv, d->rf_minus_inv};
+  for (int k = 0; k < 7; ++k)
+    if (int rc = upload(A, &t[k], src[k], tl)) return rc;
+  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6]};
+
+  // recurrence checkpoints every CK degrees
+  std::vector<int64_t> off((size_t)nr);
+  int64_t tot = 0;
+  for (int64_t i = 0; i < nr; ++i) {
+    off[i] = tot;
+    const int64_t c = P->h_cut[i];
+    tot += (c >= 1) ? (c - 1) / CK : 0;
+  }
+  P->ck_count = tot;
+  if (int rc = upload(A, &P->ck_off, off.data(), off.size())) return rc;
+  void* p;
+  if (int rc = dalloc(A, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
+  P->ck = (double2*)p;
+  if (tot > 0) {
+    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, 0)) return rc;
+  }
+
+  // FFT twiddles exp(-2 pi i u / 8192)
+  std::vector<double2> tw(8192);
+  for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
+  if (int rc = upload(A, &P->tw8192, tw.data(), tw.size())) return rc;
+
+  for (int k = 0; k < d->n_blocks; ++k) {
+    ChirpZDev cz{};
+    if (int rc = build_chirpz(P.get(), d->blocks[k], &cz)) return rc;
+    P->blocks.push_back(cz);
+  }
+  if (int rc = build_chirpz(P.get(), d->edge, &P->edge)) return rc;
+  P->has_edge = true;
+  if (d->direction == CJT_INVERSE) {
+    if (!d->scalings) return fail(CJT_EINVAL, "inverse plan requires scalings");
+    if (int rc = upload(A, &P->scal, d->scalings, (size_t)(d->n + 1))) return rc;
+  }
+  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  *out = P.release();
+  return CJT_OK;
+}
+
+int cjt_plan_destroy(cjt_plan* plan) {
+  if (!plan) return CJT_OK;
+  cudaDeviceSynchronize();
+  delete plan;
+  return CJT_OK;
+}
+
+int cjt_plan_reserve(cjt_plan* plan, int64_t max_batch) {
+  if (!plan) return fail(CJT_EINVAL, "null plan");
+  if (max_batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
+  DeviceGuard g(plan->device);
+  return reserve(plan, max_batch);
+}
+
+int cjt_plan_stats_get(const cjt_plan* plan, cjt_plan_stats* s) {
+  if (!plan || !s) return fail(CJT_EINVAL, "null argument");
+  std::memset(s, 0, sizeof(*s));
+  s->launches_per_execute = plan->last_launches;
+  s->rec_steps = plan->rec_steps;
+  s->checkpoint_bytes = plan->ck_count * 16;
+  s->workspace_bytes = plan->workspace_bytes;
+  s->reserved_batch = plan->reserved;
+  s->rec_flops_per_vector = 2.0 * (double)plan->rec_steps;
+  s->fft_points_per_vector = plan->fft_points;
+  return CJT_OK;
+}
+
+int cjt_execute(cjt_plan* plan, const double* in, double* out, int64_t batch, void* stream) {
+  if (!plan || !in || !out) return fail(CJT_EINVAL, "null argument");
+  if (batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
+  DeviceGuard g(plan->device);
+  if (int rc = reserve(plan, batch)) return rc;
+  return execute(plan, in, out, batch, (cudaStream_t)stream);
+}
+
+int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, int64_t batch,
+                     void* stream) {
+  if (!plan || !in_host || !out_host) return fail(CJT_EINVAL, "null argument");
+  if (batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
+  DeviceGuard g(plan->device);
+  if (int rc = reserve(plan, batch)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)(batch * (plan->n + 1)) * 8;
+  CJT_CUDA_TRY(cudaMemcpyAsync(plan->io_in, in_host, bytes, cudaMemcpyHostToDevice, st));
+  if (int rc = execute(plan, plan->io_in, plan->io_out, batch, st)) return rc;
+  CJT_CUDA_TRY(cudaMemcpyAsync(out_host, plan->io_out, bytes, cudaMemcpyDeviceToHost, st));
+  CJT_CUDA_TRY(cudaStreamSynchronize(st));
+  return CJT_OK;
+}
+
+int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n, double* x, double* xm) {
+  if (n < 0 || (n > 0 && (!thetas || !regions || !x || !xm))) return fail(CJT_EINVAL, "null argument");
+  for (int64_t i = 0; i < n; ++i) {
+    const double th = thetas[i];
+    x[i] = cos(th);
+    if (regions[i] == 1) {
+      const double h = sin(0.5 * th);
+      xm[i] = -2.0 * h * h;
+    } else if (regions[i] == -1) {
+      const double h = cos(0.5 * th);
+      xm[i] = 2.0 * h * h;
+    } else {
+      xm[i] = 0.0;
+    }
+  }
+  return CJT_OK;
+}
+
+int cjt_clenshaw_points(const double* A, const double* B, const double* C, const double* rb_plus,
+                        const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
+                        const double* coeffs, int64_t n_coeffs, const double* thetas,
+                        const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points) {
+  if (n_points < 0 || n_coeffs < 0) return fail(CJT_EINVAL, "negative size");
+  if (n_points == 0) return CJT_OK;
+  int64_t maxcut = 0;
+  for (int64_t i = 0; i < n_points; ++i) maxcut = std::max(maxcut, cuts[i]);
+  if (maxcut > n_coeffs) return fail(CJT_EINVAL, "cut exceeds the coefficient count");
+  const size_t tl = (size_t)maxcut + 1;  // C[n+1] is read up to n = maxcut-1
+  std::vector<double> x((size_t)n_points), xm((size_t)n_points);
+  cjt_host_angles(thetas, regions, n_points, x.data(), xm.data());
+  std::vector<void*> tmp;
+  struct Free {
+    std::vector<void*>* v;
+    ~Free() { for (void* p : *v) cudaFree(p); }
+  } fr{&tmp};
+  double *dA, *dB, *dC, *rbp, *rbm, *rbpi, *rbmi, *dc, *dx, *dxm, *dout;
+  int8_t* dreg;
+  int64_t* dcut;
+  const double* srcs[7] = {A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv};
+  double** dsts[7] = {&dA, &dB, &dC, &rbp, &rbm, &rbpi, &rbmi};
+  for (int k = 0; k < 7; ++k)
+    if (int rc = upload(tmp, dsts[k], srcs[k], tl)) return rc;
+  if (int rc = upload(tmp, &dc, coeffs, (size_t)std::max<int64_t>(n_coeffs, 1))) return rc;
+  if (int rc = upload(tmp, &dx, x.data(), x.size())) return rc;
+  if (int rc = upload(tmp, &dxm, xm.data(), xm.size())) return rc;
+  if (int rc = upload(tmp, &dreg, regions, (size_t)n_points)) return rc;
+  if (int rc = upload(tmp, &dcut, cuts, (size_t)n_points)) return rc;
+  void* p;
+  if (int rc = dalloc(tmp, &p, (size_t)n_points * 8)) return rc;
+  dout = (double*)p;
+  RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr};
+  if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, dx, dxm, dreg, dcut, dout, n_points, 0))
+    return rc;
+  CJT_CUDA_TRY(cudaMemcpy(out, dout, (size_t)n_points * 8, cudaMemcpyDeviceToHost));
+  return CJT_OK;
+}
+
+int cjt_transpose_accumulate(const double* A, const double* B, const double* C, const double* rf_plus,
+                             const double* rf_minus, const double* rf_plus_inv,
+                             const double* rf_minus_inv, const double* wv, const double* thetas,
+                             const int64_t* cuts, const int8_t* regions, double* out, int64_t n_out,
+                             int64_t n_points, int64_t table_len) {
+  if (n_points < 0 || n_out < 0) return fail(CJT_EINVAL, "negative size");
+  if (n_points == 0) return CJT_OK;
+  int64_t maxcut = 0;
+  for (int64_t i = 0; i < n_points; ++i) maxcut = std::max(maxcut, cuts[i]);
+  if (maxcut > n_out) return fail(CJT_EINVAL, "cut exceeds the output length");
+  if (table_len < maxcut) return fail(CJT_EINVAL, "tables shorter than the largest cut");
+  // a single-vector plan over the caller's rows: degrees 0..maxcut-1
+  std::unique_ptr<cjt_plan> P(new cjt_plan());
+  CJT_CUDA_TRY(cudaGetDevice(&P->device));
+  P->direction = CJT_INVERSE;
+  P->n = std::max<int64_t>(maxcut, 1) - 1;
+  P->G = n_points - 1;
+  P->nrows = n_points;
+  P->h_cut.assign(cuts, cuts + n_points);
+  std::vector<double> x((size_t)n_points), xm((size_t)n_points);
+  cjt_host_angles(thetas, regions, n_points, x.data(), xm.data());
+  auto& Al = P->allocs;
+  double *dx, *dxm;
+  int8_t* dreg;
+  int64_t* dcut;
+  if (int rc = upload(Al, &dx, x.data(), x.size())) return rc;
+  if (int rc = upload(Al, &dxm, xm.data(), xm.size())) return rc;
+  if (int rc = upload(Al, &dreg, regions, (size_t)n_points)) return rc;
+  if (int rc = upload(Al, &dcut, cuts, (size_t)n_points)) return rc;
+  P->rows = RecRowsDev{dx, dxm, dreg, dcut, n_points};
+  const size_t tl = (size_t)std::max<int64_t>(maxcut, 1);
+  double* t[7];
+  const double* src[7] = {A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv};
+  for (int k = 0; k < 7; ++k)
+    if (int rc = upload(Al, &t[k], src[k], tl)) return rc;
+  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6]};
+  std::vector<int64_t> off((size_t)n_points);
+  int64_t tot = 0;
+  for (int64_t i = 0; i < n_points; ++i) {
+    off[i] = tot;
+    tot += (cuts[i] >= 1) ? (cuts[i] - 1) / CK : 0;
+  }
+  if (int rc = upload(Al, &P->ck_off, off.data(), off.size())) return rc;
+  void* p;
+  if (int rc = dalloc(Al, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
+  P->ck = (double2*)p;
+  if (tot > 0)
+    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, 0)) return rc;
+  if (int rc = reserve(P.get(), 1)) return rc;
+  std::vector<double> ones((size_t)(P->n + 1), 1.0);
+  double *dscal, *dwv, *dres;
+  if (int rc = upload(Al, &dscal, ones.data(), ones.size())) return rc;
+  if (int rc = upload(Al, &dwv, wv, (size_t)n_points)) return rc;
+  if (int rc = dalloc(Al, &p, ones.size() * 8)) return rc;
+  dres = (double*)p;
+  if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
+                                  dwv, n_points, 1, P->part, 0)) return rc;
+  if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, P->part, nullptr, dscal, dres,
+                                     P->n + 1, 1, 0)) return rc;
+  std::vector<double> res(ones.size());
+  CJT_CUDA_TRY(cudaMemcpy(res.data(), dres, res.size() * 8, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k <= P->n && k < n_out; ++k) out[k] += res[k];
+  return CJT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+// Internal definitions shared by the CJT CUDA translation units (sm_100a).
+//
+// Data layout in HBM (all float64):
+//   coefficient batches   [batch][N+1]            row-major, one vector per row
+//   Lobatto values        [batch][G+1]
+//   chirp-z scratch       [batch][m][L] complex    (multi-pass Bluestein only)
+//   recurrence partials   [slot][batch][tile]      (deterministic split-K)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cjt.h"
+
+namespace cjt {
+
+// ---------------------------------------------------------------------------
+// errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+#define CJT_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t err__ = (expr);                                                   \
+    if (err__ != cudaSuccess)                                                     \
+      return ::cjt::fail(CJT_ECUDA, std::string(#expr " failed: ") +              \
+                                        cudaGetErrorString(err__));               \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// complex helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * (DIR * i): DIR = -1 -> a * (-i), DIR = +1 -> a * i
+template <int DIR>
+__device__ __forceinline__ double2 cmul_i(double2 a) {
+  return DIR < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+// padded shared-memory index: one slot of padding every 16 complex elements,
+// which makes the stride-16 write of the first radix-16 pass conflict-free
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int l) { return l + l / 16; }
+
+// ---------------------------------------------------------------------------
+// in-register DFT of size R (2, 4, 8, 16), natural order in and out,
+// X_k = sum_j v_j exp(DIR 2 pi i j k / R)
+
+__device__ __forceinline__ double cos16(int j) {
+  switch (j & 15) {
+    case 0: return 1.0;
+    case 1: return 0.92387953251128675613;
+    case 2: return 0.70710678118654752440;
+    case 3: return 0.38268343236508977173;
+    case 4: return 0.0;
+    case 5: return -0.38268343236508977173;
+    case 6: return -0.70710678118654752440;
+    case 7: return -0.92387953251128675613;
+    case 8: return -1.0;
+    case 9: return -0.92387953251128675613;
+    case 10: return -0.70710678118654752440;
+    case 11: return -0.38268343236508977173;
+    case 12: return 0.0;
+    case 13: return 0.38268343236508977173;
+    case 14: return 0.70710678118654752440;
+    default: return 0.92387953251128675613;
+  }
+}
+__device__ __forceinline__ double sin16(int j) { return cos16(j - 4); }
+
+// b * exp(DIR 2 pi i k / SZ), compile-time K and SZ after unrolling
+template <int DIR, int K, int SZ>
+__device__ __forceinline__ double2 twiddle_const(double2 b) {
+  if constexpr (K == 0) {
+    return b;
+  } else if constexpr (4 * K == SZ) {
+    return cmul_i<DIR>(b);
+  } else {
+    constexpr int J = K * (16 / SZ);
+    const double c = cos16(J);
+    const double s = DIR * sin16(J);
+    return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));
+  }
+}
+
+__host__ __device__ constexpr int bitrev(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+template <int DIR, int SZ, int ST, int K, int R>
+__device__ __forceinline__ void dft_stage_k(double2* v) {
+  if constexpr (K < SZ / 2) {
+    double2 a = v[ST + K];
+    double2 b = twiddle_const<DIR, K, SZ>(v[ST + K + SZ / 2]);
+    v[ST + K] = cadd(a, b);
+    v[ST + K + SZ / 2] = csub(a, b);
+    dft_stage_k<DIR, SZ, ST, K + 1, R>(v);
+  }
+}
+template <int DIR, int SZ, int ST, int R>
+__device__ __forceinline__ void dft_stage(double2* v) {
+  if constexpr (ST < R) {
+    dft_stage_k<DIR, SZ, ST, 0, R>(v);
+    dft_stage<DIR, SZ, ST + SZ, R>(v);
+  }
+}
+template <int DIR, int SZ, int R>
+__device__ __forceinline__ void dft_levels(double2* v) {
+  if constexpr (SZ <= R) {
+    dft_stage<DIR, SZ, 0, R>(v);
+    dft_levels<DIR, SZ * 2, R>(v);
+  }
+}
+template <int R, int DIR>
+__device__ __forceinline__ void dft_reg(double2* v) {
+  constexpr int BITS = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : 4;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int j = bitrev(i, BITS);
+    if (j > i) {
+      double2 t = v[i];
+      v[i] = v[j];
+      v[j] = t;
+    }
+  }
+  dft_levels<DIR, 2, R>(v);
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory Stockham FFT of length L = 2^LOGL (4 <= LOGL <= 13), executed
+// by the L/16 threads t of one group (each holds 16 elements per pass; radix
+// 16 passes, the last pass radix 2/4/8/16).  `tw` is the 8192-entry table
+// exp(-2 pi i u / 8192).  Every thread of the CTA must call it with the same
+// LOGL (it synchronises the CTA between passes).  Result in natural order.
+template <int LOGL, int DIR, int PASS>
+__device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __restrict__ tw) {
+  constexpr int NP = (LOGL + 3) / 4;
+  if constexpr (PASS < NP) {
+    constexpr int LR = (PASS < NP - 1) ? 4 : (LOGL - 4 * (NP - 1));
+    constexpr int R = 1 << LR;
+    constexpr int L = 1 << LOGL;
+    constexpr int LNS = 4 * PASS;
+    constexpr int NS = 1 << LNS;
+    constexpr int NBF = 16 / R;
+    constexpr int STRIDE = L / R;
+    constexpr int TPG = L / 16;
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < NBF; ++q) {
+      const int j = t + q * TPG;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q * R + r] = s[pad16(j + r * STRIDE)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NBF; ++q) {
+      const int j = t + q * TPG;
+      const int k = j & (NS - 1);
+      if constexpr (PASS > 0) {
+        constexpr int SH = 13 - (LNS + LR);
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          double2 w = __ldg(&tw[(r * k) << SH]);
+          if (DIR > 0) w.y = -w.y;
+          v[q * R + r] = cmul(v[q * R + r], w);
+        }
+      }
+      dft_reg<R, DIR>(&v[q * R]);
+      const int base = ((j - k) << LR) + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[pad16(base + r * NS)] = v[q * R + r];
+    }
+    __syncthreads();
+    fft_pass<LOGL, DIR, PASS + 1>(s, t, tw);
+  }
+}
+
+template <int LOGL, int DIR>
+__device__ __forceinline__ void fft_smem(double2* s, int t, const double2* __restrict__ tw) {
+  static_assert(LOGL >= 4 && LOGL <= 13, "smem FFT length out of range");
+  fft_pass<LOGL, DIR, 0>(s, t, tw);
+}
+
+// ---------------------------------------------------------------------------
+// device-side descriptors
+
+struct ChirpZDev {
+  int64_t p0, width, q0, count, length;
+  int32_t m_count, accumulate;
+  int32_t log2len, log1, log2;   // multipass split L = L1 * L2 (log1 + log2 = log2len)
+  const double2* pre;       // [m][width]
+  const double2* post;      // [m][count]
+  const double2* khat;      // fused: natural order; multipass: [k1][k2] = khat[k1 + L1 k2]
+  const double2* tw_hi;     // multipass: exp(-2 pi i (a 4096) / L)
+  const double2* tw_lo;     // multipass: exp(-2 pi i b / L), b < 4096
+};
+
+struct RecRowsDev {
+  const double* x;
+  const double* xm;
+  const int8_t* reg;
+  const int64_t* cut;
+  int64_t nrows;
+};
+
+struct RecTablesDev {
+  const double *A, *B, *C, *rfp, *rfm, *rfpi, *rfmi;
+};
+
+// forward split-K work item: rows [row0, row0+nrows) x degrees [n_begin, n_end)
+struct FwdItem {
+  int32_t row0, nrows, n_begin, n_end, slot, pad;
+};
+// inverse work item: degrees [n0, n0+64) x row tiles tile_ids[t_begin .. t_begin+t_count)
+struct InvItem {
+  int32_t n0, t_begin, t_count, slot;
+};
+
+constexpr int CK = 32;          // recurrence checkpoint spacing (degrees)
+constexpr int FWD_ROWS = 128;   // rows per forward tile (4 warps x 32 lanes)
+constexpr int FWD_VT = 32;      // vectors per forward CTA
+constexpr int FWD_CH = 32;      // degrees per staged coefficient chunk
+constexpr int INV_DT = 64;      // degrees per inverse tile
+constexpr int INV_VT = 64;      // vectors per inverse tile
+constexpr int INV_RT = 128;     // rows per inverse stage
+
+// ---------------------------------------------------------------------------
+// launchers (host)
+int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
+                  double* out, int64_t ldo, int64_t batch, double2* scratch,
+                  cudaStream_t st, int* launches);
+
+int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
+                       double2* ck, cudaStream_t st);
+int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
+                       const double2* ck, const FwdItem* items, int64_t n_items,
+                       const double* c, int64_t ldc, int64_t ncoef, int64_t batch,
+                       double* part, cudaStream_t st);
+int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nslot,
+                              int64_t nrows, const double* part, double* vals, int64_t ldv,
+                              int64_t batch, cudaStream_t st);
+int launch_rec_inverse(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
+                       const double2* ck, const InvItem* items, int64_t n_items,
+                       const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch,
+                       double* part, cudaStream_t st);
+int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,
+                          const double* part, const double* blocks_acc, const double* scal,
+                          double* out, int64_t ldo, int64_t batch, cudaStream_t st);
+int launch_clenshaw_points(const RecTablesDev& tab, const double* rbp, const double* rbm,
+                           const double* rbpi, const double* rbmi, const double* coeffs,
+                           const double* x, const double* xm, const int8_t* reg,
+                           const int64_t* cut, double* out, int64_t npts, cudaStream_t st);
+
+}  // namespace cjt

@@ -1,0 +1,640 @@
+"""Host-side planning for the B200 Chebyshev-Jacobi transform.
+
+Everything here runs once per plan on the host and produces the read-only
+tables the device executes against.  The numerics follow the reference
+package ``chebjac`` operation-for-operation wherever the device result depends
+on the exact bits (grid angles, region codes, partition, recurrence tables,
+asymptotic coefficients, modulation functions, quadrature weights,
+orthonormality constants), so a plan built here describes exactly the
+reference's transform:
+
+  * angle grid           chebjac/recurrences.py:48-66
+  * region classifier    chebjac/recurrences.py:24-45
+  * Stirling factors     chebjac/kernels.py:20-106
+  * recurrence tables    chebjac/kernels.py:336-364
+  * C_{n,m}              chebjac/kernels.py:186-252
+  * 1/A_n                chebjac/kernels.py:255-307
+  * modulation u_m, v_m  chebjac/asymptotics.py:22-75
+  * envelope g_m, n_M    chebjac/asymptotics.py:86-138
+  * partition            chebjac/asymptotics.py:147-255
+  * moments, CC weights  chebjac/quadrature.py:35-78
+
+On top of that the planner lays every trigonometric transform of the
+reference execution (engine.py:163-227, trig.py:35-63) out as a *chirp-z*
+problem with power-of-two cyclic length: for input indices p in [p0, p0+W)
+and output indices q in [q0, q0+R),
+
+    z_q = sum_p x_p exp(i pi p q / G)
+        = chirp(q) * sum_p (x_p chirp(p)) * conj(chirp(q - p)),
+    chirp(k) = exp(i pi k^2 / (2G)),
+
+so every DCT-I / bordered DST-I of the reference becomes one real part of a
+Bluestein convolution whose diagonal scalings (C_{n,m}, u_m - i v_m, the
+Clenshaw-Curtis weights, the analysis 2/G) are folded into per-plan complex
+pre/post tables.  G = 2^k - 1 and 2G = 2(2^k - 1) have large prime factors
+(8191 is prime), so the power-of-two Bluestein length keeps one FFT code path
+for every configuration.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.fft
+
+DEFAULT_M = 7
+DEFAULT_EPS = float(np.finfo(np.float64).eps)
+
+# region codes (chebjac/recurrences.py:27-29)
+INTERIOR = 0
+NEAR_PLUS_ONE = 1
+NEAR_MINUS_ONE = -1
+BREAK_LO = 0.25 * math.pi
+BREAK_HI = 0.75 * math.pi
+
+
+class ParameterRangeError(ValueError):
+    """(alpha, beta) outside the range an operation supports
+    (chebjac/parameters.py:6)."""
+
+
+@dataclass(frozen=True)
+class JacobiParameters:
+    """Weight exponents (alpha, beta); alpha, beta > -1 (parameters.py:11-44)."""
+
+    alpha: float
+    beta: float
+
+    def __post_init__(self):
+        if not (self.alpha > -1.0 and self.beta > -1.0):
+            raise ParameterRangeError(
+                f"Jacobi parameters require alpha, beta > -1, got ({self.alpha}, {self.beta})")
+
+    @property
+    def core(self) -> bool:
+        return (-0.5 < self.alpha <= 0.5) and (-0.5 < self.beta <= 0.5)
+
+    def swapped(self) -> "JacobiParameters":
+        return JacobiParameters(self.beta, self.alpha)
+
+    def require_core(self, context: str = "this operation"):
+        if not self.core:
+            raise ParameterRangeError(
+                f"{context} requires (alpha, beta) in (-1/2, 1/2]^2, got "
+                f"({self.alpha}, {self.beta}); reduce the parameters with "
+                f"integer increments/decrements first")
+
+
+# ---------------------------------------------------------------------------
+# Stirling series (kernels.py:20-106).  Coefficients are exact rationals of the
+# classical numerator/denominator sequences, rounded once.
+_STIRLING_NUM_DEN = (
+    (1, 1), (1, 12), (1, 288), (-139, 51840), (-571, 2488320),
+    (163879, 209018880), (5246819, 75246796800), (-534703531, 902961561600),
+    (-4483131259, 86684309913600), (432261921612371, 514904800886784000),
+    (6232523202521089, 86504006548979712000),
+    (-25834629665134204969, 13494625021640835072000),
+    (-1579029138854919086429, 9716130015581401251840000),
+    (746590869962651602203151, 116593560186976815022080000),
+    (1511513601028097903631961, 2798245444487443560529920000),
+    (-8849272268392873147705987190261, 299692087104605205332754432000000),
+    (-142801712490607530608130701097701, 57540880724084199423888850944000000),
+)
+STIRLING = tuple(num / den for num, den in _STIRLING_NUM_DEN)
+# smallest z for which k terms reach eps/20 (kernels.py:46-61), ascending in z
+_STIRLING_CUTS = np.array([9.0, 10.0, 11.0, 12.0, 14.0, 17.0, 20.0, 26.0, 35.0, 53.0,
+                           92.0, 196.0, 591.0, 3275.0])
+_STIRLING_TERMS = np.array([17, 16, 15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4], dtype=np.int64)
+
+
+def stirling_series(z):
+    """S(z) = Gamma(z) e^z z^(1/2-z) / sqrt(2 pi), truncated per argument."""
+    z = np.asarray(z, dtype=float)
+    if np.any(z < 9.0):
+        raise ValueError("Stirling series requires z >= 9")
+    terms = _STIRLING_TERMS[np.searchsorted(_STIRLING_CUTS, z, side="right") - 1]
+    res = np.empty_like(z)
+    for k in np.unique(terms):
+        pick = terms == k
+        zz = z[pick]
+        horner = np.zeros_like(zz)
+        for j in range(k - 1, 0, -1):
+            horner = (horner + STIRLING[j]) / zz
+        res[pick] = horner + 1.0
+    return res
+
+
+def _pow1p(x, y):
+    # (1+x)^y as exp(y log1p x) (kernels.py:118-119)
+    return np.exp(y * np.log1p(x))
+
+
+# ---------------------------------------------------------------------------
+# C_{n,m} (kernels.py:186-252)
+
+def _cnm_switch(a: float, b: float) -> int:
+    lo = min(a, b)
+    return 8 + math.ceil(abs(lo)) if lo != 0.0 else 8
+
+
+def _cnm_stirling(a, b, n, m):
+    """Closed Stirling form of C_{n,m}; n scalar or array."""
+    d = 2.0 * n + (a + b) + m + 2.0
+    lead = math.exp(m) / (4.0**m * math.sqrt(math.pi))
+    f1 = _pow1p((a - b - m) / d, n + a + 0.5)
+    f2 = _pow1p((b - a - m) / d, n + b + 0.5)
+    den = np.power(np.asarray(n, dtype=float), m + 0.5) * _pow1p(
+        ((a + b) + m + 2.0) / (2.0 * n), m + 0.5)
+    ratio = (stirling_series(n + a + 1.0) * stirling_series(n + b + 1.0)
+             / stirling_series(2.0 * n + m + (a + b) + 2.0))
+    return lead * f1 * f2 / den * ratio
+
+
+def cnm_scalar(p: JacobiParameters, n: int, m: int) -> float:
+    """C_{n,m} at one degree (kernels.py:210-228)."""
+    if n < 0 or m < 0:
+        raise ValueError("n and m must be nonnegative")
+    a, b = p.alpha, p.beta
+    if n + min(a, b) >= 8.0:
+        return float(_cnm_stirling(a, b, n, m))
+    n0 = _cnm_switch(a, b)
+    val = float(_cnm_stirling(a, b, n0, m))
+    s = a + b
+    for k in range(n0, n, -1):
+        val *= (k + (s + m + 1) / 2) * (k + (s + m) / 2) / ((k + a) * (k + b))
+    return val
+
+
+def cnm_table(p: JacobiParameters, nmax: int, m_count: int) -> np.ndarray:
+    """C_{n,m}, n = 0..nmax, m < m_count, shape (nmax+1, m_count)
+    (kernels.py:231-252)."""
+    a, b = p.alpha, p.beta
+    s = a + b
+    n0 = min(_cnm_switch(a, b), nmax)
+    col = np.empty(nmax + 1)
+    if n0 < nmax or n0 + min(a, b) >= 8.0:
+        col[n0:] = _cnm_stirling(a, b, np.arange(n0, nmax + 1, dtype=float), 0)
+    else:
+        col[n0] = cnm_scalar(p, n0, 0)
+    for k in range(n0, 0, -1):
+        col[k - 1] = col[k] * (k + (s + 1) / 2) * (k + s / 2) / ((k + a) * (k + b))
+    out = np.empty((nmax + 1, m_count))
+    out[:, 0] = col
+    deg = np.arange(nmax + 1, dtype=float)
+    for m in range(1, m_count):
+        out[:, m] = out[:, m - 1] / (2.0 * (2.0 * deg + s + m + 1.0))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# A_n (kernels.py:255-307)
+
+def _an_direct(a, b, n):
+    g = math.gamma(n + a + 1.0) * math.gamma(n + b + 1.0)
+    return (2.0 ** ((a + b) + 1.0) * g
+            / ((2.0 * n + (a + b) + 1.0) * math.gamma(n + (a + b) + 1.0) * math.gamma(n + 1.0)))
+
+
+def _an_stirling(a, b, n):
+    n = np.asarray(n, dtype=float)
+    front = 2.0 ** ((a + b) + 1.0) / (2.0 * n + (a + b) + 1.0)
+    g1 = _pow1p(-b / (n + (a + b) + 1.0), n / 2 + a + 0.25) * _pow1p(
+        -a / (n + (a + b) + 1.0), n / 2 + b + 0.25)
+    g2 = _pow1p(a / (n + 1.0), n / 2 + 0.25) * _pow1p(b / (n + 1.0), n / 2 + 0.25)
+    rat = (stirling_series(n + a + 1.0) * stirling_series(n + b + 1.0)
+           / (stirling_series(n + (a + b) + 1.0) * stirling_series(n + 1.0)))
+    return front * g1 * g2 * rat
+
+
+def orthonormality(p: JacobiParameters, nmax: int) -> np.ndarray:
+    """A_n = ||P_n||^2 for n = 0..nmax (kernels.py:298-307)."""
+    a, b = p.alpha, p.beta
+    lo = min(a, b, a + b, 0.0)
+    switch = 8 + math.ceil(-lo) if lo < 0.0 else 8
+    n0 = min(switch, nmax + 1)
+    out = np.empty(nmax + 1)
+    for n in range(n0):
+        out[n] = _an_direct(a, b, n)
+    if n0 <= nmax:
+        out[n0:] = _an_stirling(a, b, np.arange(n0, nmax + 1))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Recurrence tables (kernels.py:336-364)
+
+@dataclass(frozen=True)
+class RecurrenceTables:
+    A: np.ndarray
+    B: np.ndarray
+    C: np.ndarray
+    rf_plus: np.ndarray
+    rf_minus: np.ndarray
+    rb_plus: np.ndarray
+    rb_minus: np.ndarray
+    rf_plus_inv: np.ndarray
+    rf_minus_inv: np.ndarray
+    rb_plus_inv: np.ndarray
+    rb_minus_inv: np.ndarray
+
+
+def recurrence_tables(p: JacobiParameters, nmax: int) -> RecurrenceTables:
+    a, b = p.alpha, p.beta
+    s = a + b
+    deg = np.arange(nmax + 1, dtype=float)
+    t = 2.0 * deg + s
+    den = 2.0 * (deg + 1.0) * (deg + s + 1.0)
+    A = (t + 1.0) * (t + 2.0) / den
+    with np.errstate(divide="ignore", invalid="ignore"):
+        B = (a - b) * (a + b) * (t + 1.0) / (den * t)
+        C = 2.0 * (deg + a) * (deg + b) * (t + 2.0) / (den * t)
+    A[0] = s / 2 + 1.0
+    B[0] = (a - b) / 2
+    C[0] = 0.0
+    rfp = (deg + a + 1.0) / (deg + 1.0)
+    rfm = -(deg + b + 1.0) / (deg + 1.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        core = (deg + 1.0) * (s + deg + 1.0) * (s + 2.0 * deg) / (deg * (s + 2.0 * deg + 2.0))
+        rbp = core / (deg + b)
+        rbm = -core / (deg + a)
+    rbp[0] = rbm[0] = np.nan
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = [1.0 / v for v in (rfp, rfm, rbp, rbm)]
+    arrays = (A, B, C, rfp, rfm, rbp, rbm, *inv)
+    for arr in arrays:
+        arr.flags.writeable = False
+    return RecurrenceTables(*arrays)
+
+
+# ---------------------------------------------------------------------------
+# Grid and regions (recurrences.py:41-66)
+
+def angle_grid(g: int) -> np.ndarray:
+    if g < 1:
+        raise ValueError("grid parameter N must be >= 1")
+    th = np.pi * np.arange(g + 1) / g
+    th.flags.writeable = False
+    return th
+
+
+def region_codes(thetas: np.ndarray) -> np.ndarray:
+    reg = np.zeros(len(thetas), dtype=np.int8)
+    reg[thetas < BREAK_LO] = NEAR_PLUS_ONE
+    reg[thetas > BREAK_HI] = NEAR_MINUS_ONE
+    return reg
+
+
+# ---------------------------------------------------------------------------
+# Modulation / envelope (asymptotics.py:22-138)
+
+def _pair_weights(gamma: float, count: int) -> np.ndarray:
+    w = np.empty(count)
+    w[0] = 1.0
+    for l in range(1, count):
+        w[l] = w[l - 1] * (0.5 + gamma + l - 1) * (0.5 - gamma + l - 1) / l
+    return w
+
+
+def modulation(p: JacobiParameters, m_count: int, thetas: np.ndarray):
+    """u_m(theta), v_m(theta), shape (m_count, len(thetas))
+    (asymptotics.py:36-75)."""
+    a, b = p.alpha, p.beta
+    thetas = np.asarray(thetas, dtype=float)
+    sh = np.sin(0.5 * thetas)
+    ch = np.cos(0.5 * thetas)
+    wa = _pair_weights(a, m_count)
+    wb = _pair_weights(b, m_count)
+    phase = (a + b + 1.0) * 0.5 * thetas - (a + 0.5) * 0.5 * math.pi
+    re = np.cos(phase)
+    im = np.sin(phase)
+    u = np.empty((m_count, len(thetas)))
+    v = np.empty((m_count, len(thetas)))
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        scale0 = 1.0 / (sh ** (a + 0.5) * ch ** (b + 0.5))
+        for m in range(m_count):
+            cr, ci = re.copy(), im.copy()
+            scale = scale0 * ch ** (-float(m))
+            um = np.zeros(len(thetas))
+            vm = np.zeros(len(thetas))
+            for l in range(m + 1):
+                rho = wa[l] * wb[m - l]
+                if rho != 0.0:
+                    um += rho * cr * scale
+                    vm -= rho * ci * scale
+                if l < m:
+                    cr, ci = ci, -cr
+                    scale = scale * ch / sh
+            u[m] = um
+            v[m] = vm
+            re, im = re * ch - im * sh, re * sh + im * ch
+    return u, v
+
+
+def envelope(p: JacobiParameters, m: int, thetas: np.ndarray) -> np.ndarray:
+    """g_m over angles (asymptotics.py:86-103)."""
+    a, b = p.alpha, p.beta
+    thetas = np.asarray(thetas, dtype=float)
+    sh = np.sin(0.5 * thetas)
+    ch = np.cos(0.5 * thetas)
+    wa = _pair_weights(a, m + 1)
+    wb = _pair_weights(b, m + 1)
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        scale = 1.0 / (sh ** (a + 0.5) * ch ** (float(m) + b + 0.5))
+        g = np.zeros(len(thetas))
+        for l in range(m + 1):
+            w = wa[l] * wb[m - l]
+            if w != 0.0:
+                g += w * scale
+            if l < m:
+                scale = scale * ch / sh
+    return g
+
+
+def _degree_from_bound(g: float, m_terms: int, eps: float) -> int:
+    if g == 0.0:
+        return 0
+    val = (eps * 2.0 ** (2 * m_terms - 1) * math.sqrt(math.pi) / g) ** (-1.0 / (m_terms + 0.5))
+    return int(math.floor(val))
+
+
+def n_m(p: JacobiParameters, m_terms: int, eps: float) -> int:
+    """asymptotics.py:131-138"""
+    if m_terms < 2:
+        raise ValueError("M >= 2 required")
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    g = float(envelope(p, m_terms, np.array([0.5 * math.pi]))[0])
+    return _degree_from_bound(g, m_terms, eps)
+
+
+@dataclass(frozen=True)
+class Block:
+    j: int
+    i1: int
+    i2: int
+
+
+@dataclass(frozen=True)
+class Partition:
+    """Certified rectangles (asymptotics.py:156-200)."""
+
+    n: int
+    m_terms: int
+    eps: float
+    n_m: int
+    alpha_n: float
+    k: int
+    blocks: tuple
+    theta_bar_index: int
+
+    def column_strips(self):
+        out, top = [], self.n
+        for blk in self.blocks:
+            out.append((blk.j, top))
+            top = blk.j - 1
+        return out
+
+    def row_cuts(self) -> np.ndarray:
+        cuts = np.full(self.n + 1, self.n + 1, dtype=np.int64)
+        for blk in self.blocks:
+            cuts[blk.i1: blk.i2 + 1] = blk.j
+        return cuts
+
+
+def partition(p: JacobiParameters, g: int, m_terms: int, eps: float,
+              thetas: np.ndarray | None = None) -> Partition:
+    """asymptotics.py:203-255"""
+    p.require_core("partition construction")
+    if m_terms < 2:
+        raise ValueError("M >= 2 required")
+    if thetas is None:
+        thetas = angle_grid(g)
+    nm = n_m(p, m_terms, eps)
+    env = envelope(p, m_terms, thetas)
+    tbar = int(np.argmin(env))
+    if g <= nm:
+        return Partition(g, m_terms, eps, nm, 0.5, 0, (), tbar)
+    ratio = math.log(g / max(nm, 1))
+    alpha_n = min(1.0 / ratio, 0.5) if ratio > 0 else 0.5
+    blocks = []
+    lo_prev, hi_prev = 1, g - 1
+    k = 1
+    while True:
+        jk = int(math.floor(alpha_n ** k * g))
+        if jk <= nm or jk < 2:
+            break
+        bad = ~(2.0 * cnm_scalar(p, jk, m_terms) * env < eps)
+        if bad[tbar]:
+            break
+        left = bad[1:tbar][::-1]
+        i1 = tbar - (int(np.argmax(left)) if left.any() else left.size)
+        right = bad[tbar + 1: g]
+        i2 = tbar + (int(np.argmax(right)) if right.any() else right.size)
+        i1 = max(i1, lo_prev)
+        i2 = min(i2, hi_prev)
+        if not i1 < tbar < i2:
+            break
+        blocks.append(Block(jk, i1, i2))
+        lo_prev, hi_prev = i1, i2
+        k += 1
+    return Partition(g, m_terms, eps, nm, alpha_n, len(blocks), tuple(blocks), tbar)
+
+
+# ---------------------------------------------------------------------------
+# Quadrature (quadrature.py:35-78)
+
+def moments(p: JacobiParameters, g: int) -> np.ndarray:
+    p.require_core("the moment recurrence")
+    a, b = p.alpha, p.beta
+    s = a + b
+    mu = np.empty(g + 1)
+    mu[0] = 2.0 ** (s + 1.0) * math.gamma(a + 1.0) * math.gamma(b + 1.0) / math.gamma(s + 2.0)
+    if g >= 1:
+        mu[1] = (b - a) / (s + 2.0) * mu[0]
+    two_d = 2.0 * (a - b)
+    for k in range(1, g):
+        mu[k + 1] = -(two_d * mu[k] + (s - k + 2.0) * mu[k - 1]) / (s + k + 2.0)
+    return mu
+
+
+def dct1_host(x: np.ndarray) -> np.ndarray:
+    """sum_k cos(pi j k / G) x_k with the reference's staging (trig.py:35-40).
+    Plan-time only (quadrature weights)."""
+    st = np.array(x, dtype=float)
+    st[1:-1] *= 0.5
+    return scipy.fft.dct(st, type=1)
+
+
+def cc_weights(p: JacobiParameters, g: int, mu: np.ndarray) -> np.ndarray:
+    st = np.empty(g + 1)
+    st[0] = mu[0]
+    st[-1] = mu[g]
+    st[1:-1] = 2.0 * mu[1:g]
+    w = dct1_host(st)
+    w /= g
+    w[0] *= 0.5
+    w[-1] *= 0.5
+    return w
+
+
+# ---------------------------------------------------------------------------
+# Exact unit phases for the chirp-z layout
+
+_PI_LD = np.longdouble("3.14159265358979323846264338327950288419716939937510")
+
+
+def unit_phase(num, den: int) -> np.ndarray:
+    """exp(2 pi i num/den) for integer num, rounded from 80-bit extended."""
+    r = np.mod(np.asarray(num, dtype=np.int64), den)
+    r = np.where(2 * r > den, r - den, r).astype(np.longdouble)
+    ang = (2 * _PI_LD) * r / np.longdouble(den)
+    return np.cos(ang).astype(np.float64) + 1j * np.sin(ang).astype(np.float64)
+
+
+def chirp(k, g: int) -> np.ndarray:
+    """exp(i pi k^2 / (2G)) with k^2 reduced exactly mod 4G."""
+    k = np.asarray(k, dtype=np.int64)
+    return unit_phase(np.mod(k * k, 4 * g), 4 * g)
+
+
+def _next_pow2(v: int) -> int:
+    return 1 << max(4, int(v - 1).bit_length())
+
+
+@dataclass
+class ChirpZ:
+    """One batched chirp-z product with fused diagonal scalings:
+
+        out[b, q0+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
+        z_{b,m}[s] = sum_t exp(i pi (p0+t)(q0+s)/G) pre[m, t] x[b, p0+t].
+    """
+
+    g: int
+    p0: int
+    width: int
+    q0: int
+    count: int
+    length: int
+    pre: np.ndarray      # (M, width) complex128: scaling * chirp(p)
+    post: np.ndarray     # (M, count) complex128: scaling * chirp(q)
+    kernel_hat: np.ndarray  # (length,) complex128: FFT(conj chirp of q-p) / length
+    accumulate: bool
+
+    @property
+    def m_count(self) -> int:
+        return self.pre.shape[0]
+
+
+def chirpz(g: int, p0: int, width: int, q0: int, count: int,
+           pre_scale: np.ndarray, post_scale: np.ndarray, accumulate: bool) -> ChirpZ:
+    """Build the Bluestein layout of sum_p x_p e^{i pi p q/G}.
+    pre_scale/post_scale: (M, width)/(M, count) real or complex diagonals."""
+    length = _next_pow2(width + count - 1)
+    pidx = np.arange(p0, p0 + width, dtype=np.int64)
+    qidx = np.arange(q0, q0 + count, dtype=np.int64)
+    pre = np.atleast_2d(pre_scale) * chirp(pidx, g)[None, :]
+    post = np.atleast_2d(post_scale) * chirp(qidx, g)[None, :]
+    # kernel conj(chirp(d)), d = q - p = (q0 - p0) + s - t, cyclic over length
+    ker = np.zeros(length, dtype=np.complex128)
+    off = q0 - p0
+    ker[:count] = np.conj(chirp(off + np.arange(count, dtype=np.int64), g))
+    if width > 1:
+        ker[length - width + 1:] = np.conj(chirp(off - np.arange(width - 1, 0, -1, dtype=np.int64), g))
+    khat = np.fft.fft(ker) / length
+    return ChirpZ(g, p0, width, q0, count, length,
+                  np.ascontiguousarray(pre, dtype=np.complex128),
+                  np.ascontiguousarray(post, dtype=np.complex128),
+                  khat.astype(np.complex128), accumulate)
+
+
+# ---------------------------------------------------------------------------
+# Whole-plan host description
+
+
+@dataclass
+class HostPlan:
+    direction: str
+    p: JacobiParameters
+    n: int
+    m_terms: int
+    eps: float
+    grid_n: int
+    thetas: np.ndarray
+    regions: np.ndarray
+    cuts: np.ndarray
+    layout: Partition
+    tables: RecurrenceTables
+    rec_cuts: np.ndarray          # cuts capped to the degrees the transform keeps
+    blocks: list = field(default_factory=list)   # list[ChirpZ]
+    analysis: ChirpZ | None = None   # forward: Lobatto values -> Chebyshev coefficients
+    synthesis: ChirpZ | None = None  # inverse: Chebyshev coefficients -> weighted values
+    weights: np.ndarray | None = None
+    scalings: np.ndarray | None = None
+
+
+def build(direction: str, p: JacobiParameters, n: int,
+          m_terms: int = DEFAULT_M, eps: float = DEFAULT_EPS) -> HostPlan:
+    """Plan one direction (engine.py:96-130) and lay out its device work."""
+    if direction not in ("forward", "inverse"):
+        raise ValueError("direction must be 'forward' or 'inverse'")
+    p.require_core(f"the {direction} transform plan")
+    if n < 1:
+        raise ValueError("N must be >= 1")
+    if m_terms < 2:
+        raise ValueError("M >= 2 required")
+    g = n if direction == "forward" else 2 * n
+    th = angle_grid(g)
+    layout = partition(p, g, m_terms, eps, th)
+    tables = recurrence_tables(p, g + 1)
+    cuts = layout.row_cuts()
+    regions = region_codes(th)
+    cuts.flags.writeable = False
+    regions.flags.writeable = False
+    hp = HostPlan(direction, p, n, m_terms, eps, g, th, regions, cuts, layout, tables,
+                  np.minimum(cuts, n + 1))
+
+    if layout.blocks:
+        # engine.py:133-141: u, v with endpoint rows zeroed; C_{n,m} columns
+        u, v = modulation(p, m_terms, th)
+        u[:, 0] = u[:, -1] = 0.0
+        v[:, 0] = v[:, -1] = 0.0
+        ccols = cnm_table(p, g, m_terms)
+        w_uv = u - 1j * v
+        for (lo, hi), blk in zip(layout.column_strips(), layout.blocks):
+            rows = slice(blk.i1, blk.i2 + 1)
+            if direction == "forward":
+                # values[rows] += u_m DCT(C_m c)[rows] + v_m DST(C_m c)[rows]
+                hp.blocks.append(chirpz(
+                    g, lo, hi - lo + 1, blk.i1, blk.i2 - blk.i1 + 1,
+                    ccols[lo:hi + 1, :].T, w_uv[:, rows], accumulate=True))
+            else:
+                # out[strip] += C_m (DCT(u_m wv) + DST(v_m wv)); degrees > N dropped
+                top = min(hi, n)
+                if lo > top:
+                    continue
+                hp.blocks.append(chirpz(
+                    g, blk.i1, blk.i2 - blk.i1 + 1, lo, top - lo + 1,
+                    w_uv[:, rows], ccols[lo:top + 1, :].T, accumulate=True))
+
+    if direction == "forward":
+        # chebyshev_analysis (trig.py:53-63): scipy DCT-I of 0.5 v, i.e. the
+        # plain cosine sum with the two end samples halved, then 2/G with the
+        # two end coefficients halved
+        pre = np.ones(g + 1)
+        pre[0] = pre[-1] = 0.5
+        post = np.full(g + 1, 2.0 / g)
+        post[0] *= 0.5
+        post[-1] *= 0.5
+        hp.analysis = chirpz(g, 0, g + 1, 0, g + 1, pre[None, :],
+                             post[None, :], accumulate=False)
+    else:
+        mu = moments(p, g)
+        w = cc_weights(p, g, mu)
+        hp.weights = w
+        # wv = w * dct1([c, 0...]) (engine.py:201-203)
+        hp.synthesis = chirpz(g, 0, n + 1, 0, g + 1, np.ones((1, n + 1)),
+                              w[None, :], accumulate=False)
+        hp.scalings = 1.0 / orthonormality(p, n)
+    return hp
