@@ -116,6 +116,17 @@ int cjt_execute(cjt_plan* plan, const double* in, double* out, int64_t batch, vo
 int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host,
                      int64_t batch, void* stream);
 
+/* Timing aid: run only some stages of one execution (results are not a
+ * transform unless stages == CJT_STAGE_ALL).  batch <= reserved batch. */
+#define CJT_STAGE_REC 1
+#define CJT_STAGE_BLOCKS 2
+#define CJT_STAGE_EDGE 4
+#define CJT_STAGE_ALL 7
+int cjt_execute_stage(cjt_plan* plan, const double* in, double* out, int64_t batch,
+                      int32_t stages, void* stream);
+/* Measured fp64 FMA throughput of the current device (TFLOP/s, best of 5). */
+int cjt_probe_fp64_peak(double* tflops, void* stream);
+
 /* Reference backend-plugin signatures, host arrays (see header comment). */
 int cjt_clenshaw_points(const double* A, const double* B, const double* C,
                         const double* rb_plus, const double* rb_minus,

@@ -78,12 +78,15 @@ def lib():
     L.cjt_plan_stats_get.argtypes = [_p, ctypes.POINTER(PlanStats)]
     L.cjt_execute.argtypes = [_p, _p, _p, _i64, _p]
     L.cjt_execute_host.argtypes = [_p, _p, _p, _i64, _p]
+    L.cjt_execute_stage.argtypes = [_p, _p, _p, _i64, _i32, _p]
+    L.cjt_probe_fp64_peak.argtypes = [ctypes.POINTER(ctypes.c_double), _p]
     L.cjt_clenshaw_points.argtypes = [_p] * 8 + [_i64, _p, _p, _p, _p, _i64]
     L.cjt_transpose_accumulate.argtypes = [_p] * 12 + [_i64, _i64, _i64]
     L.cjt_host_angles.argtypes = [_p, _p, _i64, _p, _p]
     for name in ("cjt_device_count", "cjt_plan_create", "cjt_plan_destroy", "cjt_plan_reserve",
                  "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host", "cjt_clenshaw_points",
-                 "cjt_transpose_accumulate", "cjt_host_angles"):
+                 "cjt_transpose_accumulate", "cjt_host_angles", "cjt_execute_stage",
+                 "cjt_probe_fp64_peak"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -92,8 +95,10 @@ def lib():
 EXPORTED_SYMBOLS = (
     "cjt_version", "cjt_last_error", "cjt_device_count", "cjt_plan_create", "cjt_plan_destroy",
     "cjt_plan_reserve", "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host",
-    "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles",
+    "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_execute_stage",
+    "cjt_probe_fp64_peak",
 )
+STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7
 
 
 def check(rc: int, what: str = "cjt"):

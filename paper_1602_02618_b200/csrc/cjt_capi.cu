@@ -79,6 +79,7 @@ struct cjt_plan {
   double* io_out = nullptr;
   int64_t workspace_bytes = 0;
   int64_t last_launches = 0;
+  int vt = 64;
 
   ~cjt_plan() {
     int cur = 0;
@@ -189,36 +190,47 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
 }
 
 // Work lists depend on the batch size (split-K is sized to fill the GPU).
-int build_items(cjt_plan* P, int64_t batch) {
-  const int64_t nrows = P->nrows;
-  const int64_t ntiles = (nrows + FWD_ROWS - 1) / FWD_ROWS;
-  std::vector<int64_t> tile_max((size_t)ntiles, 0);
-  for (int64_t i = 0; i < nrows; ++i) {
-    const int64_t t = i / FWD_ROWS;
-    tile_max[t] = std::max(tile_max[t], P->h_cut[i]);
+std::vector<int64_t> tile_max_cut(const cjt_plan* P, int64_t rows_per_tile) {
+  const int64_t ntiles = (P->nrows + rows_per_tile - 1) / rows_per_tile;
+  std::vector<int64_t> mx((size_t)ntiles, 0);
+  for (int64_t i = 0; i < P->nrows; ++i) {
+    const int64_t t = i / rows_per_tile;
+    mx[t] = std::max(mx[t], P->h_cut[i]);
   }
-  const int64_t target = 8 * 148;
+  return mx;
+}
+
+template <typename T>
+int upload_ws(cjt_plan* P, T** dst, const std::vector<T>& v) {
+  void* p;
+  if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, v.size()) * sizeof(T))) return rc;
+  *dst = (T*)p;
+  if (!v.empty()) CJT_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return CJT_OK;
+}
+
+int build_items(cjt_plan* P, int64_t batch) {
+  const int64_t target = 8 * 148;  // CTAs worth of items to fill 148 SMs several times over
+  P->vt = pick_vt(batch);
+  const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {
-    const int64_t nbt = (batch + FWD_VT - 1) / FWD_VT;
+    const std::vector<int64_t> tmax = tile_max_cut(P, FWD_ROWS);
+    const int64_t ntiles = (int64_t)tmax.size();
     double total = 0.0;
-    int64_t mx = 0;
-    for (int64_t t = 0; t < ntiles; ++t) {
-      total += (double)tile_max[t];
-      mx = std::max(mx, tile_max[t]);
-    }
+    for (int64_t t = 0; t < ntiles; ++t) total += (double)tmax[t];
     int64_t seg = (int64_t)std::ceil(total * nbt / target);
-    seg = std::max<int64_t>(256, ((seg + CK - 1) / CK) * CK);
+    seg = std::max<int64_t>(8 * FWD_KS, ((seg + FWD_KS - 1) / FWD_KS) * FWD_KS);
     std::vector<FwdItem> items;
     std::vector<int32_t> s0((size_t)ntiles), ns((size_t)ntiles);
     int32_t slot = 0;
     for (int64_t t = 0; t < ntiles; ++t) {
       s0[t] = slot;
-      const int64_t top = ((tile_max[t] + FWD_CH - 1) / FWD_CH) * FWD_CH;
+      const int64_t top = ((tmax[t] + FWD_KS - 1) / FWD_KS) * FWD_KS;
       int32_t cnt = 0;
       for (int64_t nb = 0; nb < top; nb += seg) {
         FwdItem it{};
         it.row0 = (int32_t)(t * FWD_ROWS);
-        it.nrows = (int32_t)std::min<int64_t>(FWD_ROWS, nrows - t * FWD_ROWS);
+        it.nrows = (int32_t)std::min<int64_t>(FWD_ROWS, P->nrows - t * FWD_ROWS);
         it.n_begin = (int32_t)nb;
         it.n_end = (int32_t)std::min(top, nb + seg);
         it.slot = slot++;
@@ -231,45 +243,41 @@ int build_items(cjt_plan* P, int64_t batch) {
     std::stable_sort(items.begin(), items.end(), [](const FwdItem& a, const FwdItem& b) {
       return (a.n_end - a.n_begin) > (b.n_end - b.n_begin);
     });
-    void* p;
-    if (int rc = dalloc(P->ws_allocs, &p, items.size() * sizeof(FwdItem))) return rc;
-    P->fitems = (FwdItem*)p;
-    CJT_CUDA_TRY(cudaMemcpy(p, items.data(), items.size() * sizeof(FwdItem), cudaMemcpyHostToDevice));
-    if (int rc = dalloc(P->ws_allocs, &p, s0.size() * 4)) return rc;
-    P->tile_slot0 = (int32_t*)p;
-    CJT_CUDA_TRY(cudaMemcpy(p, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
-    if (int rc = dalloc(P->ws_allocs, &p, ns.size() * 4)) return rc;
-    P->tile_nslot = (int32_t*)p;
-    CJT_CUDA_TRY(cudaMemcpy(p, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = upload_ws(P, &P->fitems, items)) return rc;
+    if (int rc = upload_ws(P, &P->tile_slot0, s0)) return rc;
+    if (int rc = upload_ws(P, &P->tile_nslot, ns)) return rc;
     P->n_fitems = (int64_t)items.size();
     P->n_fslots = slot;
   } else {
+    const std::vector<int64_t> tmax = tile_max_cut(P, INV_RT);
+    const int64_t ntiles = (int64_t)tmax.size();
     const int64_t ndeg = P->n + 1;
     const int64_t nd = (ndeg + INV_DT - 1) / INV_DT;
-    const int64_t nbt = (batch + INV_VT - 1) / INV_VT;
     std::vector<std::vector<int32_t>> active((size_t)nd);
     int64_t total_active = 0;
     for (int64_t d = 0; d < nd; ++d) {
       for (int64_t t = 0; t < ntiles; ++t)
-        if (tile_max[t] > d * INV_DT) active[d].push_back((int32_t)t);
+        if (tmax[t] > d * INV_DT) active[d].push_back((int32_t)t);
       total_active += (int64_t)active[d].size();
     }
-    int64_t cs = INT64_MAX;
-    if (nd * nbt < target) cs = std::max<int64_t>(1, (int64_t)std::ceil((double)total_active * nbt / target));
+    const int64_t cs = std::max<int64_t>(1, (int64_t)std::ceil((double)total_active * nbt / target));
     std::vector<InvItem> items;
     std::vector<int32_t> ids, s0((size_t)nd), ns((size_t)nd);
     int32_t slot = 0;
     for (int64_t d = 0; d < nd; ++d) {
       s0[d] = slot;
       const int64_t na = (int64_t)active[d].size();
+      // split the active row tiles of this degree tile into near-equal chunks of <= cs
+      const int64_t nchunks = std::max<int64_t>(1, (na + cs - 1) / cs);
       int32_t cnt = 0;
-      for (int64_t a = 0; a < na; a += cs) {
+      for (int64_t q = 0; q < nchunks && na > 0; ++q) {
+        const int64_t a0 = na * q / nchunks, a1 = na * (q + 1) / nchunks;
+        if (a1 <= a0) continue;
         InvItem it{};
         it.n0 = (int32_t)(d * INV_DT);
         it.t_begin = (int32_t)ids.size();
-        const int64_t take = std::min(cs, na - a);
-        for (int64_t q = 0; q < take; ++q) ids.push_back(active[d][a + q]);
-        it.t_count = (int32_t)take;
+        for (int64_t a = a0; a < a1; ++a) ids.push_back(active[d][a]);
+        it.t_count = (int32_t)(a1 - a0);
         it.slot = slot++;
         items.push_back(it);
         ++cnt;
@@ -278,20 +286,10 @@ int build_items(cjt_plan* P, int64_t batch) {
     }
     std::stable_sort(items.begin(), items.end(),
                      [](const InvItem& a, const InvItem& b) { return a.t_count > b.t_count; });
-    void* p;
-    if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, items.size()) * sizeof(InvItem))) return rc;
-    P->iitems = (InvItem*)p;
-    if (!items.empty())
-      CJT_CUDA_TRY(cudaMemcpy(p, items.data(), items.size() * sizeof(InvItem), cudaMemcpyHostToDevice));
-    if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, ids.size()) * 4)) return rc;
-    P->tile_ids = (int32_t*)p;
-    if (!ids.empty()) CJT_CUDA_TRY(cudaMemcpy(p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
-    if (int rc = dalloc(P->ws_allocs, &p, s0.size() * 4)) return rc;
-    P->dt_slot0 = (int32_t*)p;
-    CJT_CUDA_TRY(cudaMemcpy(p, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
-    if (int rc = dalloc(P->ws_allocs, &p, ns.size() * 4)) return rc;
-    P->dt_nslot = (int32_t*)p;
-    CJT_CUDA_TRY(cudaMemcpy(p, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = upload_ws(P, &P->iitems, items)) return rc;
+    if (int rc = upload_ws(P, &P->tile_ids, ids)) return rc;
+    if (int rc = upload_ws(P, &P->dt_slot0, s0)) return rc;
+    if (int rc = upload_ws(P, &P->dt_nslot, ns)) return rc;
     P->n_iitems = (int64_t)items.size();
     P->n_islots = slot;
   }
@@ -342,37 +340,65 @@ int reserve(cjt_plan* P, int64_t batch) {
   return CJT_OK;
 }
 
-int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStream_t st) {
+// stage mask: CJT_STAGE_REC (recurrence contraction + its reduction),
+// CJT_STAGE_BLOCKS (asymptotic-block chirp-z), CJT_STAGE_EDGE (analysis /
+// synthesis chirp-z).  Partial masks are for timing individual kernels only.
+int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStream_t st,
+            int stages = CJT_STAGE_ALL) {
   int launches = 0;
   const int64_t N1 = P->n + 1, G1 = P->G + 1;
+  const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
   if (P->direction == CJT_FORWARD) {
-    if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
-                                    N1, batch, P->part, st)) return rc;
-    if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, P->part, P->vals,
-                                           G1, batch, st)) return rc;
-    launches += 2;
-    for (const ChirpZDev& cz : P->blocks)
-      if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+    if (rec) {
+      if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
+                                      N1, batch, P->vt, P->part, st)) return rc;
+      if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, P->part, P->vals,
+                                             G1, batch, st)) return rc;
+      launches += 2;
+    }
+    if (blk)
+      for (const ChirpZDev& cz : P->blocks)
+        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+          return rc;
+    if (edge)
+      if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, st, &launches))
         return rc;
-    if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, st, &launches))
-      return rc;
   } else {
-    if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
-      return rc;
-    if (!P->blocks.empty()) {
+    if (edge)
+      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+        return rc;
+    if (blk && !P->blocks.empty()) {
       CJT_CUDA_TRY(cudaMemsetAsync(P->yacc, 0, (size_t)(N1 * batch) * 8, st));
       for (const ChirpZDev& cz : P->blocks)
         if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, st, &launches))
           return rc;
     }
-    if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
-                                    P->vals, G1, batch, P->part, st)) return rc;
-    if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
-                                       batch, st)) return rc;
-    launches += 2;
+    if (rec) {
+      if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
+                                      P->vals, G1, batch, P->vt, P->part, st)) return rc;
+      if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
+                                         batch, st)) return rc;
+      launches += 2;
+    }
   }
-  P->last_launches = launches;
+  if (stages == CJT_STAGE_ALL) P->last_launches = launches;
   return CJT_OK;
+}
+
+// DFMA throughput probe: independent FMA chains, no memory traffic.
+__global__ void k_fp64_probe(double* sink, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double m = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 1234.5) sink[threadIdx.x] = s;
 }
 
 }  // namespace
@@ -510,6 +536,46 @@ int cjt_execute(cjt_plan* plan, const double* in, double* out, int64_t batch, vo
   return execute(plan, in, out, batch, (cudaStream_t)stream);
 }
 
+int cjt_execute_stage(cjt_plan* plan, const double* in, double* out, int64_t batch, int32_t stages,
+                      void* stream) {
+  if (!plan || !in || !out) return fail(CJT_EINVAL, "null argument");
+  if (batch < 1 || batch > plan->reserved) return fail(CJT_EINVAL, "batch must be in [1, reserved]");
+  DeviceGuard g(plan->device);
+  return execute(plan, in, out, batch, (cudaStream_t)stream, stages);
+}
+
+int cjt_probe_fp64_peak(double* tflops, void* stream) {
+  if (!tflops) return fail(CJT_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* sink = nullptr;
+  CJT_CUDA_TRY(cudaMalloc(&sink, 1024 * sizeof(double)));
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_fp64_probe<<<blocks, threads, 0, st>>>(sink, 64);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0, st);
+    k_fp64_probe<<<blocks, threads, 0, st>>>(sink, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  CJT_CUDA_TRY(cudaGetLastError());
+  const double flops = 2.0 * 8.0 * 16.0 * iters * (double)threads * blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return CJT_OK;
+}
+
 int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, int64_t batch,
                      void* stream) {
   if (!plan || !in_host || !out_host) return fail(CJT_EINVAL, "null argument");
@@ -638,7 +704,7 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   if (int rc = dalloc(Al, &p, ones.size() * 8)) return rc;
   dres = (double*)p;
   if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
-                                  dwv, n_points, 1, P->part, 0)) return rc;
+                                  dwv, n_points, 1, P->vt, P->part, 0)) return rc;
   if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, P->part, nullptr, dscal, dres,
                                      P->n + 1, 1, 0)) return rc;
   std::vector<double> res(ones.size());

@@ -224,12 +224,13 @@ struct InvItem {
 };
 
 constexpr int CK = 32;          // recurrence checkpoint spacing (degrees)
-constexpr int FWD_ROWS = 128;   // rows per forward tile (4 warps x 32 lanes)
-constexpr int FWD_VT = 32;      // vectors per forward CTA
-constexpr int FWD_CH = 32;      // degrees per staged coefficient chunk
-constexpr int INV_DT = 64;      // degrees per inverse tile
-constexpr int INV_VT = 64;      // vectors per inverse tile
-constexpr int INV_RT = 128;     // rows per inverse stage
+constexpr int FWD_ROWS = 128;   // grid rows per forward CTA tile (4 warps x 32 rows)
+constexpr int FWD_KS = 32;      // degrees per forward pipeline stage
+constexpr int INV_DT = 128;     // degrees per inverse CTA tile (4 warps x 32 degrees)
+constexpr int INV_RT = 32;      // grid rows per inverse pipeline stage (= row tile)
+
+// vectors per CTA tile of the DMMA contractions, chosen from the batch size
+inline int pick_vt(int64_t batch) { return batch >= 64 ? 64 : (batch >= 32 ? 32 : 16); }
 
 // ---------------------------------------------------------------------------
 // launchers (host)
@@ -241,7 +242,7 @@ int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const in
                        double2* ck, cudaStream_t st);
 int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const FwdItem* items, int64_t n_items,
-                       const double* c, int64_t ldc, int64_t ncoef, int64_t batch,
+                       const double* c, int64_t ldc, int64_t ncoef, int64_t batch, int vt,
                        double* part, cudaStream_t st);
 int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nslot,
                               int64_t nrows, const double* part, double* vals, int64_t ldv,
@@ -249,7 +250,7 @@ int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nsl
 int launch_rec_inverse(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const InvItem* items, int64_t n_items,
                        const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch,
-                       double* part, cudaStream_t st);
+                       int vt, double* part, cudaStream_t st);
 int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,
                           const double* part, const double* blocks_acc, const double* scal,
                           double* out, int64_t ldo, int64_t batch, cudaStream_t st);

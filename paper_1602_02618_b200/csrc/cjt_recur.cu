@@ -19,6 +19,8 @@
 // recurrence state (every CK degrees), which keeps the values bit-identical
 // while exposing parallelism; partial sums are reduced in a fixed order
 // (deterministic, no atomics).
+#include <type_traits>
+
 #include "cjt_internal.cuh"
 
 namespace cjt {
@@ -85,66 +87,130 @@ __global__ void k_checkpoints(RecRowsDev rows, RecTablesDev tab, const int64_t* 
   }
 }
 
-// K1: one lane per grid row, FWD_VT vectors per lane, coefficients staged in
-// shared memory and read as warp-wide broadcasts.
-__global__ void __launch_bounds__(FWD_ROWS)
-    k_rec_forward(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-                  const double2* __restrict__ ck, const FwdItem* __restrict__ items,
-                  const double* __restrict__ c, int64_t ldc, int64_t ncoef, int64_t batch,
-                  double* __restrict__ part) {
-  __shared__ __align__(16) double cs[FWD_CH][FWD_VT];
+// ---------------------------------------------------------------------------
+// DMMA helpers: mma.sync m8n8k4 f64 (the fp64 tensor path of sm_100a; tcgen05
+// has no f64 kind).  Fragments: A[r][k] at lane 4r+k, B[k][n] at lane 4n+k,
+// D[r][2c+j] at lane 4r+c.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// 8-byte async copy global -> shared, zero-filled when !valid
+__device__ __forceinline__ void cp_async8(void* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// K1 (forward): values[b][i] = sum_n P_n(x_i) c[b][n] over one item
+// (128 rows x a degree segment) and one tile of VT vectors.
+//   M = rows (4 warps x 32), N = vectors (VT), K = degrees (stages of 32).
+//   P^T[k][row] is generated into shared memory by thread `row` (one
+//   recurrence chain per thread, carried across stages in registers);
+//   c[b][n0..n0+32) is staged by cp.async; stages are double-buffered.
+template <int VT>
+__global__ void __launch_bounds__(128)
+    k_rec_forward_mma(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
+                      const double2* __restrict__ ck, const FwdItem* __restrict__ items,
+                      const double* __restrict__ c, int64_t ldc, int64_t ncoef, int64_t batch,
+                      double* __restrict__ part) {
+  constexpr int PT = FWD_ROWS + 4;   // P^T row stride (degrees x rows)
+  constexpr int CS = FWD_KS + 4;     // staged c row stride (vectors x degrees)
+  constexpr int NT = VT / 8;
+  extern __shared__ __align__(16) double smem_rec[];
+  double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
+  double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + 2 * FWD_KS * PT);
   const FwdItem it = items[blockIdx.x];
-  const int64_t b0 = (int64_t)blockIdx.y * FWD_VT;
-  const int lr = threadIdx.x;
-  const int64_t i = it.row0 + lr;
-  const bool live = lr < it.nrows;
+  const int64_t b0 = (int64_t)blockIdx.y * VT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // generator state for row `tid`
+  const int64_t gi = it.row0 + tid;
+  const bool live = tid < it.nrows;
   int reg = 0;
-  double x = 0.0, xm = 0.0;
+  double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
   int64_t cut = 0;
   if (live) {
-    reg = rows.reg[i];
-    x = rows.x[i];
-    xm = rows.xm[i];
-    cut = rows.cut[i];
+    reg = rows.reg[gi];
+    x = rows.x[gi];
+    xm = rows.xm[gi];
+    cut = rows.cut[gi];
+    if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
   }
-  double s0 = 0.0, s1 = 0.0;
-  if (live && cut > it.n_begin) load_state(rows, ck_off, ck, i, it.n_begin, reg, s0, s1);
-  double acc[FWD_VT];
+  // generate degrees n0+k0 .. n0+k0+KN-1 of this thread's row into Pt[buf]
+  auto generate = [&](int buf, int64_t n0, int k0, auto kn) {
 #pragma unroll
-  for (int v = 0; v < FWD_VT; ++v) acc[v] = 0.0;
-
-  for (int64_t n0 = it.n_begin; n0 < it.n_end; n0 += FWD_CH) {
-    // stage c[b0 .. b0+VT)[n0 .. n0+CH) transposed: cs[k][v]
-#pragma unroll
-    for (int q = 0; q < (FWD_CH * FWD_VT) / FWD_ROWS; ++q) {
-      const int idx = threadIdx.x + q * FWD_ROWS;
-      const int k = idx % FWD_CH, v = idx / FWD_CH;
-      const int64_t bb = b0 + v, n = n0 + k;
-      cs[k][v] = (bb < batch && n < ncoef) ? __ldg(c + bb * ldc + n) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 2
-    for (int k = 0; k < FWD_CH; ++k) {
+    for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
       const int64_t n = n0 + k;
-      const double p = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-      const double2* row = reinterpret_cast<const double2*>(&cs[k][0]);
-#pragma unroll
-      for (int v = 0; v < FWD_VT / 2; ++v) {
-        const double2 cv = row[v];
-        acc[2 * v] = fma(p, cv.x, acc[2 * v]);
-        acc[2 * v + 1] = fma(p, cv.y, acc[2 * v + 1]);
-      }
+      Pt[buf][k][tid] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
       if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
     }
+  };
+  auto stage_c = [&](int buf, int64_t n0) {
+#pragma unroll
+    for (int q = 0; q < (VT * FWD_KS) / 128; ++q) {
+      const int idx = tid + q * 128;
+      const int v = idx / FWD_KS, k = idx % FWD_KS;
+      const int64_t bb = b0 + v, n = n0 + k;
+      const bool ok = bb < batch && n < ncoef;
+      cp_async8(&Cs[buf][v][k], ok ? c + bb * ldc + n : c, ok);
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  const int nstages = (it.n_end - it.n_begin) / FWD_KS;
+  using Four = std::integral_constant<int, 4>;
+  stage_c(0, it.n_begin);
+  for (int k0 = 0; k0 < FWD_KS; k0 += 4) generate(0, it.n_begin, k0, Four{});
+  cp_async_wait_all();
+  __syncthreads();
+  const int ar = lane >> 2, ak = lane & 3;
+  for (int sidx = 0; sidx < nstages; ++sidx) {
+    const int buf = sidx & 1;
+    const bool more = sidx + 1 < nstages;
+    const int64_t nn = it.n_begin + (int64_t)(sidx + 1) * FWD_KS;
+    if (more) stage_c(buf ^ 1, nn);
+#pragma unroll
+    for (int kk = 0; kk < FWD_KS / 4; ++kk) {
+      // four recurrence steps of the next stage overlap this k-step's DMMAs
+      if (more) generate(buf ^ 1, nn, 4 * kk, Four{});
+      double a[4], bf[NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = Pt[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = Cs[buf][8 * nt + ar][4 * kk + ak];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+    }
+    cp_async_wait_all();
     __syncthreads();
   }
-  if (!live) return;
+  // D[row][vec]: row = 32 warp + 8 mt + (lane>>2), vec = 8 nt + 2 (lane&3) + j
   double* dst = part + (int64_t)it.slot * batch * FWD_ROWS;
 #pragma unroll
-  for (int v = 0; v < FWD_VT; ++v) {
-    const int64_t bb = b0 + v;
-    if (bb < batch) dst[bb * FWD_ROWS + lr] = acc[v];
-  }
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int row = 32 * warp + 8 * mt + ar;
+        const int64_t bb = b0 + 8 * nt + 2 * ak + j;
+        if (bb < batch) dst[bb * FWD_ROWS + row] = acc[mt][nt][j];
+      }
 }
 
 __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
@@ -161,91 +227,120 @@ __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
   vals[b * ldv + i] = acc;
 }
 
-// K2: degrees x vectors output tile, reduction over grid rows; P tiles are
-// generated into shared memory (two threads per row, CK degrees each) and
-// contracted with the staged wv tile.  16-byte chunks are XOR-swizzled by
-// row so the row-strided staging stores and the GEMM's 128-bit loads are both
-// nearly conflict-free.
-__device__ __forceinline__ int swz(int row, int col) {  // col in doubles, 64 per row
-  return row * 64 + ((((col >> 1) ^ (row & 7))) << 1) + (col & 1);
-}
-
-__global__ void __launch_bounds__(256)
-    k_rec_inverse(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-                  const double2* __restrict__ ck, const InvItem* __restrict__ items,
-                  const int32_t* __restrict__ tile_ids, const double* __restrict__ wv,
-                  int64_t ldw, int64_t batch, double* __restrict__ part) {
-  extern __shared__ __align__(16) double sm_inv[];
-  double* Ps = sm_inv;                      // [INV_RT][64] P_n(x_i), swizzled
-  double* Ws = sm_inv + INV_RT * 64;        // [INV_RT][64] wv, swizzled
+// K2 (inverse): out[b][n] = sum_i P_n(x_i) wv[b][i] for one item (128
+// degrees x a list of 32-row tiles) and one tile of VT vectors.
+//   M = degrees (4 warps x 32), N = vectors (VT), K = rows (stages of 32).
+//   Each stage's P[row][deg] tile is generated by 4 threads per row, each
+//   restarting from the checkpoint at n0 + 32q; wv[b][rows] is staged by
+//   cp.async; stages are double-buffered.
+template <int VT>
+__global__ void __launch_bounds__(128)
+    k_rec_inverse_mma(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
+                      const double2* __restrict__ ck, const InvItem* __restrict__ items,
+                      const int32_t* __restrict__ tile_ids, const double* __restrict__ wv,
+                      int64_t ldw, int64_t batch, double* __restrict__ part) {
+  constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
+  constexpr int WS = INV_RT + 4;
+  constexpr int NT = VT / 8;
+  extern __shared__ __align__(16) double smem_rec[];
+  double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
+  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + 2 * INV_RT * PR);
   const InvItem it = items[blockIdx.x];
-  const int64_t b0 = (int64_t)blockIdx.y * INV_VT;
-  const int tid = threadIdx.x;
-  const int td = tid >> 4, tv = tid & 15;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[a][q] = 0.0;
+  const int64_t b0 = (int64_t)blockIdx.y * VT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grow = tid >> 2, gq = tid & 3;   // generator: row in tile, degree chunk
 
+  // generator for the next row tile: row grow, degrees n0 + 32 gq + [0, 32)
+  int64_t g_cut = 0;
+  int g_reg = 0;
+  double g_x = 0.0, g_xm = 0.0, g_s0 = 0.0, g_s1 = 0.0;
+  auto gen_begin = [&](int64_t r0) {
+    const int64_t i = r0 + grow;
+    const int64_t nstart = it.n0 + CK * gq;
+    g_cut = 0;
+    g_reg = 0;
+    g_s0 = g_s1 = 0.0;
+    if (i < rows.nrows) {
+      g_cut = rows.cut[i];
+      if (g_cut > nstart) {
+        g_reg = rows.reg[i];
+        g_x = rows.x[i];
+        g_xm = rows.xm[i];
+        load_state(rows, ck_off, ck, i, nstart, g_reg, g_s0, g_s1);
+      }
+    }
+  };
+  auto generate = [&](int buf, int k0, auto kn) {
+    const int64_t nstart = it.n0 + CK * gq;
+    double* dst = &Ps[buf][grow][CK * gq + gq];
+#pragma unroll
+    for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
+      const int64_t n = nstart + k;
+      dst[k] = (n < g_cut) ? rec_value(g_reg, g_s0, g_s1) : 0.0;
+      if (n + 1 < g_cut) rec_step(g_reg, g_x, g_xm, tab, n, g_s0, g_s1);
+    }
+  };
+  auto stage_w = [&](int buf, int64_t r0) {
+#pragma unroll
+    for (int q = 0; q < (VT * INV_RT) / 128; ++q) {
+      const int idx = tid + q * 128;
+      const int v = idx / INV_RT, k = idx % INV_RT;
+      const int64_t bb = b0 + v, i = r0 + k;
+      const bool ok = bb < batch && i < rows.nrows;
+      cp_async8(&Ws[buf][v][k], ok ? wv + bb * ldw + i : wv, ok);
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  const int ar = lane >> 2, ak = lane & 3;
+  const int dbase = 32 * warp + warp;   // padded column of this warp's first degree
+  using Four = std::integral_constant<int, 4>;
+  stage_w(0, (int64_t)tile_ids[it.t_begin] * INV_RT);
+  gen_begin((int64_t)tile_ids[it.t_begin] * INV_RT);
+  for (int k0 = 0; k0 < CK; k0 += 4) generate(0, k0, Four{});
+  cp_async_wait_all();
+  __syncthreads();
   for (int tt = 0; tt < it.t_count; ++tt) {
-    const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt] * INV_RT;
-    // generate P for rows r0 + (tid & 127), degrees n0 + 32*(tid >> 7) .. +32
-    {
-      const int lr = tid & (INV_RT - 1);
-      const int half = tid >> 7;
-      const int64_t i = r0 + lr;
-      const int64_t nstart = it.n0 + half * CK;
-      int64_t cut = 0;
-      int reg = 0;
-      double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
-      if (i < rows.nrows) {
-        cut = rows.cut[i];
-        reg = rows.reg[i];
-        x = rows.x[i];
-        xm = rows.xm[i];
-        if (cut > nstart) load_state(rows, ck_off, ck, i, nstart, reg, s0, s1);
-      }
-#pragma unroll 4
-      for (int k = 0; k < CK; ++k) {
-        const int64_t n = nstart + k;
-        Ps[swz(lr, half * CK + k)] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-        if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
-      }
+    const int buf = tt & 1;
+    const bool more = tt + 1 < it.t_count;
+    if (more) {
+      const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt + 1] * INV_RT;
+      stage_w(buf ^ 1, r0);
+      gen_begin(r0);
     }
-    // stage wv[b0 + v][r0 + row] -> Ws[row][v]
-#pragma unroll 4
-    for (int q = 0; q < (INV_RT * INV_VT) / 256; ++q) {
-      const int idx = tid + q * 256;
-      const int row = idx % INV_RT, v = idx / INV_RT;
-      const int64_t bb = b0 + v, i = r0 + row;
-      Ws[swz(row, v)] = (bb < batch && i < rows.nrows) ? __ldg(wv + bb * ldw + i) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int row = 0; row < INV_RT; ++row) {
-      const int sw = row & 7;
-      const double2 p01 = *reinterpret_cast<const double2*>(&Ps[row * 64 + (((2 * td) ^ sw) << 1)]);
-      const double2 p23 = *reinterpret_cast<const double2*>(&Ps[row * 64 + (((2 * td + 1) ^ sw) << 1)]);
-      const double2 w01 = *reinterpret_cast<const double2*>(&Ws[row * 64 + (((2 * tv) ^ sw) << 1)]);
-      const double2 w23 = *reinterpret_cast<const double2*>(&Ws[row * 64 + (((2 * tv + 1) ^ sw) << 1)]);
-      const double pp[4] = {p01.x, p01.y, p23.x, p23.y};
-      const double ww[4] = {w01.x, w01.y, w23.x, w23.y};
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+    for (int kk = 0; kk < INV_RT / 4; ++kk) {
+      if (more) generate(buf ^ 1, 4 * kk, Four{});
+      double a[4], bf[NT];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[a][q] = fma(pp[a], ww[q], acc[a][q]);
+      for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = Ws[buf][8 * nt + ar][4 * kk + ak];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
     }
+    cp_async_wait_all();
     __syncthreads();
   }
   double* dst = part + (int64_t)it.slot * batch * INV_DT;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t bb = b0 + 4 * tv + q;
-    if (bb >= batch) continue;
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) dst[bb * INV_DT + 4 * td + a] = acc[a][q];
-  }
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int deg = 32 * warp + 8 * mt + ar;
+        const int64_t bb = b0 + 8 * nt + 2 * ak + j;
+        if (bb < batch) dst[bb * INV_DT + deg] = acc[mt][nt][j];
+      }
 }
 
 __global__ void k_inverse_finish(const int32_t* __restrict__ dt_slot0,
@@ -320,10 +415,27 @@ int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const in
 
 int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const FwdItem* items, int64_t n_items, const double* c,
-                       int64_t ldc, int64_t ncoef, int64_t batch, double* part, cudaStream_t st) {
+                       int64_t ldc, int64_t ncoef, int64_t batch, int vt, double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
-  dim3 grid((unsigned)n_items, (unsigned)((batch + FWD_VT - 1) / FWD_VT));
-  k_rec_forward<<<grid, FWD_ROWS, 0, st>>>(rows, tab, ck_off, ck, items, c, ldc, ncoef, batch, part);
+  dim3 grid((unsigned)n_items, (unsigned)((batch + vt - 1) / vt));
+  switch (vt) {
+#define CJT_FWD(V)                                                                               \
+  case V: {                                                                                      \
+    const int smem = 8 * 2 * (FWD_KS * (FWD_ROWS + 4) + V * (FWD_KS + 4));                       \
+    static bool init = false;                                                                    \
+    if (!init) {                                                                                 \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_mma<V>,                                    \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
+      init = true;                                                                               \
+    }                                                                                            \
+    k_rec_forward_mma<V><<<grid, 128, smem, st>>>(rows, tab, ck_off, ck, items, c, ldc, ncoef,   \
+                                                   batch, part);                                 \
+    break;                                                                                       \
+  }
+    CJT_FWD(64) CJT_FWD(32) CJT_FWD(16)
+#undef CJT_FWD
+    default: return fail(CJT_EINVAL, "bad vector tile");
+  }
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -340,17 +452,28 @@ int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nsl
 
 int launch_rec_inverse(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const InvItem* items, int64_t n_items,
-                       const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch,
+                       const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch, int vt,
                        double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
-  const int smem = 2 * INV_RT * 64 * (int)sizeof(double);
-  static bool init = false;
-  if (!init) {
-    CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    init = true;
+  dim3 grid((unsigned)n_items, (unsigned)((batch + vt - 1) / vt));
+  switch (vt) {
+#define CJT_INV(V)                                                                               \
+  case V: {                                                                                      \
+    const int smem = 8 * 2 * (INV_RT * (INV_DT + 4) + V * (INV_RT + 4));                         \
+    static bool init = false;                                                                    \
+    if (!init) {                                                                                 \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_mma<V>,                                    \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
+      init = true;                                                                               \
+    }                                                                                            \
+    k_rec_inverse_mma<V><<<grid, 128, smem, st>>>(rows, tab, ck_off, ck, items, tile_ids, wv,    \
+                                                   ldw, batch, part);                            \
+    break;                                                                                       \
   }
-  dim3 grid((unsigned)n_items, (unsigned)((batch + INV_VT - 1) / INV_VT));
-  k_rec_inverse<<<grid, 256, smem, st>>>(rows, tab, ck_off, ck, items, tile_ids, wv, ldw, batch, part);
+    CJT_INV(64) CJT_INV(32) CJT_INV(16)
+#undef CJT_INV
+    default: return fail(CJT_EINVAL, "bad vector tile");
+  }
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }

@@ -44,3 +44,20 @@ def test_golden_single_vector_api(cuda, name):
     assert f.basis == cj.CHEBYSHEV and i.basis == cj.JACOBI and i.params == p
     assert O.parity(f.data, g["fwd"][0], g["c"][0]) <= TOL
     assert O.parity(i.data, g["inv"][0], g["fwd"][0]) <= TOL
+
+
+@pytest.mark.parametrize("batch", [1, 17, 40, 70, 129])
+def test_batch_tiles_vs_oracle(cuda, batch):
+    """Every vector-tile width (16/32/64) and ragged batch tails."""
+    import torch
+    a, b, n = 0.25, -0.2, 1023
+    p = cj.JacobiParameters(a, b)
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = np.stack([O.seeded_vector(5, v, n) for v in range(batch)])
+    f = cj.forward_batched(fp, torch.from_numpy(c).to(cuda)).cpu().numpy()
+    i = cj.inverse_batched(ip, torch.from_numpy(f).to(cuda)).cpu().numpy()
+    for v in sorted({0, batch // 2, batch - 1}):
+        rf = O.oracle_forward(a, b, c[v])
+        ri = O.oracle_inverse(a, b, f[v])
+        assert O.parity(f[v], rf, c[v]) <= TOL
+        assert O.parity(i[v], ri, f[v]) <= TOL
