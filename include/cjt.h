@@ -52,12 +52,19 @@ extern "C" {
 typedef struct {
     int64_t p0, width;      /* input index range */
     int64_t q0, count;      /* output index range */
-    int64_t length;         /* power-of-two Bluestein length >= width+count-1 */
+    int64_t length;         /* power-of-two Bluestein length of one tile */
     int32_t m_count;        /* number of summed terms */
     int32_t accumulate;     /* 1: out +=, 0: out = */
     const double* pre;      /* [m_count][width] complex */
     const double* post;     /* [m_count][count] complex */
-    const double* kernel_hat; /* [length] complex, natural order, 1/length folded in */
+    /* tiling of the (width x count) index rectangle: tile (j, i) convolves
+     * input tile i with output tile j; tiles_in[i] = (offset, width_i),
+     * tiles_out[j] = (offset, count_j) relative to p0 / q0, and
+     * width_i + count_j - 1 <= length.  Untiled: n_tiles_in = n_tiles_out = 1. */
+    int32_t n_tiles_in, n_tiles_out;
+    const int64_t* tiles_in;   /* [n_tiles_in][2] */
+    const int64_t* tiles_out;  /* [n_tiles_out][2] */
+    const double* kernel_hat;  /* [n_tiles_out][n_tiles_in][length] complex, 1/length folded in */
 } cjt_chirpz_desc;
 
 typedef struct {

@@ -27,7 +27,9 @@ class ChirpZDesc(ctypes.Structure):
     _fields_ = [
         ("p0", _i64), ("width", _i64), ("q0", _i64), ("count", _i64), ("length", _i64),
         ("m_count", _i32), ("accumulate", _i32),
-        ("pre", _p), ("post", _p), ("kernel_hat", _p),
+        ("pre", _p), ("post", _p),
+        ("n_tiles_in", _i32), ("n_tiles_out", _i32), ("tiles_in", _p), ("tiles_out", _p),
+        ("kernel_hat", _p),
     ]
 
 

@@ -55,6 +55,8 @@ struct cjt_plan {
   double2* tw8192 = nullptr;
   double* scal = nullptr;
   int64_t scratch_elems_per_vec = 0;  // complex elements of multipass scratch per vector
+  int64_t part_elems_per_vec = 0;     // doubles of m-split chirp-z partials per vector
+  double* czpart = nullptr;
   double fft_points = 0.0;
 
   // batch-dependent state (cjt_plan_reserve)
@@ -155,8 +157,29 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   cz.accumulate = d.accumulate;
   const int lg = log2_exact(d.length);
   if (lg < 4 || lg > 26) return fail(CJT_EINVAL, "chirp-z length must be a power of two in [16, 2^26]");
-  if (d.width < 1 || d.count < 1 || d.width + d.count - 1 > d.length || d.m_count < 1)
+  if (d.width < 1 || d.count < 1 || d.m_count < 1 || d.n_tiles_in < 1 || d.n_tiles_out < 1)
     return fail(CJT_EINVAL, "inconsistent chirp-z descriptor");
+  if ((d.n_tiles_in > 1 || d.n_tiles_out > 1) && lg > 13)
+    return fail(CJT_EINVAL, "tiled chirp-z requires length <= 8192");
+  {
+    int64_t wsum = 0, csum = 0, wmax = 0, cmax = 0;
+    for (int i = 0; i < d.n_tiles_in; ++i) {
+      if (d.tiles_in[2 * i] != wsum) return fail(CJT_EINVAL, "input tiles must be contiguous");
+      wsum += d.tiles_in[2 * i + 1];
+      wmax = std::max(wmax, d.tiles_in[2 * i + 1]);
+    }
+    for (int j = 0; j < d.n_tiles_out; ++j) {
+      if (d.tiles_out[2 * j] != csum) return fail(CJT_EINVAL, "output tiles must be contiguous");
+      csum += d.tiles_out[2 * j + 1];
+      cmax = std::max(cmax, d.tiles_out[2 * j + 1]);
+    }
+    if (wsum != d.width || csum != d.count || wmax + cmax - 1 > d.length)
+      return fail(CJT_EINVAL, "chirp-z tiles do not cover the index rectangle");
+  }
+  cz.n_in = d.n_tiles_in;
+  cz.n_out = d.n_tiles_out;
+  if (int rc = upload(P->allocs, const_cast<int64_t**>(&cz.tin), d.tiles_in, (size_t)2 * d.n_tiles_in)) return rc;
+  if (int rc = upload(P->allocs, const_cast<int64_t**>(&cz.tout), d.tiles_out, (size_t)2 * d.n_tiles_out)) return rc;
   cz.log2len = lg;
   const size_t nm = (size_t)d.m_count;
   if (int rc = upload(P->allocs, const_cast<double2**>(&cz.pre),
@@ -164,9 +187,22 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (int rc = upload(P->allocs, const_cast<double2**>(&cz.post),
                       reinterpret_cast<const double2*>(d.post), nm * d.count)) return rc;
   const double2* kh = reinterpret_cast<const double2*>(d.kernel_hat);
-  if (lg <= 13) {
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, (size_t)d.length)) return rc;
-  } else {
+  const bool cluster = lg >= 14 && lg <= 17 && cluster_enabled();
+  if (lg <= 13 || cluster) {
+    // fused / cluster paths read the spectra in natural order
+    const size_t nk = (size_t)d.length * d.n_tiles_in * d.n_tiles_out;
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, nk)) return rc;
+  }
+  if (d.m_count > 1) P->part_elems_per_vec = std::max<int64_t>(P->part_elems_per_vec, d.m_count * d.count);
+  if (lg >= 14) {
+    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
+    std::vector<double2> hi((size_t)nhi), lo(4096);
+    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
+    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
+  }
+  if (lg >= 14 && !cluster) {
     const int l2 = std::min(13, (lg + 1) / 2);
     const int l1 = lg - l2;
     cz.log1 = l1;
@@ -176,15 +212,9 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     for (int64_t k1 = 0; k1 < L1; ++k1)
       for (int64_t k2 = 0; k2 < L2; ++k2) perm[(size_t)(k1 * L2 + k2)] = kh[k1 + L1 * k2];
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
-    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
-    std::vector<double2> hi((size_t)nhi), lo(4096);
-    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
-    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
     P->scratch_elems_per_vec = std::max<int64_t>(P->scratch_elems_per_vec, d.length * d.m_count);
   }
-  P->fft_points += 2.0 * d.m_count * (double)d.length * lg;
+  P->fft_points += 2.0 * d.m_count * d.n_tiles_in * d.n_tiles_out * (double)d.length * lg;
   *out = cz;
   return CJT_OK;
 }
@@ -325,6 +355,11 @@ int reserve(cjt_plan* P, int64_t batch) {
   } else {
     P->yacc = nullptr;
   }
+  if (P->part_elems_per_vec > 0) {
+    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(P->part_elems_per_vec * batch) * 8)) return rc;
+    P->czpart = (double*)p;
+    bytes += P->part_elems_per_vec * batch * 8;
+  }
   if (P->scratch_elems_per_vec > 0) {
     if (int rc = dalloc(P->ws_allocs, &p, (size_t)(P->scratch_elems_per_vec * batch) * 16)) return rc;
     P->scratch = (double2*)p;
@@ -358,19 +393,19 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
     }
     if (blk)
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, P->czpart, st, &launches))
           return rc;
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, P->czpart, st, &launches))
         return rc;
   } else {
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, P->czpart, st, &launches))
         return rc;
     if (blk && !P->blocks.empty()) {
       CJT_CUDA_TRY(cudaMemsetAsync(P->yacc, 0, (size_t)(N1 * batch) * 8, st));
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, P->czpart, st, &launches))
           return rc;
     }
     if (rec) {

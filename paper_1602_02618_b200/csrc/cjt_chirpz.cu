@@ -11,11 +11,20 @@
 //   L <= 8192: one fused kernel per batch of vectors; FFT, spectrum product and
 //              inverse FFT stay in shared memory (no HBM traffic besides the
 //              real input slice and the real output slice).
-//   L >  8192: three passes of a four-step FFT (L = L1 x L2): column FFTs with
+//   2^14 <= L <= 2^17: one thread-block cluster of P CTAs per vector; each CTA
+//              holds Q = L/P points in shared memory (decimated n = r + P n2),
+//              runs a local Q-point FFT, and the P-point DFTs across the
+//              cluster, the spectrum product and the inverse P-point DFTs run
+//              over distributed shared memory, followed by the local inverse
+//              FFT: the whole Bluestein product stays on chip.
+//   L >  2^17: three passes of a four-step FFT (L = L1 x L2): column FFTs with
 //              the input diagonal fused into the load and the inter-step
 //              twiddle into the store; row FFT -> spectrum product -> row
 //              inverse FFT fused in one pass; column inverse FFTs with the
 //              output diagonal and the sum over m fused into the store.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "cjt_internal.cuh"
 
 namespace cjt {
@@ -28,13 +37,18 @@ struct FusedCfg {
   static constexpr int E = (L >= 4096) ? L : 4096;  // complex elements per CTA
   static constexpr int NG = E / L;                  // vectors per CTA
   static constexpr int T = E / 16;                  // threads per CTA
-  static constexpr int SMEM = NG * padded_len(L) * 16;
+  static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8;
 };
 
+// grid: (vector groups, output tiles, m groups).  Each CTA accumulates its
+// output tile over its m range and over all input tiles in shared memory.
+// part == nullptr: write out (= or +=); else plain-store the m-group partial
+// to part[z][b][offset + s] for the fixed-order combine kernel.
 template <int LOGL>
-__global__ void __launch_bounds__(FusedCfg<LOGL>::T)
+__global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
     k_chirpz_fused(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
-                   int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch) {
+                   int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch,
+                   double* __restrict__ part, int m_per_cta) {
   using Cfg = FusedCfg<LOGL>;
   constexpr int L = Cfg::L;
   constexpr int TPG = L / 16;
@@ -44,58 +58,174 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T)
   const int64_t b = (int64_t)blockIdx.x * Cfg::NG + grp;
   const bool valid = b < batch;
   double2* s = smem + grp * padded_len(L);
+  double* acc = reinterpret_cast<double*>(smem + Cfg::NG * padded_len(L)) + grp * L;
   const double* xb = x + (valid ? b : 0) * ldx + cz.p0;
-
-  double acc[16];
+  const int j = blockIdx.y;
+  const int64_t so = cz.tout[2 * j], sc = cz.tout[2 * j + 1];
+  const int m0 = blockIdx.z * m_per_cta;
+  const int m1 = min(m0 + m_per_cta, (int)cz.m_count);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  for (int i = 0; i < 16; ++i) acc[t + i * TPG] = 0.0;
 
-  for (int m = 0; m < cz.m_count; ++m) {
+  for (int m = m0; m < m1; ++m) {
     const double2* pre = cz.pre + (int64_t)m * cz.width;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int e = t + i * TPG;
-      double2 v = make_double2(0.0, 0.0);
-      if (valid && e < cz.width) {
-        const double xv = __ldg(xb + e);
-        const double2 p = __ldg(pre + e);
-        v = make_double2(xv * p.x, xv * p.y);
-      }
-      s[pad16(e)] = v;
+    const double2* post = cz.post + (int64_t)m * cz.count + so;
+    for (int ti = 0; ti < cz.n_in; ++ti) {
+      const int64_t to = cz.tin[2 * ti], tn = cz.tin[2 * ti + 1];
+      // forward FFT straight from global: x * pre (zero padded)
+      auto load_x = [&](int e) -> double2 {
+        if (valid && e < tn) {
+          const double xv = __ldg(xb + to + e);
+          const double2 p = __ldg(pre + to + e);
+          return make_double2(xv * p.x, xv * p.y);
+        }
+        return make_double2(0.0, 0.0);
+      };
+      fft_smem_io<LOGL, -1>(s, t, tw, load_x, SmemStore{s});
+      // inverse FFT: spectrum product fused into the first pass, output
+      // diagonal and the sum over (m, input tile) fused into the last pass
+      const double2* kh = cz.khat + ((int64_t)j * cz.n_in + ti) * L;
+      auto load_spec = [&](int e) -> double2 { return cmul(s[pad16(e)], __ldg(kh + e)); };
+      auto store_out = [&](int e, double2 y) {
+        if (e < sc) {
+          const double2 q = __ldg(post + e);
+          acc[e] += fma(q.x, y.x, -q.y * y.y);
+        }
+      };
+      fft_smem_io<LOGL, +1>(s, t, tw, load_spec, store_out);
     }
-    __syncthreads();
-    fft_smem<LOGL, -1>(s, t, tw);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int e = t + i * TPG;
-      s[pad16(e)] = cmul(s[pad16(e)], __ldg(cz.khat + e));
-    }
-    __syncthreads();
-    fft_smem<LOGL, +1>(s, t, tw);
-    const double2* post = cz.post + (int64_t)m * cz.count;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int e = t + i * TPG;
-      if (e < cz.count) {
-        const double2 y = s[pad16(e)];
-        const double2 q = __ldg(post + e);
-        acc[i] += fma(q.x, y.x, -q.y * y.y);
-      }
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (!valid) return;
-  double* ob = out + b * ldo + cz.q0;
+  if (part) {
+    double* pb = part + ((int64_t)blockIdx.z * batch + b) * cz.count + so;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = t + i * TPG;
+      if (e < sc) pb[e] = acc[e];
+    }
+    return;
+  }
+  double* ob = out + b * ldo + cz.q0 + so;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int e = t + i * TPG;
-    if (e < cz.count) ob[e] = cz.accumulate ? ob[e] + acc[i] : acc[i];
+    if (e < sc) ob[e] = cz.accumulate ? ob[e] + acc[e] : acc[e];
   }
+}
+
+// out[b][q0 + s] (+)= sum_z part[z][b][s], z in fixed order
+__global__ void k_chirpz_combine(const double* __restrict__ part, int nz, int64_t count,
+                                 int accumulate, double* __restrict__ out, int64_t ldo,
+                                 int64_t q0, int64_t batch) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b = blockIdx.y;
+  if (s >= count) return;
+  double acc = 0.0;
+  for (int z = 0; z < nz; ++z) acc += part[((int64_t)z * batch + b) * count + s];
+  double* o = out + b * ldo + q0 + s;
+  *o = accumulate ? *o + acc : acc;
 }
 
 // W_L^t = exp(-2 pi i t / L) from the two-level table (t < L)
 __device__ __forceinline__ double2 twiddle_L(const ChirpZDev& cz, int64_t t) {
   return cmul(__ldg(cz.tw_hi + (t >> 12)), __ldg(cz.tw_lo + (t & 4095)));
+}
+
+template <int LOGQ, int P>
+struct ClusterCfg {
+  static constexpr int Q = 1 << LOGQ;
+  static constexpr int T = Q / 16;
+  static constexpr int SMEM = padded_len(Q) * 16 + Q * 8;   // FFT buffer + output accumulator
+};
+
+template <int LOGQ, int P>
+__global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
+    k_chirpz_cluster(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
+                     int64_t ldx, double* __restrict__ out, int64_t ldo) {
+  namespace cg = cooperative_groups;
+  using Cfg = ClusterCfg<LOGQ, P>;
+  constexpr int Q = Cfg::Q, T = Cfg::T, NCOL = 16 / P;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double2 smem[];
+  double2* s = smem;
+  double* acc = reinterpret_cast<double*>(smem + padded_len(Q));  // [Q], thread-private slots
+  const int r = (int)cluster.block_rank();   // n1: this CTA's residue class
+  const int64_t b = blockIdx.x / P;
+  const int t = threadIdx.x;
+  const double* xb = x + b * ldx + cz.p0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[t + i * T] = 0.0;
+
+  for (int m = 0; m < cz.m_count; ++m) {
+    const double2* pre = cz.pre + (int64_t)m * cz.width;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n2 = t + i * T;
+      const int64_t pidx = r + (int64_t)P * n2;
+      double2 v = make_double2(0.0, 0.0);
+      if (pidx < cz.width) {
+        const double xv = __ldg(xb + pidx);
+        const double2 pp = __ldg(pre + pidx);
+        v = make_double2(xv * pp.x, xv * pp.y);
+      }
+      s[pad16(n2)] = v;
+    }
+    __syncthreads();
+    fft_smem<LOGQ, -1>(s, t, tw);
+    if (r > 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k2 = t + i * T;
+        s[pad16(k2)] = cmul(s[pad16(k2)], twiddle_L(cz, (int64_t)r * k2));
+      }
+    }
+    cluster.sync();
+    // P-point DFT across the cluster, spectrum product, inverse P-point DFT
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) {
+      const int k2 = r * (Q / P) + t + j * T;
+      double2 v[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) v[q] = cluster.map_shared_rank(s, q)[pad16(k2)];
+      dft_reg<P, -1>(v);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) v[k1] = cmul(v[k1], __ldg(cz.khat + k2 + (int64_t)Q * k1));
+      dft_reg<P, +1>(v);
+#pragma unroll
+      for (int q = 0; q < P; ++q) cluster.map_shared_rank(s, q)[pad16(k2)] = v[q];
+    }
+    cluster.sync();
+    if (r > 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k2 = t + i * T;
+        double2 w = twiddle_L(cz, (int64_t)r * k2);
+        w.y = -w.y;
+        s[pad16(k2)] = cmul(s[pad16(k2)], w);
+      }
+    }
+    __syncthreads();
+    fft_smem<LOGQ, +1>(s, t, tw);
+    const double2* post = cz.post + (int64_t)m * cz.count;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n2 = t + i * T;
+      const int64_t sidx = r + (int64_t)P * n2;
+      if (sidx < cz.count) {
+        const double2 y = s[pad16(n2)];
+        const double2 q = __ldg(post + sidx);
+        acc[n2] += fma(q.x, y.x, -q.y * y.y);
+      }
+    }
+  }
+  double* ob = out + b * ldo + cz.q0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int n2 = t + i * T;
+    const int64_t sidx = r + (int64_t)P * n2;
+    if (sidx < cz.count) ob[sidx] = cz.accumulate ? ob[sidx] + acc[n2] : acc[n2];
+  }
 }
 
 template <int LOG1>
@@ -260,16 +390,55 @@ int set_smem(K kernel, int bytes) {
 
 template <int LOGL>
 int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t ldx, double* out,
-              int64_t ldo, int64_t batch, cudaStream_t st) {
+              int64_t ldo, int64_t batch, double* part, cudaStream_t st, int* launches) {
   using Cfg = FusedCfg<LOGL>;
   static bool init = false;
   if (!init) {
     if (int rc = set_smem(k_chirpz_fused<LOGL>, Cfg::SMEM)) return rc;
     init = true;
   }
-  dim3 grid((unsigned)((batch + Cfg::NG - 1) / Cfg::NG));
-  k_chirpz_fused<LOGL><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch);
+  const int64_t groups = (batch + Cfg::NG - 1) / Cfg::NG;
+  // split the m terms over CTAs when the grid would not fill the GPU twice
+  const int msplit = (part && cz.m_count > 1 && groups * cz.n_out < 2 * 148) ? cz.m_count : 1;
+  dim3 grid((unsigned)groups, (unsigned)cz.n_out, (unsigned)msplit);
+  k_chirpz_fused<LOGL><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch,
+                                                         msplit > 1 ? part : nullptr,
+                                                         msplit > 1 ? 1 : cz.m_count);
   CJT_CUDA_TRY(cudaGetLastError());
+  *launches += 1;
+  if (msplit > 1) {
+    dim3 g2((unsigned)((cz.count + 255) / 256), (unsigned)batch);
+    k_chirpz_combine<<<g2, 256, 0, st>>>(part, msplit, cz.count, cz.accumulate, out, ldo, cz.q0, batch);
+    CJT_CUDA_TRY(cudaGetLastError());
+    *launches += 1;
+  }
+  return CJT_OK;
+}
+
+template <int LOGQ, int P>
+int run_cluster(const ChirpZDev& cz, const double2* tw, const double* x, int64_t ldx, double* out,
+                int64_t ldo, int64_t batch, cudaStream_t st) {
+  using Cfg = ClusterCfg<LOGQ, P>;
+  auto kern = k_chirpz_cluster<LOGQ, P>;
+  static bool init = false;
+  if (!init) {
+    if (int rc = set_smem(kern, Cfg::SMEM)) return rc;
+    if (P > 8) CJT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P * batch));
+  cfg.blockDim = dim3(Cfg::T);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CJT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, cz, tw, x, ldx, out, ldo));
   return CJT_OK;
 }
 
@@ -322,25 +491,35 @@ int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, dou
 
 }  // namespace
 
+bool cluster_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CJT_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
-                  double* out, int64_t ldo, int64_t batch, double2* scratch, cudaStream_t st,
-                  int* launches) {
+                  double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
+                  cudaStream_t st, int* launches) {
   if (batch <= 0) return CJT_OK;
   const int lg = cz.log2len;
   if (lg <= 13) {
+    switch (lg) {
+#define CJT_FUSED(K) case K: return run_fused<K>(cz, tw8192, x, ldx, out, ldo, batch, part, st, launches);
+      CJT_FUSED(4) CJT_FUSED(5) CJT_FUSED(6) CJT_FUSED(7) CJT_FUSED(8) CJT_FUSED(9) CJT_FUSED(10)
+      CJT_FUSED(11) CJT_FUSED(12) CJT_FUSED(13)
+#undef CJT_FUSED
+      default: return fail(CJT_EINVAL, "chirp-z length below 16");
+    }
+  }
+  if (lg <= 17 && cluster_enabled()) {
     *launches += 1;
     switch (lg) {
-      case 4: return run_fused<4>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 5: return run_fused<5>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 6: return run_fused<6>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 7: return run_fused<7>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 8: return run_fused<8>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 9: return run_fused<9>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 10: return run_fused<10>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 11: return run_fused<11>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 12: return run_fused<12>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      case 13: return run_fused<13>(cz, tw8192, x, ldx, out, ldo, batch, st);
-      default: return fail(CJT_EINVAL, "chirp-z length below 16");
+      case 14: return run_cluster<12, 4>(cz, tw8192, x, ldx, out, ldo, batch, st);
+      case 15: return run_cluster<12, 8>(cz, tw8192, x, ldx, out, ldo, batch, st);
+      case 16: return run_cluster<12, 16>(cz, tw8192, x, ldx, out, ldo, batch, st);
+      default: return run_cluster<13, 16>(cz, tw8192, x, ldx, out, ldo, batch, st);
     }
   }
   *launches += 3;

@@ -133,30 +133,79 @@ __device__ __forceinline__ void dft_reg(double2* v) {
   dft_levels<DIR, 2, R>(v);
 }
 
+
+#ifndef CJT_TW_MODE
+#define CJT_TW_MODE 1
+#endif
+
+// v[r] *= w^r for r = 1..R-1 with w = tw[u] (conjugated for DIR > 0);
+// w^(2^j) are read from the table (u 2^j < 8192 since r k < NS R <= 8192).
+template <int R, int DIR>
+__device__ __forceinline__ void twiddle_powers(double2* v, const double2* __restrict__ tw, int u) {
+  double2 p[16];
+  p[1] = __ldg(&tw[u]);
+  if constexpr (R > 2) p[2] = __ldg(&tw[2 * u]);
+  if constexpr (R > 4) p[4] = __ldg(&tw[4 * u]);
+  if constexpr (R > 8) p[8] = __ldg(&tw[8 * u]);
+  if constexpr (DIR > 0) {
+#pragma unroll
+    for (int j = 1; j < R; j <<= 1) p[j].y = -p[j].y;
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    if ((r & (r - 1)) != 0) {  // not a power of two: r = hi + lo
+      const int hi = 1 << (31 - __clz(r));
+      p[r] = cmul(p[hi], p[r - hi]);
+    }
+    v[r] = cmul(v[r], p[r]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Shared-memory Stockham FFT of length L = 2^LOGL (4 <= LOGL <= 13), executed
-// by the L/16 threads t of one group (each holds 16 elements per pass; radix
-// 16 passes, the last pass radix 2/4/8/16).  `tw` is the 8192-entry table
-// exp(-2 pi i u / 8192).  Every thread of the CTA must call it with the same
-// LOGL (it synchronises the CTA between passes).  Result in natural order.
-template <int LOGL, int DIR, int PASS>
-__device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __restrict__ tw) {
-  constexpr int NP = (LOGL + 3) / 4;
+// by the L/EPT threads t of one group, EPT = 2^LEPT elements per thread (radix
+// EPT passes, the last pass radix L / EPT^(passes-1)).  `tw` is the
+// 8192-entry table exp(-2 pi i u / 8192).  Every thread of the CTA must call
+// it with the same LOGL (it synchronises the CTA between passes).  Result in
+// natural order.
+// First-pass loader / last-pass storer hooks: the default reads and writes
+// the shared buffer; fused kernels substitute global loads (with the input
+// diagonal), the spectrum product, or the output accumulation, saving a
+// shared-memory round trip each.
+struct SmemLoad {
+  const double2* s;
+  __device__ __forceinline__ double2 operator()(int e) const { return s[pad16(e)]; }
+};
+struct SmemStore {
+  double2* s;
+  __device__ __forceinline__ void operator()(int e, double2 v) const { s[pad16(e)] = v; }
+};
+
+template <int LOGL, int DIR, int LEPT, int PASS, class LoadF, class StoreF>
+__device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __restrict__ tw,
+                                         const LoadF& first_load, const StoreF& last_store) {
+  constexpr int NP = (LOGL + LEPT - 1) / LEPT;
   if constexpr (PASS < NP) {
-    constexpr int LR = (PASS < NP - 1) ? 4 : (LOGL - 4 * (NP - 1));
+    constexpr int EPT = 1 << LEPT;
+    constexpr int LR = (PASS < NP - 1) ? LEPT : (LOGL - LEPT * (NP - 1));
     constexpr int R = 1 << LR;
     constexpr int L = 1 << LOGL;
-    constexpr int LNS = 4 * PASS;
+    constexpr int LNS = LEPT * PASS;
     constexpr int NS = 1 << LNS;
-    constexpr int NBF = 16 / R;
+    constexpr int NBF = EPT / R;
     constexpr int STRIDE = L / R;
-    constexpr int TPG = L / 16;
-    double2 v[16];
+    constexpr int TPG = L / EPT;
+    double2 v[EPT];
 #pragma unroll
     for (int q = 0; q < NBF; ++q) {
       const int j = t + q * TPG;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q * R + r] = s[pad16(j + r * STRIDE)];
+      for (int r = 0; r < R; ++r) {
+        if constexpr (PASS == 0)
+          v[q * R + r] = first_load(j + r * STRIDE);
+        else
+          v[q * R + r] = s[pad16(j + r * STRIDE)];
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -165,27 +214,46 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __res
       const int k = j & (NS - 1);
       if constexpr (PASS > 0) {
         constexpr int SH = 13 - (LNS + LR);
+#if CJT_TW_MODE == 0
 #pragma unroll
         for (int r = 1; r < R; ++r) {
           double2 w = __ldg(&tw[(r * k) << SH]);
           if (DIR > 0) w.y = -w.y;
           v[q * R + r] = cmul(v[q * R + r], w);
         }
+#else
+        // powers of w = W^k from the tabulated w, w^2, w^4, w^8 (at most three
+        // rounded products per power)
+        twiddle_powers<R, DIR>(&v[q * R], tw, k << SH);
+#endif
       }
       dft_reg<R, DIR>(&v[q * R]);
       const int base = ((j - k) << LR) + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) s[pad16(base + r * NS)] = v[q * R + r];
+      for (int r = 0; r < R; ++r) {
+        if constexpr (PASS == NP - 1)
+          last_store(base + r * NS, v[q * R + r]);
+        else
+          s[pad16(base + r * NS)] = v[q * R + r];
+      }
     }
     __syncthreads();
-    fft_pass<LOGL, DIR, PASS + 1>(s, t, tw);
+    fft_pass<LOGL, DIR, LEPT, PASS + 1>(s, t, tw, first_load, last_store);
   }
 }
 
-template <int LOGL, int DIR>
+template <int LOGL, int DIR, int LEPT = 4>
 __device__ __forceinline__ void fft_smem(double2* s, int t, const double2* __restrict__ tw) {
+  static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
+  fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, SmemLoad{s}, SmemStore{s});
+}
+
+// FFT with a custom first-pass source and last-pass sink (see SmemLoad/SmemStore)
+template <int LOGL, int DIR, class LoadF, class StoreF>
+__device__ __forceinline__ void fft_smem_io(double2* s, int t, const double2* __restrict__ tw,
+                                            const LoadF& ld, const StoreF& st) {
   static_assert(LOGL >= 4 && LOGL <= 13, "smem FFT length out of range");
-  fft_pass<LOGL, DIR, 0>(s, t, tw);
+  fft_pass<LOGL, DIR, 4, 0>(s, t, tw, ld, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -200,6 +268,9 @@ struct ChirpZDev {
   const double2* khat;      // fused: natural order; multipass: [k1][k2] = khat[k1 + L1 k2]
   const double2* tw_hi;     // multipass: exp(-2 pi i (a 4096) / L)
   const double2* tw_lo;     // multipass: exp(-2 pi i b / L), b < 4096
+  int32_t n_in, n_out;      // tiling (fused path only; 1 x 1 otherwise)
+  const int64_t* tin;       // [n_in][2] (offset, width)
+  const int64_t* tout;      // [n_out][2] (offset, count)
 };
 
 struct RecRowsDev {
@@ -229,13 +300,19 @@ constexpr int FWD_KS = 32;      // degrees per forward pipeline stage
 constexpr int INV_DT = 128;     // degrees per inverse CTA tile (4 warps x 32 degrees)
 constexpr int INV_RT = 32;      // grid rows per inverse pipeline stage (= row tile)
 
+// Cluster (DSMEM) chirp-z path for 2^14 <= L <= 2^17; opt-in (CJT_CLUSTER=1)
+// until it beats the multi-pass path on the benchmark configurations.
+bool cluster_enabled();
+
 // vectors per CTA tile of the DMMA contractions, chosen from the batch size
 inline int pick_vt(int64_t batch) { return batch >= 64 ? 64 : (batch >= 32 ? 32 : 16); }
 
 // ---------------------------------------------------------------------------
 // launchers (host)
+// scratch: multi-pass buffer (batch x m x L complex); part: m-split partial
+// sums (m x batch x count doubles), used when too few CTAs would run.
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
-                  double* out, int64_t ldo, int64_t batch, double2* scratch,
+                  double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
                   cudaStream_t st, int* launches);
 
 int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,

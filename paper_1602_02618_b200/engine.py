@@ -99,6 +99,10 @@ class _DevicePlan:
             d.accumulate = 1 if cz.accumulate else 0
             d.pre = arr(cz.pre, np.complex128)
             d.post = arr(cz.post, np.complex128)
+            d.n_tiles_in = len(cz.tiles_in)
+            d.n_tiles_out = len(cz.tiles_out)
+            d.tiles_in = arr(cz.tiles_in, np.int64)
+            d.tiles_out = arr(cz.tiles_out, np.int64)
             d.kernel_hat = arr(cz.kernel_hat, np.complex128)
             return d
 

@@ -509,6 +509,10 @@ class ChirpZ:
 
         out[b, q0+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
         z_{b,m}[s] = sum_t exp(i pi (p0+t)(q0+s)/G) pre[m, t] x[b, p0+t].
+
+    The index rectangle (input t < width) x (output s < count) may be tiled:
+    tile (j, i) covers inputs tiles_in[i] and outputs tiles_out[j] and is one
+    Bluestein convolution of length `length` with spectrum kernel_hat[j, i].
     """
 
     g: int
@@ -519,34 +523,90 @@ class ChirpZ:
     length: int
     pre: np.ndarray      # (M, width) complex128: scaling * chirp(p)
     post: np.ndarray     # (M, count) complex128: scaling * chirp(q)
-    kernel_hat: np.ndarray  # (length,) complex128: FFT(conj chirp of q-p) / length
+    kernel_hat: np.ndarray  # (n_out, n_in, length) complex128, 1/length folded in
     accumulate: bool
+    tiles_in: np.ndarray = None   # (n_in, 2) int64: (offset, width) relative to p0
+    tiles_out: np.ndarray = None  # (n_out, 2) int64: (offset, count) relative to q0
 
     @property
     def m_count(self) -> int:
         return self.pre.shape[0]
 
 
-def chirpz(g: int, p0: int, width: int, q0: int, count: int,
-           pre_scale: np.ndarray, post_scale: np.ndarray, accumulate: bool) -> ChirpZ:
-    """Build the Bluestein layout of sum_p x_p e^{i pi p q/G}.
-    pre_scale/post_scale: (M, width)/(M, count) real or complex diagonals."""
-    length = _next_pow2(width + count - 1)
-    pidx = np.arange(p0, p0 + width, dtype=np.int64)
-    qidx = np.arange(q0, q0 + count, dtype=np.int64)
-    pre = np.atleast_2d(pre_scale) * chirp(pidx, g)[None, :]
-    post = np.atleast_2d(post_scale) * chirp(qidx, g)[None, :]
-    # kernel conj(chirp(d)), d = q - p = (q0 - p0) + s - t, cyclic over length
+FUSED_MAX = 8192        # largest Bluestein length kept entirely in one CTA's shared memory
+
+
+def _cost_per_point(length: int) -> float:
+    """Measured B200 cost (ps per point per term per vector, config-2 launch
+    list, profiles/) of one Bluestein convolution of this length: on-chip
+    fused tiles vs the multi-pass (HBM round-trip) path."""
+    if length <= 4096:
+        return 19.0
+    if length <= FUSED_MAX:
+        return 21.7
+    lg = length.bit_length() - 1
+    return 31.0 + 2.0 * max(0, lg - 15)
+
+
+def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
+    """FFT of the cyclic kernel conj(chirp(q - p)), d = (q0 - p0) + s - t, / length."""
     ker = np.zeros(length, dtype=np.complex128)
     off = q0 - p0
     ker[:count] = np.conj(chirp(off + np.arange(count, dtype=np.int64), g))
     if width > 1:
         ker[length - width + 1:] = np.conj(chirp(off - np.arange(width - 1, 0, -1, dtype=np.int64), g))
-    khat = np.fft.fft(ker) / length
+    return np.fft.fft(ker) / length
+
+
+def _split(n: int, parts: int) -> np.ndarray:
+    edges = (np.arange(parts + 1, dtype=np.int64) * n) // parts
+    return np.stack([edges[:-1], edges[1:] - edges[:-1]], axis=1)
+
+
+def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
+    """Choose (length, n_in, n_out) for a width x count chirp-z: one untiled
+    power-of-two Bluestein, or a grid of on-chip tiles, by measured cost."""
+    whole = _next_pow2(width + count - 1)
+    best = (whole * _cost_per_point(whole), whole, 1, 1)
+    lc = 1024
+    while lc <= fused_max:
+        for n_in in range(1, 65):
+            wc = -(-width // n_in)
+            if wc >= lc:
+                continue
+            n_out = -(-count // (lc - wc + 1))
+            if n_in * n_out > 256:
+                continue
+            cost = n_in * n_out * lc * _cost_per_point(lc)
+            if cost < best[0]:
+                best = (cost, lc, n_in, n_out)
+        lc *= 2
+    return best[1:]
+
+
+def chirpz(g: int, p0: int, width: int, q0: int, count: int,
+           pre_scale: np.ndarray, post_scale: np.ndarray, accumulate: bool,
+           tiled: bool = True) -> ChirpZ:
+    """Build the Bluestein layout of sum_p x_p e^{i pi p q/G}.
+    pre_scale/post_scale: (M, width)/(M, count) real or complex diagonals."""
+    pidx = np.arange(p0, p0 + width, dtype=np.int64)
+    qidx = np.arange(q0, q0 + count, dtype=np.int64)
+    pre = np.atleast_2d(pre_scale) * chirp(pidx, g)[None, :]
+    post = np.atleast_2d(post_scale) * chirp(qidx, g)[None, :]
+    if tiled:
+        length, n_in, n_out = tile_layout(width, count)
+    else:
+        length, n_in, n_out = _next_pow2(width + count - 1), 1, 1
+    tin = _split(width, n_in)
+    tout = _split(count, n_out)
+    khat = np.empty((n_out, n_in, length), dtype=np.complex128)
+    for j, (so, sc) in enumerate(tout):
+        for i, (to, tw) in enumerate(tin):
+            khat[j, i] = _spectrum(g, p0 + int(to), int(tw), q0 + int(so), int(sc), length)
     return ChirpZ(g, p0, width, q0, count, length,
                   np.ascontiguousarray(pre, dtype=np.complex128),
                   np.ascontiguousarray(post, dtype=np.complex128),
-                  khat.astype(np.complex128), accumulate)
+                  khat, accumulate, tin, tout)
 
 
 # ---------------------------------------------------------------------------
