@@ -1,0 +1,126 @@
+"""GPU: the reference-signature backend plugin, determinism, and full-size
+properties (sizes where the CPU oracle is too slow to run per test)."""
+import numpy as np
+import pytest
+
+import cjt_oracle as O
+import paper_1602_02618_b200 as cj
+from paper_1602_02618_b200 import backend
+from paper_1602_02618_b200 import planner as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _tables(p, n):
+    t = P.recurrence_tables(p, n + 1)
+    th = P.angle_grid(n)
+    return t, th, P.region_codes(th)
+
+
+def test_plugin_clenshaw_points_bitwise(cuda):
+    # same arithmetic order and the same libm angles as _kernels_cy.pyx:17-122
+    p = P.JacobiParameters(0.3, -0.45)
+    n = 1500
+    t, th, reg = _tables(p, n)
+    cuts = np.full(n + 1, n + 1, dtype=np.int64)
+    cuts[100:1300] = 211
+    cuts[400:1000] = 90
+    c = O.seeded_vector(4, 1, n)
+    got = np.empty(n + 1)
+    ref = np.empty(n + 1)
+    args = (t.A, t.B, t.C, t.rb_plus, t.rb_minus, t.rb_plus_inv, t.rb_minus_inv, c, th, cuts, reg)
+    backend.clenshaw_points(*args, got)
+    O.clenshaw_points(*args, ref)
+    assert np.array_equal(got, ref)
+
+
+def test_plugin_transpose_accumulate(cuda):
+    p = P.JacobiParameters(-0.25, 0.4)
+    n = 2 * 700
+    t, th, reg = _tables(p, n)
+    cuts = np.full(n + 1, n + 1, dtype=np.int64)
+    cuts[300:1100] = 240
+    wv = np.random.default_rng(5).standard_normal(n + 1)
+    args = (t.A, t.B, t.C, t.rf_plus, t.rf_minus, t.rf_plus_inv, t.rf_minus_inv, wv, th, cuts, reg)
+    got = np.full(n + 1, 0.5)
+    ref = np.full(n + 1, 0.5)
+    backend.transpose_accumulate(*args, got)
+    O.transpose_accumulate(*args, ref)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.sum(np.abs(wv)) * 10
+
+
+def test_reference_engine_runs_on_cuda_backend(cuda):
+    ref = O.reference_package()
+    if ref is None:
+        pytest.skip("oracle/_ref (the built reference) is not present")
+    from chebjac import backend as rb
+    from chebjac import engine
+    cj.register_with(rb)
+    p = ref.JacobiParameters(-0.25, 0.4)
+    n = 2047
+    c = O.seeded_vector(2, 0, n)
+    fp, ip = engine.plan("forward", p, n), engine.plan("inverse", p, n)
+    prev = rb.set_kernel_backend("cython")
+    want_f = engine.forward(fp, ref.jacobi(p, c)).data
+    want_i = engine.inverse(ip, ref.chebyshev(want_f)).data
+    rb.set_kernel_backend("cuda")
+    try:
+        got_f = engine.forward(fp, ref.jacobi(p, c)).data
+        got_i = engine.inverse(ip, ref.chebyshev(want_f)).data
+    finally:
+        rb.set_kernel_backend(prev)
+    assert O.parity(got_f, want_f, c) <= 1e-15
+    assert O.parity(got_i, want_i, want_f) <= 1e-13
+
+
+def test_reexecution_bit_identical(cuda):
+    import torch
+    p = cj.JacobiParameters(-0.25, 0.4)
+    n = 16383
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = torch.from_numpy(np.stack([O.seeded_vector(2, v, n) for v in range(8)])).to(cuda)
+    f1 = cj.forward_batched(fp, c).clone()
+    i1 = cj.inverse_batched(ip, f1).clone()
+    f2 = cj.forward_batched(fp, c)
+    i2 = cj.inverse_batched(ip, f2)
+    assert torch.equal(f1, f2) and torch.equal(i1, i2)
+    # batch composition does not change any vector's result (no cross-vector reduction)
+    f3 = cj.forward_batched(fp, c[3:4].contiguous())
+    assert torch.equal(f3[0], f1[3])
+
+
+def test_config3_full_batch_slice_vs_golden_and_roundtrip(cuda):
+    import torch
+    from conftest import load_golden
+    g = load_golden("cfg3_full")
+    p = cj.JacobiParameters(0.5, 0.5)
+    n = 4095
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    # 256 vectors: the two golden ones first, then more of the seeded stream
+    c = np.stack([O.seeded_vector(3, v, n) for v in range(256)])
+    f = cj.forward_batched(fp, torch.from_numpy(c).to(cuda))
+    i = cj.inverse_batched(ip, f).cpu().numpy()
+    f = f.cpu().numpy()
+    for v in range(2):
+        assert O.parity(f[v], g["fwd"][v], c[v]) <= 1e-12
+    for v in range(0, 256, 51):
+        assert O.parity(i[v], c[v], c[v]) <= 1e-12   # round trip
+
+
+@pytest.mark.parametrize("config", [2, 4])
+def test_full_size_linearity_and_roundtrip(cuda, config):
+    import torch
+    wl = O.CONFIGS[config]
+    n = wl["n"]
+    p = cj.JacobiParameters(wl["alpha"], wl["beta"])
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = np.stack([O.seeded_vector(config, v, n) for v in range(2)])
+    mix = 0.75 * c[0] - 1.25 * c[1]
+    x = torch.from_numpy(np.stack([c[0], c[1], mix])).to(cuda)
+    f = cj.forward_batched(fp, x)
+    i = cj.inverse_batched(ip, f).cpu().numpy()
+    f = f.cpu().numpy()
+    l1 = np.abs(mix).sum()
+    assert np.max(np.abs(f[2] - (0.75 * f[0] - 1.25 * f[1]))) <= 1e-13 * l1
+    for v in range(3):
+        assert O.parity(i[v], [c[0], c[1], mix][v], [c[0], c[1], mix][v]) <= 1e-11
