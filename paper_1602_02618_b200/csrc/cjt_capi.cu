@@ -70,6 +70,7 @@ struct cjt_plan {
   InvItem* iitems = nullptr;
   int64_t n_iitems = 0;
   int32_t* tile_ids = nullptr;
+  void* inv_gen = nullptr;      // K2 generator stream (GenState per row tile x thread)
   int32_t* dt_slot0 = nullptr;
   int32_t* dt_nslot = nullptr;
   int64_t n_islots = 0;
@@ -292,7 +293,7 @@ int build_items(cjt_plan* P, int64_t batch) {
     }
     const int64_t cs = std::max<int64_t>(1, (int64_t)std::ceil((double)total_active * nbt / target));
     std::vector<InvItem> items;
-    std::vector<int32_t> ids, s0((size_t)nd), ns((size_t)nd);
+    std::vector<int32_t> ids, gn0, s0((size_t)nd), ns((size_t)nd);
     int32_t slot = 0;
     for (int64_t d = 0; d < nd; ++d) {
       s0[d] = slot;
@@ -306,7 +307,10 @@ int build_items(cjt_plan* P, int64_t batch) {
         InvItem it{};
         it.n0 = (int32_t)(d * INV_DT);
         it.t_begin = (int32_t)ids.size();
-        for (int64_t a = a0; a < a1; ++a) ids.push_back(active[d][a]);
+        for (int64_t a = a0; a < a1; ++a) {
+          ids.push_back(active[d][a]);
+          gn0.push_back((int32_t)(d * INV_DT));
+        }
         it.t_count = (int32_t)(a1 - a0);
         it.slot = slot++;
         items.push_back(it);
@@ -318,6 +322,14 @@ int build_items(cjt_plan* P, int64_t batch) {
                      [](const InvItem& a, const InvItem& b) { return a.t_count > b.t_count; });
     if (int rc = upload_ws(P, &P->iitems, items)) return rc;
     if (int rc = upload_ws(P, &P->tile_ids, ids)) return rc;
+    int32_t* d_gn0 = nullptr;
+    if (int rc = upload_ws(P, &d_gn0, gn0)) return rc;
+    void* gp = nullptr;
+    const int64_t total = (int64_t)ids.size();
+    if (int rc = dalloc(P->ws_allocs, &gp, (size_t)std::max<int64_t>(total, 1) * 128 * GEN_STATE_BYTES)) return rc;
+    P->inv_gen = gp;
+    if (int rc = launch_build_inv_gen(P->rows, P->ck_off, P->ck, P->tile_ids, d_gn0, total, gp, 0)) return rc;
+    CJT_CUDA_TRY(cudaDeviceSynchronize());
     if (int rc = upload_ws(P, &P->dt_slot0, s0)) return rc;
     if (int rc = upload_ws(P, &P->dt_nslot, ns)) return rc;
     P->n_iitems = (int64_t)items.size();
@@ -409,7 +421,7 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
           return rc;
     }
     if (rec) {
-      if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
+      if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
                                       P->vals, G1, batch, P->vt, P->part, st)) return rc;
       if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
                                          batch, st)) return rc;
@@ -496,7 +508,7 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   const double* src[7] = {d->A, d->B, d->C, d->rf_plus, d->rf_minus, d->rf_plus_inv, d->rf_minus_inv};
   for (int k = 0; k < 7; ++k)
     if (int rc = upload(A, &t[k], src[k], tl)) return rc;
-  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6]};
+  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
 
   // recurrence checkpoints every CK degrees
   std::vector<int64_t> off((size_t)nr);
@@ -676,7 +688,7 @@ int cjt_clenshaw_points(const double* A, const double* B, const double* C, const
   void* p;
   if (int rc = dalloc(tmp, &p, (size_t)n_points * 8)) return rc;
   dout = (double*)p;
-  RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr};
+  RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr, (int64_t)tl};
   if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, dx, dxm, dreg, dcut, dout, n_points, 0))
     return rc;
   CJT_CUDA_TRY(cudaMemcpy(out, dout, (size_t)n_points * 8, cudaMemcpyDeviceToHost));
@@ -718,7 +730,7 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   const double* src[7] = {A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv};
   for (int k = 0; k < 7; ++k)
     if (int rc = upload(Al, &t[k], src[k], tl)) return rc;
-  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6]};
+  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
   std::vector<int64_t> off((size_t)n_points);
   int64_t tot = 0;
   for (int64_t i = 0; i < n_points; ++i) {
@@ -738,7 +750,7 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   if (int rc = upload(Al, &dwv, wv, (size_t)n_points)) return rc;
   if (int rc = dalloc(Al, &p, ones.size() * 8)) return rc;
   dres = (double*)p;
-  if (int rc = launch_rec_inverse(P->rows, P->tab, P->ck_off, P->ck, P->iitems, P->n_iitems, P->tile_ids,
+  if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
                                   dwv, n_points, 1, P->vt, P->part, 0)) return rc;
   if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, P->part, nullptr, dscal, dres,
                                      P->n + 1, 1, 0)) return rc;

@@ -283,6 +283,7 @@ struct RecRowsDev {
 
 struct RecTablesDev {
   const double *A, *B, *C, *rfp, *rfm, *rfpi, *rfmi;
+  int64_t n_tab;   // entries per table
 };
 
 // forward split-K work item: rows [row0, row0+nrows) x degrees [n_begin, n_end)
@@ -324,10 +325,14 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
 int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nslot,
                               int64_t nrows, const double* part, double* vals, int64_t ldv,
                               int64_t batch, cudaStream_t st);
-int launch_rec_inverse(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
-                       const double2* ck, const InvItem* items, int64_t n_items,
-                       const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch,
-                       int vt, double* part, cudaStream_t st);
+// K2 generator stream: 32 bytes per (work-list row tile, generator thread)
+constexpr int GEN_STATE_BYTES = 32;
+int launch_build_inv_gen(const RecRowsDev& rows, const int64_t* ck_off, const double2* ck,
+                         const int32_t* ids, const int32_t* gn0, int64_t total, void* out,
+                         cudaStream_t st);
+int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, const InvItem* items,
+                       int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
+                       int64_t batch, int vt, double* part, cudaStream_t st);
 int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,
                           const double* part, const double* blocks_acc, const double* scal,
                           double* out, int64_t ldo, int64_t batch, cudaStream_t st);

@@ -71,6 +71,66 @@ __device__ __forceinline__ void load_state(const RecRowsDev& rows, const int64_t
   }
 }
 
+// Recurrence tables of a degree window staged in shared memory:
+// rows 0..6 = A, B, C, rf+, rf-, 1/rf+, 1/rf-, each `span` entries from n_lo.
+__device__ __forceinline__ const double* table_row(const RecTablesDev& t, int r) {
+  return r == 0 ? t.A : r == 1 ? t.B : r == 2 ? t.C : r == 3 ? t.rfp : r == 4 ? t.rfm : r == 5 ? t.rfpi : t.rfmi;
+}
+struct TabWin {
+  const double* t;   // [7][span]
+  int span;
+};
+// degree n_lo + nl -> n_lo + nl + 1 with window tables (same rounding as rec_step)
+__device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w, int nl,
+                                             double& s0, double& s1) {
+  const double a = w.t[nl];
+  const double c = w.t[2 * w.span + nl];
+  if (reg == 0) {
+    const double bb = w.t[w.span + nl];
+    const double pn = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(a, xx), bb), s1), __dmul_rn(c, s0));
+    s0 = s1;
+    s1 = pn;
+  } else {
+    const int o = reg > 0 ? 3 : 4;
+    const double rf = w.t[o * w.span + nl];
+    const double rfi = w.t[(o + 2) * w.span + nl];
+    const double d = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, xx), s0), __dmul_rn(c, s1)), rfi);
+    s0 = __dmul_rn(__dadd_rn(s0, d), rf);
+    s1 = d;
+  }
+}
+
+// Per-(row tile, generator thread) start state of K2, laid out densely in
+// work-list order so the kernel streams it with one coalesced load per stage.
+struct GenState {
+  double s0, s1;   // recurrence state at degree nstart
+  double xx;       // x (interior) or x - x0 (endpoint regions)
+  int64_t cutreg;  // cut * 4 + (region + 1); cut = 0 marks an idle generator
+};
+
+__global__ void k_build_inv_gen(RecRowsDev rows, const int64_t* __restrict__ ck_off,
+                                const double2* __restrict__ ck, const int32_t* __restrict__ ids,
+                                const int32_t* __restrict__ gn0, int64_t total,
+                                GenState* __restrict__ out) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= total * 128) return;
+  const int64_t g = gi / 128;
+  const int tid = (int)(gi % 128);
+  const int64_t i = (int64_t)ids[g] * INV_RT + (tid >> 2);
+  const int64_t nstart = gn0[g] + CK * (tid & 3);
+  GenState st{0.0, 0.0, 0.0, 0};
+  if (i < rows.nrows) {
+    const int64_t cut = rows.cut[i];
+    const int reg = rows.reg[i];
+    if (cut > nstart) {
+      load_state(rows, ck_off, ck, i, nstart, reg, st.s0, st.s1);
+      st.xx = reg == 0 ? rows.x[i] : rows.xm[i];
+      st.cutreg = cut * 4 + (reg + 1);
+    }
+  }
+  out[gi] = st;
+}
+
 __global__ void k_checkpoints(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
                               double2* __restrict__ ck) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,6 +186,7 @@ __global__ void __launch_bounds__(128)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
   double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + 2 * FWD_KS * PT);
+  double(*Ts)[7 * FWD_KS] = reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + 2 * FWD_KS * PT + 2 * VT * CS);
   const FwdItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -134,22 +195,32 @@ __global__ void __launch_bounds__(128)
   const int64_t gi = it.row0 + tid;
   const bool live = tid < it.nrows;
   int reg = 0;
-  double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
+  double xx = 0.0, s0 = 0.0, s1 = 0.0;
   int64_t cut = 0;
   if (live) {
     reg = rows.reg[gi];
-    x = rows.x[gi];
-    xm = rows.xm[gi];
+    xx = reg == 0 ? rows.x[gi] : rows.xm[gi];
     cut = rows.cut[gi];
     if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
   }
   // generate degrees n0+k0 .. n0+k0+KN-1 of this thread's row into Pt[buf]
+  // (tables of the stage's 32 degrees come from Ts[buf])
   auto generate = [&](int buf, int64_t n0, int k0, auto kn) {
+    const TabWin w{Ts[buf], FWD_KS};
 #pragma unroll
     for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
       const int64_t n = n0 + k;
       Pt[buf][k][tid] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-      if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
+      if (n + 1 < cut) rec_step_win(reg, xx, w, k, s0, s1);
+    }
+  };
+  auto stage_tables = [&](int buf, int64_t n0) {
+    for (int idx = tid; idx < 7 * FWD_KS; idx += 128) {
+      const int r = idx / FWD_KS, k = idx % FWD_KS;
+      const int64_t n = n0 + k;
+      const bool ok = n < tab.n_tab;
+      const double* src = table_row(tab, r);
+      cp_async8(&Ts[buf][idx], ok ? src + n : src, ok);
     }
   };
   auto stage_c = [&](int buf, int64_t n0) {
@@ -172,8 +243,15 @@ __global__ void __launch_bounds__(128)
 
   const int nstages = (it.n_end - it.n_begin) / FWD_KS;
   using Four = std::integral_constant<int, 4>;
+  stage_tables(0, it.n_begin);
   stage_c(0, it.n_begin);
+  cp_async_wait_all();
+  __syncthreads();
   for (int k0 = 0; k0 < FWD_KS; k0 += 4) generate(0, it.n_begin, k0, Four{});
+  if (nstages > 1) {
+    stage_tables(1, it.n_begin + FWD_KS);
+    cp_async_commit();
+  }
   cp_async_wait_all();
   __syncthreads();
   const int ar = lane >> 2, ak = lane & 3;
@@ -181,7 +259,13 @@ __global__ void __launch_bounds__(128)
     const int buf = sidx & 1;
     const bool more = sidx + 1 < nstages;
     const int64_t nn = it.n_begin + (int64_t)(sidx + 1) * FWD_KS;
-    if (more) stage_c(buf ^ 1, nn);
+    // Ts[buf] (stage sidx's tables) is free: refill it with stage sidx+2's,
+    // consumed next iteration after this iteration's closing wait + barrier
+    if (sidx + 2 < nstages) stage_tables(buf, it.n_begin + (int64_t)(sidx + 2) * FWD_KS);
+    if (more)
+      stage_c(buf ^ 1, nn);
+    else
+      cp_async_commit();
 #pragma unroll
     for (int kk = 0; kk < FWD_KS / 4; ++kk) {
       // four recurrence steps of the next stage overlap this k-step's DMMAs
@@ -235,49 +319,46 @@ __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
 //   cp.async; stages are double-buffered.
 template <int VT>
 __global__ void __launch_bounds__(128)
-    k_rec_inverse_mma(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-                      const double2* __restrict__ ck, const InvItem* __restrict__ items,
-                      const int32_t* __restrict__ tile_ids, const double* __restrict__ wv,
-                      int64_t ldw, int64_t batch, double* __restrict__ part) {
+    k_rec_inverse_mma(RecTablesDev tab, const GenState* __restrict__ gen, int64_t nrows,
+                      const InvItem* __restrict__ items, const int32_t* __restrict__ tile_ids,
+                      const double* __restrict__ wv, int64_t ldw, int64_t batch,
+                      double* __restrict__ part) {
   constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
   constexpr int WS = INV_RT + 4;
   constexpr int NT = VT / 8;
+  constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + 2 * INV_RT * PR);
+  double* Tw = smem_rec + 2 * INV_RT * PR + 2 * VT * WS;   // [7][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grow = tid >> 2, gq = tid & 3;   // generator: row in tile, degree chunk
 
-  // generator for the next row tile: row grow, degrees n0 + 32 gq + [0, 32)
-  int64_t g_cut = 0;
-  int g_reg = 0;
-  double g_x = 0.0, g_xm = 0.0, g_s0 = 0.0, g_s1 = 0.0;
-  auto gen_begin = [&](int64_t r0) {
-    const int64_t i = r0 + grow;
-    const int64_t nstart = it.n0 + CK * gq;
-    g_cut = 0;
-    g_reg = 0;
-    g_s0 = g_s1 = 0.0;
-    if (i < rows.nrows) {
-      g_cut = rows.cut[i];
-      if (g_cut > nstart) {
-        g_reg = rows.reg[i];
-        g_x = rows.x[i];
-        g_xm = rows.xm[i];
-        load_state(rows, ck_off, ck, i, nstart, g_reg, g_s0, g_s1);
-      }
-    }
-  };
-  auto generate = [&](int buf, int k0, auto kn) {
-    const int64_t nstart = it.n0 + CK * gq;
+  for (int idx = tid; idx < 7 * SPAN; idx += 128) {
+    const int r = idx / SPAN, k = idx % SPAN;
+    const bool ok = it.n0 + k < tab.n_tab;
+    const double* src = table_row(tab, r);
+    cp_async8(&Tw[idx], ok ? src + it.n0 + k : src, ok);
+  }
+  cp_async_commit();
+  const TabWin win{Tw, SPAN};
+  const GenState* gbase = gen + (int64_t)it.t_begin * 128 + tid;
+
+  // generator of the tile being prepared: row grow, degrees n0 + 32 gq + [0, 32)
+  GenState cur = gbase[0];
+  auto generate = [&](const GenState& g, int buf, int k0, auto kn) {
+    const int64_t cut = g.cutreg >> 2;
+    const int reg = (int)(g.cutreg & 3) - 1;
+    const int nl0 = CK * gq;
+    const int64_t nstart = it.n0 + nl0;
     double* dst = &Ps[buf][grow][CK * gq + gq];
 #pragma unroll
     for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
       const int64_t n = nstart + k;
-      dst[k] = (n < g_cut) ? rec_value(g_reg, g_s0, g_s1) : 0.0;
-      if (n + 1 < g_cut) rec_step(g_reg, g_x, g_xm, tab, n, g_s0, g_s1);
+      dst[k] = (n < cut) ? rec_value(reg, cur.s0, cur.s1) : 0.0;
+      if (n + 1 < cut) rec_step_win(reg, g.xx, win, nl0 + k, cur.s0, cur.s1);
     }
   };
   auto stage_w = [&](int buf, int64_t r0) {
@@ -286,7 +367,7 @@ __global__ void __launch_bounds__(128)
       const int idx = tid + q * 128;
       const int v = idx / INV_RT, k = idx % INV_RT;
       const int64_t bb = b0 + v, i = r0 + k;
-      const bool ok = bb < batch && i < rows.nrows;
+      const bool ok = bb < batch && i < nrows;
       cp_async8(&Ws[buf][v][k], ok ? wv + bb * ldw + i : wv, ok);
     }
     cp_async_commit();
@@ -302,21 +383,26 @@ __global__ void __launch_bounds__(128)
   const int dbase = 32 * warp + warp;   // padded column of this warp's first degree
   using Four = std::integral_constant<int, 4>;
   stage_w(0, (int64_t)tile_ids[it.t_begin] * INV_RT);
-  gen_begin((int64_t)tile_ids[it.t_begin] * INV_RT);
-  for (int k0 = 0; k0 < CK; k0 += 4) generate(0, k0, Four{});
+  cp_async_wait_all();
+  __syncthreads();
+  {
+    const GenState g0 = cur;
+    for (int k0 = 0; k0 < CK; k0 += 4) generate(g0, 0, k0, Four{});
+  }
+  GenState nxt = cur;
+  if (it.t_count > 1) nxt = gbase[128];
   cp_async_wait_all();
   __syncthreads();
   for (int tt = 0; tt < it.t_count; ++tt) {
     const int buf = tt & 1;
     const bool more = tt + 1 < it.t_count;
-    if (more) {
-      const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt + 1] * INV_RT;
-      stage_w(buf ^ 1, r0);
-      gen_begin(r0);
-    }
+    cur = nxt;                                   // state of tile tt + 1 (loaded a stage ago)
+    const GenState g = cur;
+    if (tt + 2 < it.t_count) nxt = gbase[(int64_t)(tt + 2) * 128];
+    if (more) stage_w(buf ^ 1, (int64_t)tile_ids[it.t_begin + tt + 1] * INV_RT);
 #pragma unroll
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
-      if (more) generate(buf ^ 1, 4 * kk, Four{});
+      if (more) generate(g, buf ^ 1, 4 * kk, Four{});
       double a[4], bf[NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
@@ -421,7 +507,7 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
   switch (vt) {
 #define CJT_FWD(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * 2 * (FWD_KS * (FWD_ROWS + 4) + V * (FWD_KS + 4));                       \
+    const int smem = 8 * 2 * (FWD_KS * (FWD_ROWS + 4) + V * (FWD_KS + 4) + 7 * FWD_KS);          \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_mma<V>,                                    \
@@ -450,24 +536,35 @@ int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nsl
   return CJT_OK;
 }
 
-int launch_rec_inverse(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
-                       const double2* ck, const InvItem* items, int64_t n_items,
-                       const int32_t* tile_ids, const double* wv, int64_t ldw, int64_t batch, int vt,
-                       double* part, cudaStream_t st) {
+int launch_build_inv_gen(const RecRowsDev& rows, const int64_t* ck_off, const double2* ck,
+                         const int32_t* ids, const int32_t* gn0, int64_t total, void* out,
+                         cudaStream_t st) {
+  if (total <= 0) return CJT_OK;
+  const int T = 128;
+  k_build_inv_gen<<<(unsigned)((total * 128 + T - 1) / T), T, 0, st>>>(rows, ck_off, ck, ids, gn0, total,
+                                                                       (GenState*)out);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, const InvItem* items,
+                       int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
+                       int64_t batch, int vt, double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
   dim3 grid((unsigned)n_items, (unsigned)((batch + vt - 1) / vt));
+  const GenState* g = (const GenState*)gen;
   switch (vt) {
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * 2 * (INV_RT * (INV_DT + 4) + V * (INV_RT + 4));                         \
+    const int smem = 8 * (2 * INV_RT * (INV_DT + 4) + 2 * V * (INV_RT + 4) + 7 * INV_DT);         \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_mma<V>,                                    \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_inverse_mma<V><<<grid, 128, smem, st>>>(rows, tab, ck_off, ck, items, tile_ids, wv,    \
-                                                   ldw, batch, part);                            \
+    k_rec_inverse_mma<V><<<grid, 128, smem, st>>>(tab, g, nrows, items, tile_ids, wv, ldw,       \
+                                                   batch, part);                                 \
     break;                                                                                       \
   }
     CJT_INV(64) CJT_INV(32) CJT_INV(16)
