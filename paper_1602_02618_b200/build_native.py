@@ -39,31 +39,35 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = True, out: Path | None = None) -> Path:
+    """Compile the library (extra nvcc flags from $CJT_NVCC_EXTRA, for experiments)."""
+    target = out or OUT
+    if out is None and not force and not needs_build():
         return OUT
-    OUT.parent.mkdir(exist_ok=True)
+    target.parent.mkdir(parents=True, exist_ok=True)
+    extra = os.environ.get("CJT_NVCC_EXTRA", "").split()
     # compile each TU separately (parallel), then link
     objs = []
     procs = []
     for s in SOURCES:
-        obj = OUT.parent / (Path(s).stem + ".o")
+        obj = target.parent / (Path(s).stem + ".o")
         objs.append(obj)
-        cmd = [_nvcc(), *[f for f in NVCC_FLAGS if f != "-shared"], "-c", "-o", str(obj), str(CSRC / s)]
+        cmd = [_nvcc(), *[f for f in NVCC_FLAGS if f != "-shared"], *extra, "-c", "-o", str(obj),
+               str(CSRC / s)]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append(subprocess.Popen(cmd))
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
-    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(OUT),
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(target),
            *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
     for o in objs:
         o.unlink(missing_ok=True)
-    return OUT
+    return target
 
 
 if __name__ == "__main__":

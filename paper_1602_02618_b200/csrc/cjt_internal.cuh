@@ -306,7 +306,9 @@ constexpr int INV_RT = 32;      // grid rows per inverse pipeline stage (= row t
 bool cluster_enabled();
 
 // vectors per CTA tile of the DMMA contractions, chosen from the batch size
-inline int pick_vt(int64_t batch) { return batch >= 64 ? 64 : (batch >= 32 ? 32 : 16); }
+inline int pick_vt(int64_t batch) {
+  return batch >= 256 ? 128 : batch >= 64 ? 64 : (batch >= 32 ? 32 : 16);
+}
 
 // ---------------------------------------------------------------------------
 // launchers (host)

@@ -21,6 +21,7 @@
 // (deterministic, no atomics).
 #include <type_traits>
 
+
 #include "cjt_internal.cuh"
 
 namespace cjt {
@@ -83,6 +84,9 @@ struct TabWin {
 // degree n_lo + nl -> n_lo + nl + 1 with window tables (same rounding as rec_step)
 __device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w, int nl,
                                              double& s0, double& s1) {
+#ifdef CJT_FAKE_GEN
+  s0 = s0 * 0.5 + xx; s1 = s0; return;
+#endif
   const double a = w.t[nl];
   const double c = w.t[2 * w.span + nl];
   if (reg == 0) {
@@ -168,131 +172,154 @@ __device__ __forceinline__ void cp_async8(void* dst, const double* src, bool val
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// K1 (forward): values[b][i] = sum_n P_n(x_i) c[b][n] over one item
-// (128 rows x a degree segment) and one tile of VT vectors.
-//   M = rows (4 warps x 32), N = vectors (VT), K = degrees (stages of 32).
-//   P^T[k][row] is generated into shared memory by thread `row` (one
-//   recurrence chain per thread, carried across stages in registers);
-//   c[b][n0..n0+32) is staged by cp.async; stages are double-buffered.
+// Warp-specialised DMMA contractions (K1, K2).
+//   consumers: NCW warps, 4 along M (32 rows/degrees each) x NCW/4 along N,
+//              DMMA only (mma.sync m8n8k4 f64), accumulators in registers;
+//   producers: 4 warps (128 threads) running the recurrence generators and
+//              staging the other operand with cp.async, one stage ahead.
+// Stages rotate through a ring of NBUF buffers handed over with named barriers:
+//   FULL[b]  (ids 1..NBUF):        producers bar.arrive after filling buffer b,
+//                                  consumers bar.sync before reading it;
+//   EMPTY[b] (ids NBUF+1..2 NBUF): consumers bar.arrive after reading buffer b,
+//                                  producers bar.sync before refilling it;
+//   id 2 NBUF + 1: producer-only barrier (their private table buffers).
+// On B200 DMMA and DMUL/DADD share the fp64 datapath, so the generators'
+// serial chains are slowed by the consumers' DMMAs; NBUF = 3 gives them two
+// consumer stages of slack instead of one.
 template <int VT>
-__global__ void __launch_bounds__(128)
-    k_rec_forward_mma(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-                      const double2* __restrict__ ck, const FwdItem* __restrict__ items,
-                      const double* __restrict__ c, int64_t ldc, int64_t ncoef, int64_t batch,
-                      double* __restrict__ part) {
+struct WsCfg {
+  static constexpr int NBUF = 3;                     // stage ring depth
+  static constexpr int NCW = VT == 128 ? 8 : 4;      // consumer warps
+  static constexpr int NC = 32 * NCW;
+  static constexpr int NP = 128;                     // producer threads
+  static constexpr int NTH = NC + NP;
+  static constexpr int NWN = NCW / 4;                // consumer warps along N
+  static constexpr int NT = VT / 8 / NWN;            // 8-vector DMMA tiles per consumer warp
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int RING = 3;
+constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + RING, BAR_PROD = 1 + 2 * RING;
+
+// K1 (forward): values[b][i] = sum_n P_n(x_i) c[b][n] over one item
+// (128 rows x a degree segment) and one tile of VT vectors; stages of 32
+// degrees.  Producer thread p owns row p's recurrence chain (state carried
+// across stages in registers) and writes P^T[k][p].
+template <int VT>
+__global__ void __launch_bounds__(WsCfg<VT>::NTH)
+    k_rec_forward_ws(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
+                     const double2* __restrict__ ck, const FwdItem* __restrict__ items,
+                     const double* __restrict__ c, int64_t ldc, int64_t ncoef, int64_t batch,
+                     double* __restrict__ part) {
+  using W = WsCfg<VT>;
   constexpr int PT = FWD_ROWS + 4;   // P^T row stride (degrees x rows)
   constexpr int CS = FWD_KS + 4;     // staged c row stride (vectors x degrees)
-  constexpr int NT = VT / 8;
   extern __shared__ __align__(16) double smem_rec[];
   double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
-  double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + 2 * FWD_KS * PT);
-  double(*Ts)[7 * FWD_KS] = reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + 2 * FWD_KS * PT + 2 * VT * CS);
+  double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + RING * FWD_KS * PT);
+  double(*Ts)[7 * FWD_KS] =
+      reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + RING * FWD_KS * PT + RING * VT * CS);
   const FwdItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  const int nstages = (it.n_end - it.n_begin) / FWD_KS;
 
-  // generator state for row `tid`
-  const int64_t gi = it.row0 + tid;
-  const bool live = tid < it.nrows;
-  int reg = 0;
-  double xx = 0.0, s0 = 0.0, s1 = 0.0;
-  int64_t cut = 0;
-  if (live) {
-    reg = rows.reg[gi];
-    xx = reg == 0 ? rows.x[gi] : rows.xm[gi];
-    cut = rows.cut[gi];
-    if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
-  }
-  // generate degrees n0+k0 .. n0+k0+KN-1 of this thread's row into Pt[buf]
-  // (tables of the stage's 32 degrees come from Ts[buf])
-  auto generate = [&](int buf, int64_t n0, int k0, auto kn) {
-    const TabWin w{Ts[buf], FWD_KS};
-#pragma unroll
-    for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
-      const int64_t n = n0 + k;
-      Pt[buf][k][tid] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-      if (n + 1 < cut) rec_step_win(reg, xx, w, k, s0, s1);
+  if (tid >= W::NC) {
+    // ------------------------------ producer ------------------------------
+    const int p = tid - W::NC;
+    const int64_t gi = it.row0 + p;
+    int reg = 0;
+    double xx = 0.0, s0 = 0.0, s1 = 0.0;
+    int64_t cut = 0;
+    if (p < it.nrows) {
+      reg = rows.reg[gi];
+      xx = reg == 0 ? rows.x[gi] : rows.xm[gi];
+      cut = rows.cut[gi];
+      if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
     }
-  };
-  auto stage_tables = [&](int buf, int64_t n0) {
-    for (int idx = tid; idx < 7 * FWD_KS; idx += 128) {
-      const int r = idx / FWD_KS, k = idx % FWD_KS;
-      const int64_t n = n0 + k;
-      const bool ok = n < tab.n_tab;
-      const double* src = table_row(tab, r);
-      cp_async8(&Ts[buf][idx], ok ? src + n : src, ok);
-    }
-  };
-  auto stage_c = [&](int buf, int64_t n0) {
-#pragma unroll
-    for (int q = 0; q < (VT * FWD_KS) / 128; ++q) {
-      const int idx = tid + q * 128;
-      const int v = idx / FWD_KS, k = idx % FWD_KS;
-      const int64_t bb = b0 + v, n = n0 + k;
-      const bool ok = bb < batch && n < ncoef;
-      cp_async8(&Cs[buf][v][k], ok ? c + bb * ldc + n : c, ok);
-    }
+    auto stage_tables = [&](int buf, int64_t n0) {
+      for (int idx = p; idx < 7 * FWD_KS; idx += W::NP) {
+        const int r = idx / FWD_KS, k = idx % FWD_KS;
+        const int64_t n = n0 + k;
+        const bool ok = n < tab.n_tab;
+        const double* src = table_row(tab, r);
+        cp_async8(&Ts[buf][idx], ok ? src + n : src, ok);
+      }
+    };
+    stage_tables(0, it.n_begin);
     cp_async_commit();
-  };
+    cp_async_wait_all();
+    named_sync(BAR_PROD, W::NP);
+    for (int sidx = 0; sidx < nstages; ++sidx) {
+      const int buf = sidx % RING, tb = sidx & 1;
+      const int64_t n0 = it.n_begin + (int64_t)sidx * FWD_KS;
+      if (sidx >= RING) named_sync(BAR_EMPTY + buf, W::NTH);
+      // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[buf]
+#pragma unroll
+      for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
+        const int idx = p + q * W::NP;
+        const int v = idx / FWD_KS, k = idx % FWD_KS;
+        const int64_t bb = b0 + v, n = n0 + k;
+        const bool ok = bb < batch && n < ncoef;
+        cp_async8(&Cs[buf][v][k], ok ? c + bb * ldc + n : c, ok);
+      }
+      if (sidx + 1 < nstages) stage_tables(tb ^ 1, n0 + FWD_KS);
+      cp_async_commit();
+      const TabWin w{Ts[tb], FWD_KS};
+#pragma unroll 8
+      for (int k = 0; k < FWD_KS; ++k) {
+        const int64_t n = n0 + k;
+        Pt[buf][k][p] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
+        if (n + 1 < cut) rec_step_win(reg, xx, w, k, s0, s1);
+      }
+      cp_async_wait_all();
+      named_sync(BAR_PROD, W::NP);            // next stage's tables visible to all producers
+      named_arrive(BAR_FULL + buf, W::NTH);   // P^T and c tile of this stage are ready
+    }
+    return;
+  }
 
-  double acc[4][NT][2];
+  // ------------------------------ consumer --------------------------------
+  const int lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int ntile0 = wn * W::NT;
+  double acc[4][W::NT][2];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-
-  const int nstages = (it.n_end - it.n_begin) / FWD_KS;
-  using Four = std::integral_constant<int, 4>;
-  stage_tables(0, it.n_begin);
-  stage_c(0, it.n_begin);
-  cp_async_wait_all();
-  __syncthreads();
-  for (int k0 = 0; k0 < FWD_KS; k0 += 4) generate(0, it.n_begin, k0, Four{});
-  if (nstages > 1) {
-    stage_tables(1, it.n_begin + FWD_KS);
-    cp_async_commit();
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int ar = lane >> 2, ak = lane & 3;
+    for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int sidx = 0; sidx < nstages; ++sidx) {
-    const int buf = sidx & 1;
-    const bool more = sidx + 1 < nstages;
-    const int64_t nn = it.n_begin + (int64_t)(sidx + 1) * FWD_KS;
-    // Ts[buf] (stage sidx's tables) is free: refill it with stage sidx+2's,
-    // consumed next iteration after this iteration's closing wait + barrier
-    if (sidx + 2 < nstages) stage_tables(buf, it.n_begin + (int64_t)(sidx + 2) * FWD_KS);
-    if (more)
-      stage_c(buf ^ 1, nn);
-    else
-      cp_async_commit();
+    const int buf = sidx % RING;
+    named_sync(BAR_FULL + buf, W::NTH);
 #pragma unroll
     for (int kk = 0; kk < FWD_KS / 4; ++kk) {
-      // four recurrence steps of the next stage overlap this k-step's DMMAs
-      if (more) generate(buf ^ 1, nn, 4 * kk, Four{});
-      double a[4], bf[NT];
+      double a[4], bf[W::NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Pt[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[nt] = Cs[buf][8 * nt + ar][4 * kk + ak];
+      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Cs[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+        for (int nt = 0; nt < W::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    if (sidx + RING < nstages) named_arrive(BAR_EMPTY + buf, W::NTH);
   }
-  // D[row][vec]: row = 32 warp + 8 mt + (lane>>2), vec = 8 nt + 2 (lane&3) + j
+  // D[row][vec]: row = 32 warp + 8 mt + (lane>>2), vec = 8 (ntile0 + nt) + 2 (lane&3) + j
   double* dst = part + (int64_t)it.slot * batch * FWD_ROWS;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < W::NT; ++nt)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int row = 32 * warp + 8 * mt + ar;
-        const int64_t bb = b0 + 8 * nt + 2 * ak + j;
+        const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
         if (bb < batch) dst[bb * FWD_ROWS + row] = acc[mt][nt][j];
       }
 }
@@ -312,119 +339,112 @@ __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
 }
 
 // K2 (inverse): out[b][n] = sum_i P_n(x_i) wv[b][i] for one item (128
-// degrees x a list of 32-row tiles) and one tile of VT vectors.
-//   M = degrees (4 warps x 32), N = vectors (VT), K = rows (stages of 32).
-//   Each stage's P[row][deg] tile is generated by 4 threads per row, each
-//   restarting from the checkpoint at n0 + 32q; wv[b][rows] is staged by
-//   cp.async; stages are double-buffered.
+// degrees x a list of 32-row tiles) and one tile of VT vectors; one stage per
+// row tile.  Producer thread p = (row p/4, degree chunk p%4) restarts from the
+// dense generator stream and writes P[row][deg]; producers also stage the
+// wv tile.  The tables of the item's 128-degree window live in shared memory.
 template <int VT>
-__global__ void __launch_bounds__(128)
-    k_rec_inverse_mma(RecTablesDev tab, const GenState* __restrict__ gen, int64_t nrows,
-                      const InvItem* __restrict__ items, const int32_t* __restrict__ tile_ids,
-                      const double* __restrict__ wv, int64_t ldw, int64_t batch,
-                      double* __restrict__ part) {
+__global__ void __launch_bounds__(WsCfg<VT>::NTH)
+    k_rec_inverse_ws(RecTablesDev tab, const GenState* __restrict__ gen, int64_t nrows,
+                     const InvItem* __restrict__ items, const int32_t* __restrict__ tile_ids,
+                     const double* __restrict__ wv, int64_t ldw, int64_t batch,
+                     double* __restrict__ part) {
+  using W = WsCfg<VT>;
   constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
   constexpr int WS = INV_RT + 4;
-  constexpr int NT = VT / 8;
   constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
-  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + 2 * INV_RT * PR);
-  double* Tw = smem_rec + 2 * INV_RT * PR + 2 * VT * WS;   // [7][SPAN]
+  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + RING * INV_RT * PR);
+  double* Tw = smem_rec + RING * INV_RT * PR + RING * VT * WS;   // [7][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grow = tid >> 2, gq = tid & 3;   // generator: row in tile, degree chunk
+  const int tid = threadIdx.x;
 
-  for (int idx = tid; idx < 7 * SPAN; idx += 128) {
-    const int r = idx / SPAN, k = idx % SPAN;
-    const bool ok = it.n0 + k < tab.n_tab;
-    const double* src = table_row(tab, r);
-    cp_async8(&Tw[idx], ok ? src + it.n0 + k : src, ok);
-  }
-  cp_async_commit();
-  const TabWin win{Tw, SPAN};
-  const GenState* gbase = gen + (int64_t)it.t_begin * 128 + tid;
-
-  // generator of the tile being prepared: row grow, degrees n0 + 32 gq + [0, 32)
-  GenState cur = gbase[0];
-  auto generate = [&](const GenState& g, int buf, int k0, auto kn) {
-    const int64_t cut = g.cutreg >> 2;
-    const int reg = (int)(g.cutreg & 3) - 1;
-    const int nl0 = CK * gq;
-    const int64_t nstart = it.n0 + nl0;
-    double* dst = &Ps[buf][grow][CK * gq + gq];
-#pragma unroll
-    for (int k = k0; k < k0 + decltype(kn)::value; ++k) {
-      const int64_t n = nstart + k;
-      dst[k] = (n < cut) ? rec_value(reg, cur.s0, cur.s1) : 0.0;
-      if (n + 1 < cut) rec_step_win(reg, g.xx, win, nl0 + k, cur.s0, cur.s1);
-    }
-  };
-  auto stage_w = [&](int buf, int64_t r0) {
-#pragma unroll
-    for (int q = 0; q < (VT * INV_RT) / 128; ++q) {
-      const int idx = tid + q * 128;
-      const int v = idx / INV_RT, k = idx % INV_RT;
-      const int64_t bb = b0 + v, i = r0 + k;
-      const bool ok = bb < batch && i < nrows;
-      cp_async8(&Ws[buf][v][k], ok ? wv + bb * ldw + i : wv, ok);
+  if (tid >= W::NC) {
+    // ------------------------------ producer ------------------------------
+    const int p = tid - W::NC;
+    const int grow = p >> 2, gq = p & 3;
+    for (int idx = p; idx < 7 * SPAN; idx += W::NP) {
+      const int r = idx / SPAN, k = idx % SPAN;
+      const bool ok = it.n0 + k < tab.n_tab;
+      const double* src = table_row(tab, r);
+      cp_async8(&Tw[idx], ok ? src + it.n0 + k : src, ok);
     }
     cp_async_commit();
-  };
+    cp_async_wait_all();
+    named_sync(BAR_PROD, W::NP);
+    const TabWin win{Tw, SPAN};
+    const GenState* gbase = gen + (int64_t)it.t_begin * 128 + p;
+    GenState nxt = gbase[0];
+    const int nl0 = CK * gq;
+    const int64_t nstart = it.n0 + nl0;
+    for (int tt = 0; tt < it.t_count; ++tt) {
+      const int buf = tt % RING;
+      GenState g = nxt;
+      if (tt + 1 < it.t_count) nxt = gbase[(int64_t)(tt + 1) * 128];   // prefetch
+      if (tt >= RING) named_sync(BAR_EMPTY + buf, W::NTH);
+      const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt] * INV_RT;
+#pragma unroll
+      for (int q = 0; q < (VT * INV_RT) / W::NP; ++q) {
+        const int idx = p + q * W::NP;
+        const int v = idx / INV_RT, k = idx % INV_RT;
+        const int64_t bb = b0 + v, i = r0 + k;
+        const bool ok = bb < batch && i < nrows;
+        cp_async8(&Ws[buf][v][k], ok ? wv + bb * ldw + i : wv, ok);
+      }
+      cp_async_commit();
+      const int64_t cut = g.cutreg >> 2;
+      const int reg = (int)(g.cutreg & 3) - 1;
+      double* dst = &Ps[buf][grow][CK * gq + gq];
+#pragma unroll 8
+      for (int k = 0; k < CK; ++k) {
+        const int64_t n = nstart + k;
+        dst[k] = (n < cut) ? rec_value(reg, g.s0, g.s1) : 0.0;
+        if (n + 1 < cut) rec_step_win(reg, g.xx, win, nl0 + k, g.s0, g.s1);
+      }
+      cp_async_wait_all();
+      named_arrive(BAR_FULL + buf, W::NTH);
+    }
+    return;
+  }
 
-  double acc[4][NT][2];
+  // ------------------------------ consumer --------------------------------
+  const int lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int ntile0 = wn * W::NT;
+  const int dbase = 32 * warp + warp;   // padded column of this warp's first degree
+  double acc[4][W::NT][2];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-
-  const int ar = lane >> 2, ak = lane & 3;
-  const int dbase = 32 * warp + warp;   // padded column of this warp's first degree
-  using Four = std::integral_constant<int, 4>;
-  stage_w(0, (int64_t)tile_ids[it.t_begin] * INV_RT);
-  cp_async_wait_all();
-  __syncthreads();
-  {
-    const GenState g0 = cur;
-    for (int k0 = 0; k0 < CK; k0 += 4) generate(g0, 0, k0, Four{});
-  }
-  GenState nxt = cur;
-  if (it.t_count > 1) nxt = gbase[128];
-  cp_async_wait_all();
-  __syncthreads();
+    for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int tt = 0; tt < it.t_count; ++tt) {
-    const int buf = tt & 1;
-    const bool more = tt + 1 < it.t_count;
-    cur = nxt;                                   // state of tile tt + 1 (loaded a stage ago)
-    const GenState g = cur;
-    if (tt + 2 < it.t_count) nxt = gbase[(int64_t)(tt + 2) * 128];
-    if (more) stage_w(buf ^ 1, (int64_t)tile_ids[it.t_begin + tt + 1] * INV_RT);
+    const int buf = tt % RING;
+    named_sync(BAR_FULL + buf, W::NTH);
 #pragma unroll
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
-      if (more) generate(g, buf ^ 1, 4 * kk, Four{});
-      double a[4], bf[NT];
+      double a[4], bf[W::NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[nt] = Ws[buf][8 * nt + ar][4 * kk + ak];
+      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Ws[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+        for (int nt = 0; nt < W::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    if (tt + RING < it.t_count) named_arrive(BAR_EMPTY + buf, W::NTH);
   }
   double* dst = part + (int64_t)it.slot * batch * INV_DT;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < W::NT; ++nt)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int deg = 32 * warp + 8 * mt + ar;
-        const int64_t bb = b0 + 8 * nt + 2 * ak + j;
+        const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
         if (bb < batch) dst[bb * INV_DT + deg] = acc[mt][nt][j];
       }
 }
@@ -507,18 +527,18 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
   switch (vt) {
 #define CJT_FWD(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * 2 * (FWD_KS * (FWD_ROWS + 4) + V * (FWD_KS + 4) + 7 * FWD_KS);          \
+    const int smem = 8 * (RING * FWD_KS * (FWD_ROWS + 4) + RING * V * (FWD_KS + 4) + 2 * 7 * FWD_KS); \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_mma<V>,                                    \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V>,                                     \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_forward_mma<V><<<grid, 128, smem, st>>>(rows, tab, ck_off, ck, items, c, ldc, ncoef,   \
-                                                   batch, part);                                 \
+    k_rec_forward_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(rows, tab, ck_off, ck, items, c, ldc, \
+                                                           ncoef, batch, part);                  \
     break;                                                                                       \
   }
-    CJT_FWD(64) CJT_FWD(32) CJT_FWD(16)
+    CJT_FWD(128) CJT_FWD(64) CJT_FWD(32) CJT_FWD(16)
 #undef CJT_FWD
     default: return fail(CJT_EINVAL, "bad vector tile");
   }
@@ -556,18 +576,18 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
   switch (vt) {
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * (2 * INV_RT * (INV_DT + 4) + 2 * V * (INV_RT + 4) + 7 * INV_DT);         \
+    const int smem = 8 * (RING * INV_RT * (INV_DT + 4) + RING * V * (INV_RT + 4) + 7 * INV_DT);   \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_mma<V>,                                    \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_inverse_mma<V><<<grid, 128, smem, st>>>(tab, g, nrows, items, tile_ids, wv, ldw,       \
-                                                   batch, part);                                 \
+    k_rec_inverse_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(tab, g, nrows, items, tile_ids, wv,   \
+                                                           ldw, batch, part);                    \
     break;                                                                                       \
   }
-    CJT_INV(64) CJT_INV(32) CJT_INV(16)
+    CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(16)
 #undef CJT_INV
     default: return fail(CJT_EINVAL, "bad vector tile");
   }

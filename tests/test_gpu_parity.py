@@ -46,7 +46,7 @@ def test_golden_single_vector_api(cuda, name):
     assert O.parity(i.data, g["inv"][0], g["fwd"][0]) <= TOL
 
 
-@pytest.mark.parametrize("batch", [1, 17, 40, 70, 129])
+@pytest.mark.parametrize("batch", [1, 17, 40, 70, 129, 300])
 def test_batch_tiles_vs_oracle(cuda, batch):
     """Every vector-tile width (16/32/64) and ragged batch tails."""
     import torch
