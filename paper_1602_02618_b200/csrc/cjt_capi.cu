@@ -71,6 +71,14 @@ struct cjt_plan {
   int64_t n_iitems = 0;
   int32_t* tile_ids = nullptr;
   void* inv_gen = nullptr;      // K2 generator stream (GenState per row tile x thread)
+  int32_t* d_gn0 = nullptr;     // n0 of each work-list row tile (inverse)
+  // two-pass contraction (P workspace generated per execution)
+  bool two_pass = false;
+  GemmItem* gitems = nullptr;
+  int64_t n_gitems = 0;
+  int2* blk_tj = nullptr;       // forward P blocks (tile, stage)
+  int64_t n_pblk = 0;
+  double* pwork = nullptr;
   int32_t* dt_slot0 = nullptr;
   int32_t* dt_nslot = nullptr;
   int64_t n_islots = 0;
@@ -220,6 +228,18 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   return CJT_OK;
 }
 
+// Per-execution P workspace budget for the two-pass contraction: min(8 GiB,
+// a quarter of free device memory); $CJT_PGEN_BUDGET_MB overrides (0 = off).
+int64_t pgen_budget() {
+  if (const char* e = getenv("CJT_PGEN_BUDGET_MB")) return (int64_t)atoll(e) << 20;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min<int64_t>((int64_t)8 << 30, (int64_t)(fr / 4));
+}
+
 // Work lists depend on the batch size (split-K is sized to fill the GPU).
 std::vector<int64_t> tile_max_cut(const cjt_plan* P, int64_t rows_per_tile) {
   const int64_t ntiles = (P->nrows + rows_per_tile - 1) / rows_per_tile;
@@ -242,6 +262,7 @@ int upload_ws(cjt_plan* P, T** dst, const std::vector<T>& v) {
 
 int build_items(cjt_plan* P, int64_t batch) {
   const int64_t target = 8 * 148;  // CTAs worth of items to fill 148 SMs several times over
+  P->two_pass = false;
   P->vt = pick_vt(batch);
   const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {
@@ -274,6 +295,37 @@ int build_items(cjt_plan* P, int64_t batch) {
     std::stable_sort(items.begin(), items.end(), [](const FwdItem& a, const FwdItem& b) {
       return (a.n_end - a.n_begin) > (b.n_end - b.n_begin);
     });
+    // two-pass layout: P blocks (tile t, stage j) for j < ceil(maxcut_t / 32)
+    {
+      std::vector<int64_t> base((size_t)ntiles + 1, 0);
+      std::vector<int2> tj;
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t nst = (tmax[t] + FWD_KS - 1) / FWD_KS;
+        base[t + 1] = base[t] + nst;
+        for (int64_t j = 0; j < nst; ++j) tj.push_back(make_int2((int)t, (int)j));
+      }
+      const int64_t bytes = (int64_t)tj.size() * FWD_KS * FWD_ROWS * 8;
+      if (bytes <= pgen_budget()) {
+        std::vector<GemmItem> gi;
+        for (const FwdItem& it : items) {
+          GemmItem g{};
+          g.p_block0 = base[it.row0 / FWD_ROWS] + it.n_begin / FWD_KS;
+          g.x_off0 = it.n_begin;
+          g.ids_off = -1;
+          g.nstages = (it.n_end - it.n_begin) / FWD_KS;
+          g.slot = it.slot;
+          gi.push_back(g);
+        }
+        if (int rc = upload_ws(P, &P->gitems, gi)) return rc;
+        if (int rc = upload_ws(P, &P->blk_tj, tj)) return rc;
+        void* pw = nullptr;
+        if (int rc = dalloc(P->ws_allocs, &pw, (size_t)bytes)) return rc;
+        P->pwork = (double*)pw;
+        P->n_gitems = (int64_t)gi.size();
+        P->n_pblk = (int64_t)tj.size();
+        P->two_pass = true;
+      }
+    }
     if (int rc = upload_ws(P, &P->fitems, items)) return rc;
     if (int rc = upload_ws(P, &P->tile_slot0, s0)) return rc;
     if (int rc = upload_ws(P, &P->tile_nslot, ns)) return rc;
@@ -320,10 +372,33 @@ int build_items(cjt_plan* P, int64_t batch) {
     }
     std::stable_sort(items.begin(), items.end(),
                      [](const InvItem& a, const InvItem& b) { return a.t_count > b.t_count; });
+    {
+      const int64_t bytes = (int64_t)ids.size() * INV_RT * INV_DT * 8;
+      if (bytes <= pgen_budget()) {
+        std::vector<GemmItem> gi;
+        for (const InvItem& it : items) {
+          GemmItem g{};
+          g.p_block0 = it.t_begin;
+          g.x_off0 = 0;
+          g.ids_off = it.t_begin;
+          g.nstages = it.t_count;
+          g.slot = it.slot;
+          gi.push_back(g);
+        }
+        if (int rc = upload_ws(P, &P->gitems, gi)) return rc;
+        void* pw = nullptr;
+        if (int rc = dalloc(P->ws_allocs, &pw, (size_t)std::max<int64_t>(bytes, 8))) return rc;
+        P->pwork = (double*)pw;
+        P->n_gitems = (int64_t)gi.size();
+        P->n_pblk = (int64_t)ids.size();
+        P->two_pass = true;
+      }
+    }
     if (int rc = upload_ws(P, &P->iitems, items)) return rc;
     if (int rc = upload_ws(P, &P->tile_ids, ids)) return rc;
     int32_t* d_gn0 = nullptr;
     if (int rc = upload_ws(P, &d_gn0, gn0)) return rc;
+    P->d_gn0 = d_gn0;
     void* gp = nullptr;
     const int64_t total = (int64_t)ids.size();
     if (int rc = dalloc(P->ws_allocs, &gp, (size_t)std::max<int64_t>(total, 1) * 128 * GEN_STATE_BYTES)) return rc;
@@ -396,9 +471,17 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
   const int64_t N1 = P->n + 1, G1 = P->G + 1;
   const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
   if (P->direction == CJT_FORWARD) {
-    if (rec) {
+    if (rec && P->two_pass) {
+      if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj, P->n_pblk, P->pwork, st))
+        return rc;
+      if (int rc = launch_rec_gemm(P->gitems, P->n_gitems, P->pwork, nullptr, in, N1, N1, batch, P->vt,
+                                   P->part, st)) return rc;
+      launches += 1;
+    } else if (rec) {
       if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
                                       N1, batch, P->vt, P->part, st)) return rc;
+    }
+    if (rec) {
       if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, P->part, P->vals,
                                              G1, batch, st)) return rc;
       launches += 2;
@@ -420,9 +503,16 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
         if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, P->czpart, st, &launches))
           return rc;
     }
-    if (rec) {
+    if (rec && P->two_pass) {
+      if (int rc = launch_pgen_inv(P->tab, P->inv_gen, P->d_gn0, P->n_pblk, P->pwork, st)) return rc;
+      if (int rc = launch_rec_gemm(P->gitems, P->n_gitems, P->pwork, P->tile_ids, P->vals, G1, G1, batch,
+                                   P->vt, P->part, st)) return rc;
+      launches += 1;
+    } else if (rec) {
       if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
                                       P->vals, G1, batch, P->vt, P->part, st)) return rc;
+    }
+    if (rec) {
       if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
                                          batch, st)) return rc;
       launches += 2;

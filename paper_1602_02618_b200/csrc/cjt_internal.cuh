@@ -290,6 +290,13 @@ struct RecTablesDev {
 struct FwdItem {
   int32_t row0, nrows, n_begin, n_end, slot, pad;
 };
+// two-pass contraction item: stages s < nstages use P block p_block0 + s and
+// operand columns x_off0 + 32 s (ids_off < 0) or 32 * ids[ids_off + s]
+struct GemmItem {
+  int64_t p_block0;
+  int64_t x_off0;
+  int32_t ids_off, nstages, slot, pad;
+};
 // inverse work item: degrees [n0, n0+64) x row tiles tile_ids[t_begin .. t_begin+t_count)
 struct InvItem {
   int32_t n0, t_begin, t_count, slot;
@@ -335,6 +342,13 @@ int launch_build_inv_gen(const RecRowsDev& rows, const int64_t* ck_off, const do
 int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, const InvItem* items,
                        int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
                        int64_t batch, int vt, double* part, cudaStream_t st);
+int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
+                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st);
+int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t nblk,
+                    double* P, cudaStream_t st);
+int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, const int32_t* ids,
+                    const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, double* part,
+                    cudaStream_t st);
 int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,
                           const double* part, const double* blocks_acc, const double* scal,
                           double* out, int64_t ldo, int64_t batch, cudaStream_t st);

@@ -188,7 +188,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // consumer stages of slack instead of one.
 template <int VT>
 struct WsCfg {
-  static constexpr int NBUF = 3;                     // stage ring depth
+  static constexpr int NBUF = VT >= 64 ? 3 : 2;      // stage ring depth (small tiles: occupancy)
   static constexpr int NCW = VT == 128 ? 8 : 4;      // consumer warps
   static constexpr int NC = 32 * NCW;
   static constexpr int NP = 128;                     // producer threads
@@ -203,8 +203,8 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int RING = 3;
-constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + RING, BAR_PROD = 1 + 2 * RING;
+constexpr int RING_MAX = 3;
+constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + RING_MAX, BAR_PROD = 1 + 2 * RING_MAX;
 
 // K1 (forward): values[b][i] = sum_n P_n(x_i) c[b][n] over one item
 // (128 rows x a degree segment) and one tile of VT vectors; stages of 32
@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   constexpr int CS = FWD_KS + 4;     // staged c row stride (vectors x degrees)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
-  double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + RING * FWD_KS * PT);
+  double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + W::NBUF * FWD_KS * PT);
   double(*Ts)[7 * FWD_KS] =
-      reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + RING * FWD_KS * PT + RING * VT * CS);
+      reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + W::NBUF * FWD_KS * PT + W::NBUF * VT * CS);
   const FwdItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -256,9 +256,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     cp_async_wait_all();
     named_sync(BAR_PROD, W::NP);
     for (int sidx = 0; sidx < nstages; ++sidx) {
-      const int buf = sidx % RING, tb = sidx & 1;
+      const int buf = sidx % W::NBUF, tb = sidx & 1;
       const int64_t n0 = it.n_begin + (int64_t)sidx * FWD_KS;
-      if (sidx >= RING) named_sync(BAR_EMPTY + buf, W::NTH);
+      if (sidx >= W::NBUF) named_sync(BAR_EMPTY + buf, W::NTH);
       // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[buf]
 #pragma unroll
       for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
     for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int sidx = 0; sidx < nstages; ++sidx) {
-    const int buf = sidx % RING;
+    const int buf = sidx % W::NBUF;
     named_sync(BAR_FULL + buf, W::NTH);
 #pragma unroll
     for (int kk = 0; kk < FWD_KS / 4; ++kk) {
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
         for (int nt = 0; nt < W::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
     }
-    if (sidx + RING < nstages) named_arrive(BAR_EMPTY + buf, W::NTH);
+    if (sidx + W::NBUF < nstages) named_arrive(BAR_EMPTY + buf, W::NTH);
   }
   // D[row][vec]: row = 32 warp + 8 mt + (lane>>2), vec = 8 (ntile0 + nt) + 2 (lane&3) + j
   double* dst = part + (int64_t)it.slot * batch * FWD_ROWS;
@@ -355,8 +355,8 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
-  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + RING * INV_RT * PR);
-  double* Tw = smem_rec + RING * INV_RT * PR + RING * VT * WS;   // [7][SPAN]
+  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
+  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NBUF * VT * WS;   // [7][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -380,10 +380,10 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     const int nl0 = CK * gq;
     const int64_t nstart = it.n0 + nl0;
     for (int tt = 0; tt < it.t_count; ++tt) {
-      const int buf = tt % RING;
+      const int buf = tt % W::NBUF;
       GenState g = nxt;
       if (tt + 1 < it.t_count) nxt = gbase[(int64_t)(tt + 1) * 128];   // prefetch
-      if (tt >= RING) named_sync(BAR_EMPTY + buf, W::NTH);
+      if (tt >= W::NBUF) named_sync(BAR_EMPTY + buf, W::NTH);
       const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt] * INV_RT;
 #pragma unroll
       for (int q = 0; q < (VT * INV_RT) / W::NP; ++q) {
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
     for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int tt = 0; tt < it.t_count; ++tt) {
-    const int buf = tt % RING;
+    const int buf = tt % W::NBUF;
     named_sync(BAR_FULL + buf, W::NTH);
 #pragma unroll
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
         for (int nt = 0; nt < W::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
     }
-    if (tt + RING < it.t_count) named_arrive(BAR_EMPTY + buf, W::NTH);
+    if (tt + W::NBUF < it.t_count) named_arrive(BAR_EMPTY + buf, W::NTH);
   }
   double* dst = part + (int64_t)it.slot * batch * INV_DT;
 #pragma unroll
@@ -508,6 +508,176 @@ __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ r
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-pass recurrence contraction (default when the P workspace fits):
+//   pass 1  k_pgen_fwd / k_pgen_inv: generate every P_n(x_i) of the recurrence
+//           region once per execution, fully row- and segment-parallel from the
+//           per-plan checkpoints, into an HBM workspace laid out as the 32 x 128
+//           blocks the contraction streams;
+//   pass 2  k_rec_gemm: a cp.async-pipelined fp64 DMMA GEMM over those blocks.
+// Generating in its own pass keeps the generators' DMUL/DADD chains off the
+// fp64 datapath the DMMAs saturate (on B200 they share it).
+
+// forward blocks: block (t, j) = P^T[k][row] for rows 128 t.. and degrees 32 j..
+__global__ void __launch_bounds__(128)
+    k_pgen_fwd(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
+               const double2* __restrict__ ck, const int2* __restrict__ blk_tj,
+               double* __restrict__ P) {
+  const int2 tj = blk_tj[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int64_t i = (int64_t)tj.x * FWD_ROWS + tid;
+  const int64_t n0 = (int64_t)tj.y * FWD_KS;
+  double* out = P + (int64_t)blockIdx.x * (FWD_KS * FWD_ROWS) + tid;
+  int64_t cut = 0;
+  int reg = 0;
+  double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
+  if (i < rows.nrows) {
+    cut = rows.cut[i];
+    if (cut > n0) {
+      reg = rows.reg[i];
+      x = rows.x[i];
+      xm = rows.xm[i];
+      load_state(rows, ck_off, ck, i, n0, reg, s0, s1);
+    }
+  }
+#pragma unroll 4
+  for (int k = 0; k < FWD_KS; ++k) {
+    const int64_t n = n0 + k;
+    out[k * FWD_ROWS] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
+    if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
+  }
+}
+
+// inverse blocks: block g = P[row][deg] for work-list row tile g (32 rows) and
+// the item's 128 degrees; thread (row = tid/4, chunk = tid%4) runs 32 degrees
+// from the generator stream, staged through shared memory for coalesced writes
+__global__ void __launch_bounds__(128)
+    k_pgen_inv(RecTablesDev tab, const GenState* __restrict__ gen, const int32_t* __restrict__ gn0,
+               double* __restrict__ P) {
+  __shared__ double tile[INV_RT][INV_DT + 1];
+  const int64_t g = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int row = tid >> 2, q = tid & 3;
+  GenState st = gen[g * 128 + tid];
+  const int64_t cut = st.cutreg >> 2;
+  const int reg = (int)(st.cutreg & 3) - 1;
+  const int64_t nstart = (int64_t)gn0[g] + CK * q;
+  double x = reg == 0 ? st.xx : 0.0, xm = reg == 0 ? 0.0 : st.xx;
+#pragma unroll 4
+  for (int k = 0; k < CK; ++k) {
+    const int64_t n = nstart + k;
+    tile[row][CK * q + k] = (n < cut) ? rec_value(reg, st.s0, st.s1) : 0.0;
+    if (n + 1 < cut) rec_step(reg, x, xm, tab, n, st.s0, st.s1);
+  }
+  __syncthreads();
+  double* out = P + g * (INV_RT * INV_DT);
+  for (int idx = tid; idx < INV_RT * INV_DT; idx += 128) out[idx] = tile[idx / INV_DT][idx % INV_DT];
+}
+
+// 16-byte async copy (both addresses 16-byte aligned)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int VT>
+struct GemmCfg {
+  static constexpr int NCW = VT == 128 ? 8 : 4;   // warps: 4 along M x NCW/4 along N
+  static constexpr int NTH = 32 * NCW;
+  static constexpr int NWN = NCW / 4;
+  static constexpr int NT = VT / 8 / NWN;
+  static constexpr int STAGES = 3;
+  static constexpr int AS = 128 + 4;              // A row stride: conflict-free fragment loads
+  static constexpr int XS = 32 + 4;
+  static constexpr int SMEM = 8 * STAGES * (32 * AS + VT * XS);
+};
+
+// out[slot][b][m] = sum over the item's stages s, k < 32 of
+//   A_s[k][m] * x[b][xoff(s) + k],  A_s = P block (p_block0 + s) (32 x 128),
+// xoff(s) = x_off0 + 32 s (forward: contiguous degrees) or 32 * ids[ids_off + s]
+// (inverse: the item's row tiles).
+template <int VT>
+__global__ void __launch_bounds__(GemmCfg<VT>::NTH)
+    k_rec_gemm(const GemmItem* __restrict__ items, const double* __restrict__ P,
+               const int32_t* __restrict__ ids, const double* __restrict__ x, int64_t ldx,
+               int64_t xlen, int64_t batch, double* __restrict__ part) {
+  using C = GemmCfg<VT>;
+  extern __shared__ __align__(16) double smem_g[];
+  double(*As)[32][C::AS] = reinterpret_cast<double(*)[32][C::AS]>(smem_g);
+  double(*Xs)[VT][C::XS] = reinterpret_cast<double(*)[VT][C::XS]>(smem_g + C::STAGES * 32 * C::AS);
+  const GemmItem it = items[blockIdx.y];
+  const int64_t b0 = (int64_t)blockIdx.x * VT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int ntile0 = wn * C::NT;
+
+  auto load_stage = [&](int buf, int sidx) {
+    const double* a = P + (it.p_block0 + sidx) * (int64_t)(32 * 128);
+#pragma unroll
+    for (int q = 0; q < (32 * 64) / C::NTH; ++q) {   // 32 rows x 64 chunks of 16 bytes
+      const int idx = tid + q * C::NTH;
+      const int r = idx >> 6, ch = idx & 63;
+      cp_async16(&As[buf][r][2 * ch], a + r * 128 + 2 * ch);
+    }
+    const int64_t xoff = it.ids_off >= 0 ? (int64_t)ids[it.ids_off + sidx] * 32 : it.x_off0 + 32 * (int64_t)sidx;
+#pragma unroll
+    for (int q = 0; q < (VT * 32) / C::NTH; ++q) {
+      const int idx = tid + q * C::NTH;
+      const int v = idx >> 5, k = idx & 31;
+      const int64_t bb = b0 + v, kk = xoff + k;
+      const bool ok = bb < batch && kk < xlen;
+      cp_async8(&Xs[buf][v][k], ok ? x + bb * ldx + kk : x, ok);
+    }
+  };
+
+  double acc[4][C::NT][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  const int ns = it.nstages;
+#pragma unroll
+  for (int sidx = 0; sidx < C::STAGES - 1; ++sidx) {
+    if (sidx < ns) load_stage(sidx, sidx);
+    cp_async_commit();
+  }
+  for (int sidx = 0; sidx < ns; ++sidx) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    const int nxt = sidx + C::STAGES - 1;
+    if (nxt < ns) load_stage(nxt % C::STAGES, nxt);
+    cp_async_commit();
+    const int buf = sidx % C::STAGES;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double a[4], bf[C::NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = As[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) bf[nt] = Xs[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+    }
+  }
+  cp_async_wait<0>();
+  double* dst = part + (int64_t)it.slot * batch * 128;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m = 32 * warp + 8 * mt + ar;
+        const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
+        if (bb < batch) dst[bb * 128 + m] = acc[mt][nt][j];
+      }
+}
+
 }  // namespace
 
 int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
@@ -527,7 +697,8 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
   switch (vt) {
 #define CJT_FWD(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * (RING * FWD_KS * (FWD_ROWS + 4) + RING * V * (FWD_KS + 4) + 2 * 7 * FWD_KS); \
+    constexpr int R = WsCfg<V>::NBUF;                                                            \
+    const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + R * V * (FWD_KS + 4) + 2 * 7 * FWD_KS);  \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V>,                                     \
@@ -576,7 +747,8 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
   switch (vt) {
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
-    const int smem = 8 * (RING * INV_RT * (INV_DT + 4) + RING * V * (INV_RT + 4) + 7 * INV_DT);   \
+    constexpr int R = WsCfg<V>::NBUF;                                                            \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + 7 * INV_DT);         \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
@@ -589,6 +761,49 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
   }
     CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(16)
 #undef CJT_INV
+    default: return fail(CJT_EINVAL, "bad vector tile");
+  }
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+
+int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
+                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st) {
+  if (nblk <= 0) return CJT_OK;
+  k_pgen_fwd<<<(unsigned)nblk, 128, 0, st>>>(rows, tab, ck_off, ck, blk_tj, P);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t nblk,
+                    double* P, cudaStream_t st) {
+  if (nblk <= 0) return CJT_OK;
+  k_pgen_inv<<<(unsigned)nblk, 128, 0, st>>>(tab, (const GenState*)gen, gn0, P);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, const int32_t* ids,
+                    const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, double* part,
+                    cudaStream_t st) {
+  if (n_items <= 0 || batch <= 0) return CJT_OK;
+  dim3 grid((unsigned)((batch + vt - 1) / vt), (unsigned)n_items);
+  switch (vt) {
+#define CJT_GEMM(V)                                                                              \
+  case V: {                                                                                      \
+    static bool init = false;                                                                    \
+    if (!init) {                                                                                 \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        GemmCfg<V>::SMEM));                                      \
+      init = true;                                                                               \
+    }                                                                                            \
+    k_rec_gemm<V><<<grid, GemmCfg<V>::NTH, GemmCfg<V>::SMEM, st>>>(items, P, ids, x, ldx, xlen,  \
+                                                                   batch, part);                 \
+    break;                                                                                       \
+  }
+    CJT_GEMM(128) CJT_GEMM(64) CJT_GEMM(32) CJT_GEMM(16)
+#undef CJT_GEMM
     default: return fail(CJT_EINVAL, "bad vector tile");
   }
   CJT_CUDA_TRY(cudaGetLastError());
