@@ -16,7 +16,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 
 #include "cjt_internal.cuh"
 
@@ -72,13 +74,17 @@ struct cjt_plan {
   int32_t* tile_ids = nullptr;
   void* inv_gen = nullptr;      // K2 generator stream (GenState per row tile x thread)
   int32_t* d_gn0 = nullptr;     // n0 of each work-list row tile (inverse)
-  // two-pass contraction (P workspace generated per execution)
+  // two-pass contraction: P blocks generated per execution in chunks that fit
+  // the per-stream workspace arena, each chunk followed by its DMMA GEMM
+  struct Chunk {
+    int64_t b0, b1;             // forward: blk_tj range; inverse: work-list row tiles g
+    GemmItem* items;
+    int64_t n_items;
+  };
   bool two_pass = false;
-  GemmItem* gitems = nullptr;
-  int64_t n_gitems = 0;
+  std::vector<Chunk> chunks;
   int2* blk_tj = nullptr;       // forward P blocks (tile, stage)
-  int64_t n_pblk = 0;
-  double* pwork = nullptr;
+  int64_t chunk_bytes = 0;      // largest chunk's P bytes
   int32_t* dt_slot0 = nullptr;
   int32_t* dt_nslot = nullptr;
   int64_t n_islots = 0;
@@ -228,16 +234,49 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   return CJT_OK;
 }
 
-// Per-execution P workspace budget for the two-pass contraction: min(8 GiB,
-// a quarter of free device memory); $CJT_PGEN_BUDGET_MB overrides (0 = off).
-int64_t pgen_budget() {
-  if (const char* e = getenv("CJT_PGEN_BUDGET_MB")) return (int64_t)atoll(e) << 20;
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
+// P chunk size of the two-pass contraction (bytes of generated P per chunk):
+// $CJT_PGEN_CHUNK_MB, default 2 GiB; 0 disables the two-pass path.
+int64_t pgen_chunk_budget() {
+  if (const char* e = getenv("CJT_PGEN_CHUNK_MB")) return (int64_t)atoll(e) << 20;
+  return (int64_t)2 << 30;
+}
+
+// Per-(device, stream) workspace arena for the P chunks, shared by every plan
+// executing on that stream (stream order makes the reuse safe).  Grown outside
+// graph capture (first execution on a stream / reserve).
+struct Arena {
+  void* ptr = nullptr;
+  int64_t bytes = 0;
+};
+std::map<std::pair<int, cudaStream_t>, Arena>& arenas() {
+  static std::map<std::pair<int, cudaStream_t>, Arena> m;
+  return m;
+}
+std::mutex& arena_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+int arena_get(int device, cudaStream_t st, int64_t need, double** out) {
+  std::lock_guard<std::mutex> lk(arena_mutex());
+  Arena& a = arenas()[{device, st}];
+  if (a.bytes < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(CJT_EINVAL, "P workspace arena must be grown before graph capture (run once uncaptured)");
+    CJT_CUDA_TRY(cudaStreamSynchronize(st));
+    if (a.ptr) cudaFree(a.ptr);
+    a.ptr = nullptr;
+    a.bytes = 0;
+    cudaError_t e = cudaMalloc(&a.ptr, (size_t)need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CJT_ENOMEM, std::string("arena cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    a.bytes = need;
   }
-  return std::min<int64_t>((int64_t)8 << 30, (int64_t)(fr / 4));
+  *out = (double*)a.ptr;
+  return CJT_OK;
 }
 
 // Work lists depend on the batch size (split-K is sized to fill the GPU).
@@ -263,6 +302,12 @@ int upload_ws(cjt_plan* P, T** dst, const std::vector<T>& v) {
 int build_items(cjt_plan* P, int64_t batch) {
   const int64_t target = 8 * 148;  // CTAs worth of items to fill 148 SMs several times over
   P->two_pass = false;
+  P->vt = pick_vt(batch);
+  P->chunks.clear();
+  P->chunk_bytes = 0;
+  // two-pass only pays when each generated P value feeds >= 32 vectors; at
+  // VT = 16 the streamed P makes the GEMM memory-bound (fused kernels win)
+  const int64_t budget_blocks = P->vt >= 32 ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
   P->vt = pick_vt(batch);
   const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {
@@ -295,8 +340,9 @@ int build_items(cjt_plan* P, int64_t batch) {
     std::stable_sort(items.begin(), items.end(), [](const FwdItem& a, const FwdItem& b) {
       return (a.n_end - a.n_begin) > (b.n_end - b.n_begin);
     });
-    // two-pass layout: P blocks (tile t, stage j) for j < ceil(maxcut_t / 32)
-    {
+    // two-pass layout: P blocks (tile t, stage j) for j < ceil(maxcut_t / 32),
+    // cut into chunks of whole tiles of at most budget_blocks blocks
+    if (budget_blocks > 0) {
       std::vector<int64_t> base((size_t)ntiles + 1, 0);
       std::vector<int2> tj;
       for (int64_t t = 0; t < ntiles; ++t) {
@@ -304,25 +350,35 @@ int build_items(cjt_plan* P, int64_t batch) {
         base[t + 1] = base[t] + nst;
         for (int64_t j = 0; j < nst; ++j) tj.push_back(make_int2((int)t, (int)j));
       }
-      const int64_t bytes = (int64_t)tj.size() * FWD_KS * FWD_ROWS * 8;
-      if (bytes <= pgen_budget()) {
-        std::vector<GemmItem> gi;
-        for (const FwdItem& it : items) {
-          GemmItem g{};
-          g.p_block0 = base[it.row0 / FWD_ROWS] + it.n_begin / FWD_KS;
-          g.x_off0 = it.n_begin;
-          g.ids_off = -1;
-          g.nstages = (it.n_end - it.n_begin) / FWD_KS;
-          g.slot = it.slot;
-          gi.push_back(g);
-        }
-        if (int rc = upload_ws(P, &P->gitems, gi)) return rc;
+      bool ok = true;
+      std::vector<std::pair<int64_t, int64_t>> tranges;   // [t0, t1) per chunk
+      for (int64_t t0 = 0; t0 < ntiles && ok;) {
+        int64_t t1 = t0;
+        while (t1 < ntiles && (base[t1 + 1] - base[t0]) <= budget_blocks) ++t1;
+        if (t1 == t0) ok = false;   // a single tile exceeds the budget
+        tranges.push_back({t0, t1});
+        t0 = t1;
+      }
+      if (ok && !tj.empty()) {
         if (int rc = upload_ws(P, &P->blk_tj, tj)) return rc;
-        void* pw = nullptr;
-        if (int rc = dalloc(P->ws_allocs, &pw, (size_t)bytes)) return rc;
-        P->pwork = (double*)pw;
-        P->n_gitems = (int64_t)gi.size();
-        P->n_pblk = (int64_t)tj.size();
+        for (auto [t0, t1] : tranges) {
+          std::vector<GemmItem> gi;
+          for (const FwdItem& it : items) {
+            const int64_t t = it.row0 / FWD_ROWS;
+            if (t < t0 || t >= t1) continue;
+            GemmItem g{};
+            g.p_block0 = base[t] - base[t0] + it.n_begin / FWD_KS;
+            g.x_off0 = it.n_begin;
+            g.ids_off = -1;
+            g.nstages = (it.n_end - it.n_begin) / FWD_KS;
+            g.slot = it.slot;
+            gi.push_back(g);
+          }
+          cjt_plan::Chunk ch{base[t0], base[t1], nullptr, (int64_t)gi.size()};
+          if (int rc = upload_ws(P, &ch.items, gi)) return rc;
+          P->chunks.push_back(ch);
+          P->chunk_bytes = std::max<int64_t>(P->chunk_bytes, (base[t1] - base[t0]) * 32 * 128 * 8);
+        }
         P->two_pass = true;
       }
     }
@@ -372,25 +428,47 @@ int build_items(cjt_plan* P, int64_t batch) {
     }
     std::stable_sort(items.begin(), items.end(),
                      [](const InvItem& a, const InvItem& b) { return a.t_count > b.t_count; });
-    {
-      const int64_t bytes = (int64_t)ids.size() * INV_RT * INV_DT * 8;
-      if (bytes <= pgen_budget()) {
+    if (budget_blocks > 0 && !items.empty()) {
+      // chunks of whole items over the work-list row tiles g (items own
+      // disjoint contiguous g ranges), each at most budget_blocks tiles
+      std::vector<InvItem> by_g = items;
+      std::stable_sort(by_g.begin(), by_g.end(),
+                       [](const InvItem& a, const InvItem& b) { return a.t_begin < b.t_begin; });
+      bool ok = true;
+      size_t i0 = 0;
+      std::vector<cjt_plan::Chunk> chs;
+      std::vector<std::vector<GemmItem>> chitems;
+      while (i0 < by_g.size() && ok) {
+        const int64_t g0 = by_g[i0].t_begin;
+        size_t i1 = i0;
+        while (i1 < by_g.size() && (by_g[i1].t_begin + by_g[i1].t_count - g0) <= budget_blocks) ++i1;
+        if (i1 == i0) {
+          ok = false;
+          break;
+        }
+        const int64_t g1 = by_g[i1 - 1].t_begin + by_g[i1 - 1].t_count;
         std::vector<GemmItem> gi;
-        for (const InvItem& it : items) {
+        for (size_t q = i0; q < i1; ++q) {
           GemmItem g{};
-          g.p_block0 = it.t_begin;
+          g.p_block0 = by_g[q].t_begin - g0;
           g.x_off0 = 0;
-          g.ids_off = it.t_begin;
-          g.nstages = it.t_count;
-          g.slot = it.slot;
+          g.ids_off = by_g[q].t_begin;
+          g.nstages = by_g[q].t_count;
+          g.slot = by_g[q].slot;
           gi.push_back(g);
         }
-        if (int rc = upload_ws(P, &P->gitems, gi)) return rc;
-        void* pw = nullptr;
-        if (int rc = dalloc(P->ws_allocs, &pw, (size_t)std::max<int64_t>(bytes, 8))) return rc;
-        P->pwork = (double*)pw;
-        P->n_gitems = (int64_t)gi.size();
-        P->n_pblk = (int64_t)ids.size();
+        std::stable_sort(gi.begin(), gi.end(),
+                         [](const GemmItem& a, const GemmItem& b) { return a.nstages > b.nstages; });
+        chs.push_back(cjt_plan::Chunk{g0, g1, nullptr, (int64_t)gi.size()});
+        chitems.push_back(std::move(gi));
+        i0 = i1;
+      }
+      if (ok) {
+        for (size_t c = 0; c < chs.size(); ++c) {
+          if (int rc = upload_ws(P, &chs[c].items, chitems[c])) return rc;
+          P->chunk_bytes = std::max<int64_t>(P->chunk_bytes, (chs[c].b1 - chs[c].b0) * INV_RT * INV_DT * 8);
+        }
+        P->chunks = chs;
         P->two_pass = true;
       }
     }
@@ -472,11 +550,16 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
   const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
   if (P->direction == CJT_FORWARD) {
     if (rec && P->two_pass) {
-      if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj, P->n_pblk, P->pwork, st))
-        return rc;
-      if (int rc = launch_rec_gemm(P->gitems, P->n_gitems, P->pwork, nullptr, in, N1, N1, batch, P->vt,
-                                   P->part, st)) return rc;
-      launches += 1;
+      double* pw = nullptr;
+      if (int rc = arena_get(P->device, st, P->chunk_bytes, &pw)) return rc;
+      for (const auto& ch : P->chunks) {
+        if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj + ch.b0, ch.b1 - ch.b0, pw, st))
+          return rc;
+        if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, nullptr, in, N1, N1, batch, P->vt, false,
+                                     P->part, st)) return rc;
+        launches += 2;
+      }
+      launches -= 1;
     } else if (rec) {
       if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
                                       N1, batch, P->vt, P->part, st)) return rc;
@@ -504,10 +587,15 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
           return rc;
     }
     if (rec && P->two_pass) {
-      if (int rc = launch_pgen_inv(P->tab, P->inv_gen, P->d_gn0, P->n_pblk, P->pwork, st)) return rc;
-      if (int rc = launch_rec_gemm(P->gitems, P->n_gitems, P->pwork, P->tile_ids, P->vals, G1, G1, batch,
-                                   P->vt, P->part, st)) return rc;
-      launches += 1;
+      double* pw = nullptr;
+      if (int rc = arena_get(P->device, st, P->chunk_bytes, &pw)) return rc;
+      for (const auto& ch : P->chunks) {
+        if (int rc = launch_pgen_inv(P->tab, P->inv_gen, P->d_gn0, ch.b0, ch.b1, pw, st)) return rc;
+        if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, P->tile_ids, P->vals, G1, G1, batch, P->vt, true,
+                                     P->part, st)) return rc;
+        launches += 2;
+      }
+      launches -= 1;
     } else if (rec) {
       if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
                                       P->vals, G1, batch, P->vt, P->part, st)) return rc;

@@ -19,6 +19,7 @@
 // recurrence state (every CK degrees), which keeps the values bit-identical
 // while exposing parallelism; partial sums are reduced in a fixed order
 // (deterministic, no atomics).
+#include <algorithm>
 #include <type_traits>
 
 
@@ -520,59 +521,60 @@ __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ r
 // fp64 datapath the DMMAs saturate (on B200 they share it).
 
 // forward blocks: block (t, j) = P^T[k][row] for rows 128 t.. and degrees 32 j..
+// (grid-stride over blocks: many resident warps hide the chains' latency)
 __global__ void __launch_bounds__(128)
     k_pgen_fwd(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-               const double2* __restrict__ ck, const int2* __restrict__ blk_tj,
+               const double2* __restrict__ ck, const int2* __restrict__ blk_tj, int64_t nblk,
                double* __restrict__ P) {
-  const int2 tj = blk_tj[blockIdx.x];
   const int tid = threadIdx.x;
-  const int64_t i = (int64_t)tj.x * FWD_ROWS + tid;
-  const int64_t n0 = (int64_t)tj.y * FWD_KS;
-  double* out = P + (int64_t)blockIdx.x * (FWD_KS * FWD_ROWS) + tid;
-  int64_t cut = 0;
-  int reg = 0;
-  double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
-  if (i < rows.nrows) {
-    cut = rows.cut[i];
-    if (cut > n0) {
-      reg = rows.reg[i];
-      x = rows.x[i];
-      xm = rows.xm[i];
-      load_state(rows, ck_off, ck, i, n0, reg, s0, s1);
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int2 tj = blk_tj[blk];
+    const int64_t i = (int64_t)tj.x * FWD_ROWS + tid;
+    const int64_t n0 = (int64_t)tj.y * FWD_KS;
+    double* out = P + blk * (FWD_KS * FWD_ROWS) + tid;
+    int64_t cut = 0;
+    int reg = 0;
+    double x = 0.0, xm = 0.0, s0 = 0.0, s1 = 0.0;
+    if (i < rows.nrows) {
+      cut = rows.cut[i];
+      if (cut > n0) {
+        reg = rows.reg[i];
+        x = rows.x[i];
+        xm = rows.xm[i];
+        load_state(rows, ck_off, ck, i, n0, reg, s0, s1);
+      }
     }
-  }
 #pragma unroll 4
-  for (int k = 0; k < FWD_KS; ++k) {
-    const int64_t n = n0 + k;
-    out[k * FWD_ROWS] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-    if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
+    for (int k = 0; k < FWD_KS; ++k) {
+      const int64_t n = n0 + k;
+      out[k * FWD_ROWS] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
+      if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
+    }
   }
 }
 
-// inverse blocks: block g = P[row][deg] for work-list row tile g (32 rows) and
-// the item's 128 degrees; thread (row = tid/4, chunk = tid%4) runs 32 degrees
-// from the generator stream, staged through shared memory for coalesced writes
+// inverse blocks: block g = P[deg][row] (128 degrees x 32 rows) for work-list
+// row tile g; thread (chunk q = tid/32, row = tid%32) runs degrees 32 q..32 q+31
+// from the generator stream; each warp store is 32 consecutive doubles
 __global__ void __launch_bounds__(128)
     k_pgen_inv(RecTablesDev tab, const GenState* __restrict__ gen, const int32_t* __restrict__ gn0,
-               double* __restrict__ P) {
-  __shared__ double tile[INV_RT][INV_DT + 1];
-  const int64_t g = blockIdx.x;
+               int64_t gbeg, int64_t gend, double* __restrict__ P) {
   const int tid = threadIdx.x;
-  const int row = tid >> 2, q = tid & 3;
-  GenState st = gen[g * 128 + tid];
-  const int64_t cut = st.cutreg >> 2;
-  const int reg = (int)(st.cutreg & 3) - 1;
-  const int64_t nstart = (int64_t)gn0[g] + CK * q;
-  double x = reg == 0 ? st.xx : 0.0, xm = reg == 0 ? 0.0 : st.xx;
+  const int q = tid >> 5, row = tid & 31;
+  for (int64_t g = gbeg + blockIdx.x; g < gend; g += gridDim.x) {
+    GenState st = gen[g * 128 + row * 4 + q];
+    const int64_t cut = st.cutreg >> 2;
+    const int reg = (int)(st.cutreg & 3) - 1;
+    const int64_t nstart = (int64_t)gn0[g] + CK * q;
+    const double x = reg == 0 ? st.xx : 0.0, xm = reg == 0 ? 0.0 : st.xx;
+    double* out = P + (g - gbeg) * (INV_RT * INV_DT) + (CK * q) * INV_RT + row;
 #pragma unroll 4
-  for (int k = 0; k < CK; ++k) {
-    const int64_t n = nstart + k;
-    tile[row][CK * q + k] = (n < cut) ? rec_value(reg, st.s0, st.s1) : 0.0;
-    if (n + 1 < cut) rec_step(reg, x, xm, tab, n, st.s0, st.s1);
+    for (int k = 0; k < CK; ++k) {
+      const int64_t n = nstart + k;
+      out[k * INV_RT] = (n < cut) ? rec_value(reg, st.s0, st.s1) : 0.0;
+      if (n + 1 < cut) rec_step(reg, x, xm, tab, n, st.s0, st.s1);
+    }
   }
-  __syncthreads();
-  double* out = P + g * (INV_RT * INV_DT);
-  for (int idx = tid; idx < INV_RT * INV_DT; idx += 128) out[idx] = tile[idx / INV_DT][idx % INV_DT];
 }
 
 // 16-byte async copy (both addresses 16-byte aligned)
@@ -582,31 +584,36 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int VT>
+// A block in global memory: AMK = false -> [k 32][m 128] (forward P^T),
+// AMK = true -> [m 128][k 32] (inverse P transposed for coalesced generation);
+// the shared-memory copy keeps the same orientation with padded rows so the
+// DMMA A-fragment loads are conflict-free either way.
+template <int VT, bool AMK>
 struct GemmCfg {
   static constexpr int NCW = VT == 128 ? 8 : 4;   // warps: 4 along M x NCW/4 along N
   static constexpr int NTH = 32 * NCW;
   static constexpr int NWN = NCW / 4;
   static constexpr int NT = VT / 8 / NWN;
   static constexpr int STAGES = 3;
-  static constexpr int AS = 128 + 4;              // A row stride: conflict-free fragment loads
+  static constexpr int AROWS = AMK ? 128 : 32;
+  static constexpr int AS = AMK ? 32 + 4 : 128 + 4;   // A row stride
   static constexpr int XS = 32 + 4;
-  static constexpr int SMEM = 8 * STAGES * (32 * AS + VT * XS);
+  static constexpr int SMEM = 8 * STAGES * (AROWS * AS + VT * XS);
 };
 
 // out[slot][b][m] = sum over the item's stages s, k < 32 of
 //   A_s[k][m] * x[b][xoff(s) + k],  A_s = P block (p_block0 + s) (32 x 128),
 // xoff(s) = x_off0 + 32 s (forward: contiguous degrees) or 32 * ids[ids_off + s]
 // (inverse: the item's row tiles).
-template <int VT>
-__global__ void __launch_bounds__(GemmCfg<VT>::NTH)
+template <int VT, bool AMK>
+__global__ void __launch_bounds__(GemmCfg<VT, AMK>::NTH)
     k_rec_gemm(const GemmItem* __restrict__ items, const double* __restrict__ P,
                const int32_t* __restrict__ ids, const double* __restrict__ x, int64_t ldx,
                int64_t xlen, int64_t batch, double* __restrict__ part) {
-  using C = GemmCfg<VT>;
+  using C = GemmCfg<VT, AMK>;
   extern __shared__ __align__(16) double smem_g[];
-  double(*As)[32][C::AS] = reinterpret_cast<double(*)[32][C::AS]>(smem_g);
-  double(*Xs)[VT][C::XS] = reinterpret_cast<double(*)[VT][C::XS]>(smem_g + C::STAGES * 32 * C::AS);
+  double(*As)[C::AROWS][C::AS] = reinterpret_cast<double(*)[C::AROWS][C::AS]>(smem_g);
+  double(*Xs)[VT][C::XS] = reinterpret_cast<double(*)[VT][C::XS]>(smem_g + C::STAGES * C::AROWS * C::AS);
   const GemmItem it = items[blockIdx.y];
   const int64_t b0 = (int64_t)blockIdx.x * VT;
   const int tid = threadIdx.x, lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
@@ -615,11 +622,12 @@ __global__ void __launch_bounds__(GemmCfg<VT>::NTH)
 
   auto load_stage = [&](int buf, int sidx) {
     const double* a = P + (it.p_block0 + sidx) * (int64_t)(32 * 128);
+    constexpr int CPR = (AMK ? 32 : 128) / 2;        // 16-byte chunks per A row
 #pragma unroll
-    for (int q = 0; q < (32 * 64) / C::NTH; ++q) {   // 32 rows x 64 chunks of 16 bytes
+    for (int q = 0; q < (32 * 64) / C::NTH; ++q) {
       const int idx = tid + q * C::NTH;
-      const int r = idx >> 6, ch = idx & 63;
-      cp_async16(&As[buf][r][2 * ch], a + r * 128 + 2 * ch);
+      const int r = idx / CPR, ch = idx % CPR;
+      cp_async16(&As[buf][r][2 * ch], a + r * (2 * CPR) + 2 * ch);
     }
     const int64_t xoff = it.ids_off >= 0 ? (int64_t)ids[it.ids_off + sidx] * 32 : it.x_off0 + 32 * (int64_t)sidx;
 #pragma unroll
@@ -655,7 +663,8 @@ __global__ void __launch_bounds__(GemmCfg<VT>::NTH)
     for (int kk = 0; kk < 8; ++kk) {
       double a[4], bf[C::NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = As[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
+      for (int mt = 0; mt < 4; ++mt)
+        a[mt] = AMK ? As[buf][32 * warp + 8 * mt + ar][4 * kk + ak] : As[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt) bf[nt] = Xs[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
 #pragma unroll
@@ -771,43 +780,43 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                     const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st) {
   if (nblk <= 0) return CJT_OK;
-  k_pgen_fwd<<<(unsigned)nblk, 128, 0, st>>>(rows, tab, ck_off, ck, blk_tj, P);
+  const int64_t grid = std::min<int64_t>(nblk, 148 * 16);
+  k_pgen_fwd<<<(unsigned)grid, 128, 0, st>>>(rows, tab, ck_off, ck, blk_tj, nblk, P);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
 
-int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t nblk,
-                    double* P, cudaStream_t st) {
-  if (nblk <= 0) return CJT_OK;
-  k_pgen_inv<<<(unsigned)nblk, 128, 0, st>>>(tab, (const GenState*)gen, gn0, P);
+int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t gbeg,
+                    int64_t gend, double* P, cudaStream_t st) {
+  if (gend <= gbeg) return CJT_OK;
+  const int64_t grid = std::min<int64_t>(gend - gbeg, 148 * 16);
+  k_pgen_inv<<<(unsigned)grid, 128, 0, st>>>(tab, (const GenState*)gen, gn0, gbeg, gend, P);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
 
 int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, const int32_t* ids,
-                    const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, double* part,
-                    cudaStream_t st) {
+                    const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, bool amk,
+                    double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
   dim3 grid((unsigned)((batch + vt - 1) / vt), (unsigned)n_items);
-  switch (vt) {
-#define CJT_GEMM(V)                                                                              \
-  case V: {                                                                                      \
+#define CJT_GEMM(V, M)                                                                           \
+  if (vt == V && amk == M) {                                                                     \
+    using Cf = GemmCfg<V, M>;                                                                    \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        GemmCfg<V>::SMEM));                                      \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V, M>,                                        \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM)); \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_gemm<V><<<grid, GemmCfg<V>::NTH, GemmCfg<V>::SMEM, st>>>(items, P, ids, x, ldx, xlen,  \
-                                                                   batch, part);                 \
-    break;                                                                                       \
+    k_rec_gemm<V, M><<<grid, Cf::NTH, Cf::SMEM, st>>>(items, P, ids, x, ldx, xlen, batch, part); \
+    CJT_CUDA_TRY(cudaGetLastError());                                                            \
+    return CJT_OK;                                                                               \
   }
-    CJT_GEMM(128) CJT_GEMM(64) CJT_GEMM(32) CJT_GEMM(16)
+  CJT_GEMM(128, false) CJT_GEMM(64, false) CJT_GEMM(32, false) CJT_GEMM(16, false)
+  CJT_GEMM(128, true) CJT_GEMM(64, true) CJT_GEMM(32, true) CJT_GEMM(16, true)
 #undef CJT_GEMM
-    default: return fail(CJT_EINVAL, "bad vector tile");
-  }
-  CJT_CUDA_TRY(cudaGetLastError());
-  return CJT_OK;
+  return fail(CJT_EINVAL, "bad vector tile");
 }
 
 int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,

@@ -124,3 +124,22 @@ def test_full_size_linearity_and_roundtrip(cuda, config):
     assert np.max(np.abs(f[2] - (0.75 * f[0] - 1.25 * f[1]))) <= 1e-13 * l1
     for v in range(3):
         assert O.parity(i[v], [c[0], c[1], mix][v], [c[0], c[1], mix][v]) <= 1e-11
+
+
+@pytest.mark.parametrize("chunk_mb", ["1", "0"])
+def test_two_pass_chunking_and_fused_fallback(cuda, chunk_mb, monkeypatch):
+    """Small P chunks (many generate/contract rounds) and the fused single-pass
+    kernels (chunking disabled) give the same results as the oracle."""
+    import torch
+    monkeypatch.setenv("CJT_PGEN_CHUNK_MB", chunk_mb)
+    a, b, n = -0.25, 0.4, 2047
+    p = cj.JacobiParameters(a, b)
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = np.stack([O.seeded_vector(2, v, n) for v in range(70)])
+    f = cj.forward_batched(fp, torch.from_numpy(c).to(cuda))
+    i = cj.inverse_batched(ip, f).cpu().numpy()
+    f = f.cpu().numpy()
+    for v in (0, 33, 69):
+        rf = O.oracle_forward(a, b, c[v])
+        assert O.parity(f[v], rf, c[v]) <= 1e-12
+        assert O.parity(i[v], O.oracle_inverse(a, b, f[v]), f[v]) <= 1e-12
