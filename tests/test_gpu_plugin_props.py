@@ -143,3 +143,44 @@ def test_two_pass_chunking_and_fused_fallback(cuda, chunk_mb, monkeypatch):
         rf = O.oracle_forward(a, b, c[v])
         assert O.parity(f[v], rf, c[v]) <= 1e-12
         assert O.parity(i[v], O.oracle_inverse(a, b, f[v]), f[v]) <= 1e-12
+
+
+def test_ragged_groups_graph_and_streams(cuda):
+    """RaggedPlan: mixed (alpha, beta, N) groups on several streams, captured in a
+    CUDA graph, match the oracle per vector (configuration 5 path)."""
+    import torch
+    from paper_1602_02618_b200.ragged import RaggedPlan
+    params = [(-0.45, 0.25, 255), (0.5, 0.5, 511), (-0.45, 0.25, 255), (0.0, -0.2, 1023),
+              (0.5, 0.5, 511), (0.25, 0.5, 2047), (0.0, -0.2, 1023), (-0.2, -0.45, 255)]
+    rp = RaggedPlan(params, threads=2)
+    vecs = {i: O.seeded_vector(5, i, n) for i, (_, _, n) in enumerate(params)}
+    x = torch.from_numpy(rp.pack(vecs)).to(cuda)
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    rp.reserve()
+    streams = [torch.cuda.Stream(cuda) for _ in range(3)]
+    asg = rp.assign(3)
+
+    def step():
+        rp.execute("forward", x, y, streams, asg)
+        rp.execute("inverse", y, z, streams, asg)
+
+    step()
+    torch.cuda.synchronize()
+    y_eager, z_eager = y.clone(), z.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    y.zero_()
+    z.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_eager) and torch.equal(z, z_eager)
+    yh, zh = y.cpu().numpy(), z.cpu().numpy()
+    for gi, mem in enumerate(rp.members):
+        a, b, n = rp.keys[gi]
+        blk_y = yh[rp.offsets[gi]:rp.offsets[gi + 1]].reshape(len(mem), n + 1)
+        blk_z = zh[rp.offsets[gi]:rp.offsets[gi + 1]].reshape(len(mem), n + 1)
+        for r, i in enumerate(mem):
+            rf = O.oracle_forward(a, b, vecs[i])
+            assert O.parity(blk_y[r], rf, vecs[i]) <= 1e-12
+            assert O.parity(blk_z[r], O.oracle_inverse(a, b, blk_y[r]), blk_y[r]) <= 1e-12
