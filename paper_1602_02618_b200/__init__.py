@@ -20,6 +20,7 @@ from .engine import (
     inverse,
     inverse_batched,
     jacobi,
+    pipeline,
     plan,
 )
 from .planner import DEFAULT_EPS, DEFAULT_M, JacobiParameters, ParameterRangeError
@@ -30,5 +31,5 @@ __all__ = [
     "AngleGrid", "CHEBYSHEV", "CoefficientVector", "DEFAULT_EPS", "DEFAULT_M", "JACOBI",
     "JacobiParameters", "ParameterRangeError", "TransformPlan", "available_backends",
     "chebyshev", "forward", "forward_batched", "inverse", "inverse_batched", "jacobi",
-    "kernel_backend", "plan", "register_with", "set_kernel_backend",
+    "kernel_backend", "pipeline", "plan", "register_with", "set_kernel_backend",
 ]

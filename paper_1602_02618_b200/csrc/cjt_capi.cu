@@ -58,7 +58,6 @@ struct cjt_plan {
   double* scal = nullptr;
   int64_t scratch_elems_per_vec = 0;  // complex elements of multipass scratch per vector
   int64_t part_elems_per_vec = 0;     // doubles of m-split chirp-z partials per vector
-  double* czpart = nullptr;
   double fft_points = 0.0;
 
   // batch-dependent state (cjt_plan_reserve)
@@ -88,12 +87,21 @@ struct cjt_plan {
   int32_t* dt_slot0 = nullptr;
   int32_t* dt_nslot = nullptr;
   int64_t n_islots = 0;
-  double* part = nullptr;
-  double* vals = nullptr;    // forward values / inverse wv, [B][G+1]
-  double* yacc = nullptr;    // inverse block accumulator [B][N+1]
-  double2* scratch = nullptr;
-  double* io_in = nullptr;
-  double* io_out = nullptr;
+  // per-stream mutable workspaces, so concurrent executions of one plan on
+  // different streams never share buffers
+  struct Workspace {
+    std::vector<void*> allocs;
+    int64_t batch = 0;
+    double* part = nullptr;
+    double* vals = nullptr;    // forward values / inverse wv, [B][G+1]
+    double* yacc = nullptr;    // inverse block accumulator [B][N+1]
+    double* czpart = nullptr;  // chirp-z m-split partials
+    double2* scratch = nullptr;
+    double* io_in = nullptr;
+    double* io_out = nullptr;
+  };
+  std::map<cudaStream_t, Workspace> ws;
+  std::mutex ws_mu;
   int64_t workspace_bytes = 0;
   int64_t last_launches = 0;
   int vt = 64;
@@ -102,6 +110,8 @@ struct cjt_plan {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
+    for (auto& kv : ws)
+      for (void* p : kv.second.allocs) cudaFree(p);
     for (void* p : ws_allocs) cudaFree(p);
     for (void* p : allocs) cudaFree(p);
     cudaSetDevice(cur);
@@ -502,41 +512,62 @@ int reserve(cjt_plan* P, int64_t batch) {
   if (batch <= P->reserved) return CJT_OK;
   CJT_CUDA_TRY(cudaDeviceSynchronize());
   free_workspace(P);
+  {
+    std::lock_guard<std::mutex> lk(P->ws_mu);
+    for (auto& kv : P->ws)
+      for (void* q : kv.second.allocs) cudaFree(q);
+    P->ws.clear();
+  }
   if (int rc = build_items(P, batch)) return rc;
-  void* p;
+  P->reserved = batch;
+  return CJT_OK;
+}
+
+// workspace of `st`, allocated on first use (outside graph capture)
+int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
+  std::lock_guard<std::mutex> lk(P->ws_mu);
+  cjt_plan::Workspace& W = P->ws[st];
+  *out = &W;
+  if (W.batch >= P->reserved) return CJT_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(CJT_EINVAL, "plan workspace for this stream must exist before graph capture (run once uncaptured)");
+  for (void* q : W.allocs) cudaFree(q);
+  W = cjt_plan::Workspace{};
+  const int64_t batch = P->reserved;
   const int64_t G1 = P->G + 1, N1 = P->n + 1;
+  void* p;
   int64_t bytes = 0;
   const int64_t part_elems = (P->direction == CJT_FORWARD) ? P->n_fslots * FWD_ROWS : P->n_islots * INV_DT;
-  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
-  P->part = (double*)p;
+  if (int rc = dalloc(W.allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
+  W.part = (double*)p;
   bytes += part_elems * batch * 8;
-  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
-  P->vals = (double*)p;
+  if (int rc = dalloc(W.allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
+  W.vals = (double*)p;
   bytes += G1 * batch * 8;
   if (P->direction == CJT_INVERSE && !P->blocks.empty()) {
-    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
-    P->yacc = (double*)p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+    W.yacc = (double*)p;
     bytes += N1 * batch * 8;
-  } else {
-    P->yacc = nullptr;
   }
   if (P->part_elems_per_vec > 0) {
-    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(P->part_elems_per_vec * batch) * 8)) return rc;
-    P->czpart = (double*)p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(P->part_elems_per_vec * batch) * 8)) return rc;
+    W.czpart = (double*)p;
     bytes += P->part_elems_per_vec * batch * 8;
   }
   if (P->scratch_elems_per_vec > 0) {
-    if (int rc = dalloc(P->ws_allocs, &p, (size_t)(P->scratch_elems_per_vec * batch) * 16)) return rc;
-    P->scratch = (double2*)p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(P->scratch_elems_per_vec * batch) * 16)) return rc;
+    W.scratch = (double2*)p;
     bytes += P->scratch_elems_per_vec * batch * 16;
   }
-  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
-  P->io_in = (double*)p;
-  if (int rc = dalloc(P->ws_allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
-  P->io_out = (double*)p;
+  if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+  W.io_in = (double*)p;
+  if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+  W.io_out = (double*)p;
   bytes += 2 * N1 * batch * 8;
-  P->workspace_bytes = bytes;
-  P->reserved = batch;
+  W.batch = batch;
+  P->workspace_bytes = std::max<int64_t>(P->workspace_bytes, bytes);
   return CJT_OK;
 }
 
@@ -545,6 +576,9 @@ int reserve(cjt_plan* P, int64_t batch) {
 // synthesis chirp-z).  Partial masks are for timing individual kernels only.
 int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStream_t st,
             int stages = CJT_STAGE_ALL) {
+  cjt_plan::Workspace* Wp = nullptr;
+  if (int rc = get_workspace(P, st, &Wp)) return rc;
+  cjt_plan::Workspace& W = *Wp;
   int launches = 0;
   const int64_t N1 = P->n + 1, G1 = P->G + 1;
   const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
@@ -556,34 +590,34 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
         if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj + ch.b0, ch.b1 - ch.b0, pw, st))
           return rc;
         if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, nullptr, in, N1, N1, batch, P->vt, false,
-                                     P->part, st)) return rc;
+                                     W.part, st)) return rc;
         launches += 2;
       }
       launches -= 1;
     } else if (rec) {
       if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
-                                      N1, batch, P->vt, P->part, st)) return rc;
+                                      N1, batch, P->vt, W.part, st)) return rc;
     }
     if (rec) {
-      if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, P->part, P->vals,
+      if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, W.part, W.vals,
                                              G1, batch, st)) return rc;
       launches += 2;
     }
     if (blk)
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, P->czpart, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, st, &launches))
           return rc;
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, P->vals, G1, out, N1, batch, P->scratch, P->czpart, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, W.vals, G1, out, N1, batch, W.scratch, W.czpart, st, &launches))
         return rc;
   } else {
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, P->vals, G1, batch, P->scratch, P->czpart, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, st, &launches))
         return rc;
     if (blk && !P->blocks.empty()) {
-      CJT_CUDA_TRY(cudaMemsetAsync(P->yacc, 0, (size_t)(N1 * batch) * 8, st));
+      CJT_CUDA_TRY(cudaMemsetAsync(W.yacc, 0, (size_t)(N1 * batch) * 8, st));
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, P->vals, G1, P->yacc, N1, batch, P->scratch, P->czpart, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, W.vals, G1, W.yacc, N1, batch, W.scratch, W.czpart, st, &launches))
           return rc;
     }
     if (rec && P->two_pass) {
@@ -591,17 +625,17 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       if (int rc = arena_get(P->device, st, P->chunk_bytes, &pw)) return rc;
       for (const auto& ch : P->chunks) {
         if (int rc = launch_pgen_inv(P->tab, P->inv_gen, P->d_gn0, ch.b0, ch.b1, pw, st)) return rc;
-        if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, P->tile_ids, P->vals, G1, G1, batch, P->vt, true,
-                                     P->part, st)) return rc;
+        if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, P->tile_ids, W.vals, G1, G1, batch, P->vt, true,
+                                     W.part, st)) return rc;
         launches += 2;
       }
       launches -= 1;
     } else if (rec) {
       if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
-                                      P->vals, G1, batch, P->vt, P->part, st)) return rc;
+                                      W.vals, G1, batch, P->vt, W.part, st)) return rc;
     }
     if (rec) {
-      if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, P->part, P->yacc, P->scal, out, N1,
+      if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, W.part, W.yacc, P->scal, out, N1,
                                          batch, st)) return rc;
       launches += 2;
     }
@@ -808,10 +842,12 @@ int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, in
   DeviceGuard g(plan->device);
   if (int rc = reserve(plan, batch)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  cjt_plan::Workspace* W = nullptr;
+  if (int rc = get_workspace(plan, st, &W)) return rc;
   const size_t bytes = (size_t)(batch * (plan->n + 1)) * 8;
-  CJT_CUDA_TRY(cudaMemcpyAsync(plan->io_in, in_host, bytes, cudaMemcpyHostToDevice, st));
-  if (int rc = execute(plan, plan->io_in, plan->io_out, batch, st)) return rc;
-  CJT_CUDA_TRY(cudaMemcpyAsync(out_host, plan->io_out, bytes, cudaMemcpyDeviceToHost, st));
+  CJT_CUDA_TRY(cudaMemcpyAsync(W->io_in, in_host, bytes, cudaMemcpyHostToDevice, st));
+  if (int rc = execute(plan, W->io_in, W->io_out, batch, st)) return rc;
+  CJT_CUDA_TRY(cudaMemcpyAsync(out_host, W->io_out, bytes, cudaMemcpyDeviceToHost, st));
   CJT_CUDA_TRY(cudaStreamSynchronize(st));
   return CJT_OK;
 }
@@ -928,9 +964,11 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   if (int rc = upload(Al, &dwv, wv, (size_t)n_points)) return rc;
   if (int rc = dalloc(Al, &p, ones.size() * 8)) return rc;
   dres = (double*)p;
+  cjt_plan::Workspace* W = nullptr;
+  if (int rc = get_workspace(P.get(), 0, &W)) return rc;
   if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
-                                  dwv, n_points, 1, P->vt, P->part, 0)) return rc;
-  if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, P->part, nullptr, dscal, dres,
+                                  dwv, n_points, 1, P->vt, W->part, 0)) return rc;
+  if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, W->part, nullptr, dscal, dres,
                                      P->n + 1, 1, 0)) return rc;
   std::vector<double> res(ones.size());
   CJT_CUDA_TRY(cudaMemcpy(res.data(), dres, res.size() * 8, cudaMemcpyDeviceToHost));

@@ -316,3 +316,53 @@ def inverse_batched(tp: TransformPlan, c, out=None, check_finite: bool = True, s
     if tp.direction != "inverse":
         raise ValueError("not an inverse plan")
     return _execute_batched(tp, c, out, check_finite, stream)
+
+
+def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: int = 2,
+             device: int | None = None):
+    """Apply `plans` in sequence (e.g. ``(forward_plan, inverse_plan)``) to a
+    (B, N+1) float64 host array, with host<->device copies overlapped with the
+    transforms: the batch is cut into chunks that alternate between `streams`
+    CUDA streams (H2D of chunk k+1 and D2H of chunk k-1 run under chunk k's
+    kernels).  Pinned host memory (e.g. ``torch.empty(..., pin_memory=True)``)
+    is required for the copies to be asynchronous.  Returns host_out."""
+    import torch
+    if not plans:
+        raise ValueError("no plans")
+    n1 = plans[0].n + 1
+    for i, tp in enumerate(plans):
+        if tp.n + 1 != n1:
+            raise ValueError("plans must share the degree N")
+        if i and plans[i - 1].direction == tp.direction:
+            raise ValueError("consecutive plans must alternate direction")
+    hin = host_in if hasattr(host_in, "data_ptr") else torch.from_numpy(np.ascontiguousarray(host_in))
+    if hin.dtype != torch.float64 or hin.dim() != 2 or hin.shape[1] != n1:
+        raise ValueError(f"host input must be float64 with shape (B, {n1})")
+    if host_out is None:
+        host_out = torch.empty_like(hin, pin_memory=True)
+    hout = host_out if hasattr(host_out, "data_ptr") else torch.from_numpy(host_out)
+    batch = hin.shape[0]
+    chunk = batch if chunk is None else max(1, min(int(chunk), batch))
+    dev = torch.device("cuda", _current_device() if device is None else device)
+    nstreams = max(1, min(streams, -(-batch // chunk)))
+    ss = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+    bufs = [(torch.empty((chunk, n1), dtype=torch.float64, device=dev),
+             torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nstreams)]
+    cur = torch.cuda.current_stream(dev)
+    for s in ss:
+        s.wait_stream(cur)
+    for k, r0 in enumerate(range(0, batch, chunk)):
+        r1 = min(batch, r0 + chunk)
+        s = ss[k % nstreams]
+        a, b = bufs[k % nstreams]
+        with torch.cuda.stream(s):
+            a[: r1 - r0].copy_(hin[r0:r1], non_blocking=True)
+            src, dst = a[: r1 - r0], b[: r1 - r0]
+            for tp in plans:
+                _execute_batched(tp, src, out=dst, check_finite=False)
+                src, dst = dst, src
+            hout[r0:r1].copy_(src, non_blocking=True)
+    for s in ss:
+        cur.wait_stream(s)
+    torch.cuda.synchronize(dev)
+    return host_out

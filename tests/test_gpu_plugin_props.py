@@ -184,3 +184,28 @@ def test_ragged_groups_graph_and_streams(cuda):
             rf = O.oracle_forward(a, b, vecs[i])
             assert O.parity(blk_y[r], rf, vecs[i]) <= 1e-12
             assert O.parity(blk_z[r], O.oracle_inverse(a, b, blk_y[r]), blk_y[r]) <= 1e-12
+
+
+def test_pipeline_and_concurrent_streams(cuda):
+    """pipeline(): chunked, overlapped host round trip equals the device path;
+    one plan executed concurrently on two streams (per-stream workspaces)."""
+    import torch
+    a, b, n = -0.25, 0.4, 1023
+    p = cj.JacobiParameters(a, b)
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = np.stack([O.seeded_vector(2, v, n) for v in range(96)])
+    pin = torch.from_numpy(c).pin_memory()
+    out = cj.pipeline((fp, ip), pin, chunk=32, streams=2)
+    ref = cj.inverse_batched(ip, cj.forward_batched(fp, torch.from_numpy(c).to(cuda)[:32]))
+    assert torch.equal(out[:32], ref.cpu())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    x = torch.from_numpy(c).to(cuda)
+    y1, y2 = torch.empty_like(x[:48]), torch.empty_like(x[48:])
+    fp.device_plan().reserve(48)
+    with torch.cuda.stream(s1):
+        cj.forward_batched(fp, x[:48].contiguous(), out=y1)
+    with torch.cuda.stream(s2):
+        cj.forward_batched(fp, x[48:].contiguous(), out=y2)
+    torch.cuda.synchronize()
+    whole = cj.forward_batched(fp, x)
+    assert torch.equal(torch.cat([y1, y2]), whole)
