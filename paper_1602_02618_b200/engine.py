@@ -318,6 +318,9 @@ def inverse_batched(tp: TransformPlan, c, out=None, check_finite: bool = True, s
     return _execute_batched(tp, c, out, check_finite, stream)
 
 
+_PIPE_CACHE: dict = {}
+
+
 def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: int = 2,
              device: int | None = None):
     """Apply `plans` in sequence (e.g. ``(forward_plan, inverse_plan)``) to a
@@ -345,9 +348,16 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
     chunk = batch if chunk is None else max(1, min(int(chunk), batch))
     dev = torch.device("cuda", _current_device() if device is None else device)
     nstreams = max(1, min(streams, -(-batch // chunk)))
-    ss = [torch.cuda.Stream(dev) for _ in range(nstreams)]
-    bufs = [(torch.empty((chunk, n1), dtype=torch.float64, device=dev),
-             torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nstreams)]
+    # streams and device buffers are cached: plan workspaces are per stream, so
+    # fresh streams would re-allocate them on every call
+    key = (dev.index, nstreams, chunk, n1)
+    cached = _PIPE_CACHE.get(key)
+    if cached is None:
+        ss = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+        bufs = [(torch.empty((chunk, n1), dtype=torch.float64, device=dev),
+                 torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nstreams)]
+        cached = _PIPE_CACHE[key] = (ss, bufs)
+    ss, bufs = cached
     cur = torch.cuda.current_stream(dev)
     for s in ss:
         s.wait_stream(cur)
