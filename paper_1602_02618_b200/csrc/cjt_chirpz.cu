@@ -34,9 +34,11 @@ namespace {
 template <int LOGL>
 struct FusedCfg {
   static constexpr int L = 1 << LOGL;
+  static constexpr int LEPT = LOGL == 13 ? 5 : 4;   // radix-32 passes for 8192: 3 passes, not 4
+  static constexpr int EPT = 1 << LEPT;             // elements per thread
   static constexpr int E = (L >= 4096) ? L : 4096;  // complex elements per CTA
   static constexpr int NG = E / L;                  // vectors per CTA
-  static constexpr int T = E / 16;                  // threads per CTA
+  static constexpr int T = E / EPT;                 // threads per CTA
   static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8;
 };
 
@@ -51,7 +53,8 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
                    double* __restrict__ part, int m_per_cta) {
   using Cfg = FusedCfg<LOGL>;
   constexpr int L = Cfg::L;
-  constexpr int TPG = L / 16;
+  constexpr int EPT = Cfg::EPT;
+  constexpr int TPG = L / EPT;
   extern __shared__ double2 smem[];
   const int grp = threadIdx.x / TPG;
   const int t = threadIdx.x % TPG;
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
   const int m0 = blockIdx.z * m_per_cta;
   const int m1 = min(m0 + m_per_cta, (int)cz.m_count);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[t + i * TPG] = 0.0;
+  for (int i = 0; i < EPT; ++i) acc[t + i * TPG] = 0.0;
 
   for (int m = m0; m < m1; ++m) {
     const double2* pre = cz.pre + (int64_t)m * cz.width;
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
         }
         return make_double2(0.0, 0.0);
       };
-      fft_smem_io<LOGL, -1>(s, t, tw, load_x, SmemStore{s});
+      fft_smem_io<LOGL, -1, decltype(load_x), SmemStore, Cfg::LEPT>(s, t, tw, load_x, SmemStore{s});
       // inverse FFT: spectrum product fused into the first pass, output
       // diagonal and the sum over (m, input tile) fused into the last pass
       const double2* kh = cz.khat + ((int64_t)j * cz.n_in + ti) * L;
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
           acc[e] += fma(q.x, y.x, -q.y * y.y);
         }
       };
-      fft_smem_io<LOGL, +1>(s, t, tw, load_spec, store_out);
+      fft_smem_io<LOGL, +1, decltype(load_spec), decltype(store_out), Cfg::LEPT>(s, t, tw, load_spec, store_out);
     }
   }
   __syncthreads();
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
   if (part) {
     double* pb = part + ((int64_t)blockIdx.z * batch + b) * cz.count + so;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < EPT; ++i) {
       const int e = t + i * TPG;
       if (e < sc) pb[e] = acc[e];
     }
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
   }
   double* ob = out + b * ldo + cz.q0 + so;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < EPT; ++i) {
     const int e = t + i * TPG;
     if (e < sc) ob[e] = cz.accumulate ? ob[e] + acc[e] : acc[e];
   }

@@ -73,7 +73,30 @@ __device__ __forceinline__ double cos16(int j) {
 }
 __device__ __forceinline__ double sin16(int j) { return cos16(j - 4); }
 
-// b * exp(DIR 2 pi i k / SZ), compile-time K and SZ after unrolling
+__device__ __forceinline__ double cos32(int j) {
+  switch (j & 31) {
+    case 1: return 0.98078528040323044913;
+    case 3: return 0.83146961230254523708;
+    case 5: return 0.55557023301960222474;
+    case 7: return 0.19509032201612826785;
+    case 9: return -0.19509032201612826785;
+    case 11: return -0.55557023301960222474;
+    case 13: return -0.83146961230254523708;
+    case 15: return -0.98078528040323044913;
+    case 17: return -0.98078528040323044913;
+    case 19: return -0.83146961230254523708;
+    case 21: return -0.55557023301960222474;
+    case 23: return -0.19509032201612826785;
+    case 25: return 0.19509032201612826785;
+    case 27: return 0.55557023301960222474;
+    case 29: return 0.83146961230254523708;
+    case 31: return 0.98078528040323044913;
+    default: return cos16((j & 31) >> 1);
+  }
+}
+__device__ __forceinline__ double sin32(int j) { return cos32(j - 8); }
+
+// b * exp(DIR 2 pi i k / SZ), compile-time K and SZ after unrolling (SZ <= 32)
 template <int DIR, int K, int SZ>
 __device__ __forceinline__ double2 twiddle_const(double2 b) {
   if constexpr (K == 0) {
@@ -81,9 +104,9 @@ __device__ __forceinline__ double2 twiddle_const(double2 b) {
   } else if constexpr (4 * K == SZ) {
     return cmul_i<DIR>(b);
   } else {
-    constexpr int J = K * (16 / SZ);
-    const double c = cos16(J);
-    const double s = DIR * sin16(J);
+    constexpr int J = K * (32 / SZ);
+    const double c = cos32(J);
+    const double s = DIR * sin32(J);
     return make_double2(fma(b.x, c, -b.y * s), fma(b.x, s, b.y * c));
   }
 }
@@ -120,7 +143,7 @@ __device__ __forceinline__ void dft_levels(double2* v) {
 }
 template <int R, int DIR>
 __device__ __forceinline__ void dft_reg(double2* v) {
-  constexpr int BITS = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : 4;
+  constexpr int BITS = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : (R == 16) ? 4 : 5;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int j = bitrev(i, BITS);
@@ -142,11 +165,12 @@ __device__ __forceinline__ void dft_reg(double2* v) {
 // w^(2^j) are read from the table (u 2^j < 8192 since r k < NS R <= 8192).
 template <int R, int DIR>
 __device__ __forceinline__ void twiddle_powers(double2* v, const double2* __restrict__ tw, int u) {
-  double2 p[16];
+  double2 p[32];
   p[1] = __ldg(&tw[u]);
   if constexpr (R > 2) p[2] = __ldg(&tw[2 * u]);
   if constexpr (R > 4) p[4] = __ldg(&tw[4 * u]);
   if constexpr (R > 8) p[8] = __ldg(&tw[8 * u]);
+  if constexpr (R > 16) p[16] = __ldg(&tw[16 * u]);
   if constexpr (DIR > 0) {
 #pragma unroll
     for (int j = 1; j < R; j <<= 1) p[j].y = -p[j].y;
@@ -249,11 +273,11 @@ __device__ __forceinline__ void fft_smem(double2* s, int t, const double2* __res
 }
 
 // FFT with a custom first-pass source and last-pass sink (see SmemLoad/SmemStore)
-template <int LOGL, int DIR, class LoadF, class StoreF>
+template <int LOGL, int DIR, class LoadF, class StoreF, int LEPT = 4>
 __device__ __forceinline__ void fft_smem_io(double2* s, int t, const double2* __restrict__ tw,
                                             const LoadF& ld, const StoreF& st) {
-  static_assert(LOGL >= 4 && LOGL <= 13, "smem FFT length out of range");
-  fft_pass<LOGL, DIR, 4, 0>(s, t, tw, ld, st);
+  static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
+  fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, ld, st);
 }
 
 // ---------------------------------------------------------------------------

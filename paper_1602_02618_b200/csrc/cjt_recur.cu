@@ -590,7 +590,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // DMMA A-fragment loads are conflict-free either way.
 template <int VT, bool AMK>
 struct GemmCfg {
-  static constexpr int NCW = VT == 128 ? 8 : 4;   // warps: 4 along M x NCW/4 along N
+  static constexpr int NCW = VT >= 64 ? 8 : 4;    // warps: 4 along M x NCW/4 along N
   static constexpr int NTH = 32 * NCW;
   static constexpr int NWN = NCW / 4;
   static constexpr int NT = VT / 8 / NWN;

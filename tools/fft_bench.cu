@@ -15,9 +15,12 @@ using namespace cjt;
 #define MINB 1
 #endif
 constexpr int EPTB = 1 << LEPT_B;
+#ifndef LOGL_B
+#define LOGL_B 12
+#endif
 template <int LOGL>
-__global__ void __launch_bounds__(4096 / EPTB, MINB) k_fft_rt(double2* data, const double2* tw, int reps) {
-  constexpr int L = 1 << LOGL, TPG = L / EPTB, NG = 4096 / L;
+__global__ void __launch_bounds__((1 << LOGL_B) / EPTB, MINB) k_fft_rt(double2* data, const double2* tw, int reps) {
+  constexpr int L = 1 << LOGL, TPG = L / EPTB, NG = 1;
   extern __shared__ double2 sm[];
   const int grp = threadIdx.x / TPG, t = threadIdx.x % TPG;
   double2* s = sm + grp * padded_len(L);
@@ -39,22 +42,22 @@ int main() {
   std::vector<double2> tw(8192);
   for (int u = 0; u < 8192; ++u) { long double a = -2.0L * 3.14159265358979323846264338327950288L * u / 8192; tw[u] = make_double2((double)cosl(a), (double)sinl(a)); }
   double2* dtw; cudaMalloc(&dtw, 8192 * 16); cudaMemcpy(dtw, tw.data(), 8192 * 16, cudaMemcpyHostToDevice);
-  const int LOGL = 12, L = 1 << LOGL;
-  const int blocks = sms * 8, n = blocks * 4096;
+  const int LOGL = LOGL_B, L = 1 << LOGL;
+  const int blocks = sms * 8, n = blocks * L;
   std::vector<double2> h(n);
   for (int i = 0; i < n; ++i) h[i] = make_double2(sin(0.37 * i) , cos(1.3 * i + 0.1));
   double2* d; cudaMalloc(&d, (size_t)n * 16);
   cudaMemcpy(d, h.data(), (size_t)n * 16, cudaMemcpyHostToDevice);
   const int smem = padded_len(L) * 16;
   cudaFuncSetAttribute(k_fft_rt<LOGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_fft_rt<LOGL><<<blocks, 4096 / EPTB, smem>>>(d, dtw, 1);
+  k_fft_rt<LOGL><<<blocks, L / EPTB, smem>>>(d, dtw, 1);
   cudaDeviceSynchronize();
   std::vector<double2> o(n); cudaMemcpy(o.data(), d, (size_t)n * 16, cudaMemcpyDeviceToHost);
   double err = 0; for (int i = 0; i < n; ++i) err = fmax(err, fmax(fabs(o[i].x - h[i].x), fabs(o[i].y - h[i].y)));
   cudaMemcpy(d, h.data(), (size_t)n * 16, cudaMemcpyHostToDevice);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int reps = 50;
-  cudaEventRecord(e0); k_fft_rt<LOGL><<<blocks, 4096 / EPTB, smem>>>(d, dtw, reps); cudaEventRecord(e1); cudaEventSynchronize(e1);
+  cudaEventRecord(e0); k_fft_rt<LOGL><<<blocks, L / EPTB, smem>>>(d, dtw, reps); cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   const double passes = 2.0 * reps * ((LOGL + LEPT_B - 1) / LEPT_B);
   const double ep = passes * (double)n;
