@@ -228,7 +228,9 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
   }
   if (lg >= 14 && !cluster) {
-    const int l2 = std::min(13, (lg + 1) / 2);
+    // longest on-chip rows (8192, radix-32 passes) and short columns: wide,
+    // coalesced column tiles (E / L1 columns) in passes 1 and 3
+    const int l2 = std::min(13, lg - 4);
     const int l1 = lg - l2;
     cz.log1 = l1;
     cz.log2 = l2;

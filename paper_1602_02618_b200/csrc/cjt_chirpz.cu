@@ -251,8 +251,9 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
   extern __shared__ double2 smem[];
   const int64_t L2 = (int64_t)1 << cz.log2;
   const int64_t L = cz.length;
-  const int64_t c0 = (int64_t)blockIdx.x * NC;
-  const int64_t b = blockIdx.y;
+  // consecutive CTAs share a column tile across vectors: the pre table stays in L2
+  const int64_t c0 = (int64_t)blockIdx.y * NC;
+  const int64_t b = blockIdx.x;
   const double* xb = x + b * ldx + cz.p0;
   const int grp = threadIdx.x / (L1 / 16);
   const int t = threadIdx.x % (L1 / 16);
@@ -288,46 +289,37 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
 template <int LOG2>
 struct RowCfg {
   static constexpr int L2 = 1 << LOG2;
+  static constexpr int LEPT = LOG2 == 13 ? 5 : 4;
+  static constexpr int EPT = 1 << LEPT;
   static constexpr int E = (L2 >= 4096) ? L2 : 4096;
   static constexpr int NR = E / L2;
-  static constexpr int T = E / 16;
+  static constexpr int T = E / EPT;
   static constexpr int SMEM = NR * padded_len(L2) * 16;
 };
 
 // pass 2: rows k1 of buf: FFT over n2 -> * khat[k1][k2] -> inverse FFT over k2
+// (global load fused into the first forward pass, the spectrum product into
+// the first inverse pass, the global store into the last inverse pass)
 template <int LOG2>
 __global__ void __launch_bounds__(RowCfg<LOG2>::T)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ tw, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
   constexpr int L2 = Cfg::L2, NR = Cfg::NR;
-  constexpr int TPG = L2 / 16;
+  constexpr int TPG = L2 / Cfg::EPT;
   extern __shared__ double2 smem[];
   const int grp = threadIdx.x / TPG;
   const int t = threadIdx.x % TPG;
-  const int64_t k1 = (int64_t)blockIdx.x * NR + grp;
+  // consecutive CTAs share spectrum rows across (vector, term): khat stays in L2
+  const int64_t k1 = (int64_t)blockIdx.y * NR + grp;
   const int64_t L = cz.length;
-  double2* row = buf + (int64_t)blockIdx.y * L + k1 * L2;
+  double2* row = buf + (int64_t)blockIdx.x * L + k1 * L2;
   const double2* kh = cz.khat + k1 * L2;
   double2* s = smem + grp * padded_len(L2);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int e = t + i * TPG;
-    s[pad16(e)] = row[e];
-  }
-  __syncthreads();
-  fft_smem<LOG2, -1>(s, t, tw);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int e = t + i * TPG;
-    s[pad16(e)] = cmul(s[pad16(e)], __ldg(kh + e));
-  }
-  __syncthreads();
-  fft_smem<LOG2, +1>(s, t, tw);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int e = t + i * TPG;
-    row[e] = s[pad16(e)];
-  }
+  auto load_row = [&](int e) -> double2 { return row[e]; };
+  fft_smem_io<LOG2, -1, decltype(load_row), SmemStore, Cfg::LEPT>(s, t, tw, load_row, SmemStore{s});
+  auto load_spec = [&](int e) -> double2 { return cmul(s[pad16(e)], __ldg(kh + e)); };
+  auto store_row = [&](int e, double2 v) { row[e] = v; };
+  fft_smem_io<LOG2, +1, decltype(load_spec), decltype(store_row), Cfg::LEPT>(s, t, tw, load_spec, store_row);
 }
 
 // pass 3: columns n2: * W_L^{-n2 k1} -> inverse FFT over k1 -> sum_m Re(post_m * y) -> out
@@ -340,8 +332,8 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
   extern __shared__ double2 smem[];
   const int64_t L2 = (int64_t)1 << cz.log2;
   const int64_t L = cz.length;
-  const int64_t c0 = (int64_t)blockIdx.x * NC;
-  const int64_t b = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.y * NC;
+  const int64_t b = blockIdx.x;
   const int grp = threadIdx.x / (L1 / 16);
   const int t = threadIdx.x % (L1 / 16);
   double acc[16];
@@ -455,7 +447,7 @@ int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_
     init = true;
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
-  dim3 grid((unsigned)(L2 / Cfg::NC), (unsigned)batch);
+  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
   k_chirpz_cols_fwd<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, buf);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
@@ -470,7 +462,7 @@ int run_rows(const ChirpZDev& cz, const double2* tw, double2* buf, int64_t batch
     init = true;
   }
   const int64_t L1 = (int64_t)1 << cz.log1;
-  dim3 grid((unsigned)(L1 / Cfg::NR), (unsigned)(batch * cz.m_count));
+  dim3 grid((unsigned)(batch * cz.m_count), (unsigned)(L1 / Cfg::NR));
   k_chirpz_rows<LOG2><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
@@ -486,7 +478,7 @@ int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, dou
     init = true;
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
-  dim3 grid((unsigned)(L2 / Cfg::NC), (unsigned)batch);
+  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
   k_chirpz_cols_inv<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf, out, ldo);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
@@ -529,21 +521,23 @@ int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, i
   int rc = CJT_OK;
   switch (cz.log1) {
 #define CJT_COLF(K) case K: rc = run_cols_fwd<K>(cz, tw8192, x, ldx, scratch, batch, st); break;
-    CJT_COLF(7) CJT_COLF(8) CJT_COLF(9) CJT_COLF(10) CJT_COLF(11) CJT_COLF(12) CJT_COLF(13)
+    CJT_COLF(4) CJT_COLF(5) CJT_COLF(6) CJT_COLF(7) CJT_COLF(8) CJT_COLF(9) CJT_COLF(10) CJT_COLF(11)
+    CJT_COLF(12) CJT_COLF(13)
 #undef CJT_COLF
     default: return fail(CJT_EINVAL, "chirp-z column length out of range");
   }
   if (rc) return rc;
   switch (cz.log2) {
 #define CJT_ROW(K) case K: rc = run_rows<K>(cz, tw8192, scratch, batch, st); break;
-    CJT_ROW(7) CJT_ROW(8) CJT_ROW(9) CJT_ROW(10) CJT_ROW(11) CJT_ROW(12) CJT_ROW(13)
+    CJT_ROW(10) CJT_ROW(11) CJT_ROW(12) CJT_ROW(13)
 #undef CJT_ROW
     default: return fail(CJT_EINVAL, "chirp-z row length out of range");
   }
   if (rc) return rc;
   switch (cz.log1) {
 #define CJT_COLI(K) case K: rc = run_cols_inv<K>(cz, tw8192, scratch, out, ldo, batch, st); break;
-    CJT_COLI(7) CJT_COLI(8) CJT_COLI(9) CJT_COLI(10) CJT_COLI(11) CJT_COLI(12) CJT_COLI(13)
+    CJT_COLI(4) CJT_COLI(5) CJT_COLI(6) CJT_COLI(7) CJT_COLI(8) CJT_COLI(9) CJT_COLI(10) CJT_COLI(11)
+    CJT_COLI(12) CJT_COLI(13)
 #undef CJT_COLI
     default: return fail(CJT_EINVAL, "chirp-z column length out of range");
   }

@@ -541,11 +541,10 @@ def _cost_per_point(length: int) -> float:
     list, profiles/) of one Bluestein convolution of this length: on-chip
     fused tiles vs the multi-pass (HBM round-trip) path."""
     if length <= 4096:
-        return 19.0
+        return 16.5
     if length <= FUSED_MAX:
-        return 21.7
-    lg = length.bit_length() - 1
-    return 31.0 + 2.0 * max(0, lg - 15)
+        return 19.0
+    return 32.0
 
 
 def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
