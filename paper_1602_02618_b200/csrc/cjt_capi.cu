@@ -57,7 +57,6 @@ struct cjt_plan {
   double2* tw8192 = nullptr;
   double* scal = nullptr;
   int64_t scratch_elems_per_vec = 0;  // complex elements of multipass scratch per vector
-  int64_t part_elems_per_vec = 0;     // doubles of m-split chirp-z partials per vector
   double fft_points = 0.0;
 
   // batch-dependent state (cjt_plan_reserve)
@@ -97,6 +96,7 @@ struct cjt_plan {
     double* yacc = nullptr;    // inverse block accumulator [B][N+1]
     double* czpart = nullptr;  // chirp-z m-split partials
     double2* scratch = nullptr;
+    double2* spec = nullptr;   // tiled chirp-z spectrum sums
     double* io_in = nullptr;
     double* io_out = nullptr;
   };
@@ -203,6 +203,8 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   }
   cz.n_in = d.n_tiles_in;
   cz.n_out = d.n_tiles_out;
+  cz.count_max = 0;
+  for (int j = 0; j < d.n_tiles_out; ++j) cz.count_max = std::max<int64_t>(cz.count_max, d.tiles_out[2 * j + 1]);
   if (int rc = upload(P->allocs, const_cast<int64_t**>(&cz.tin), d.tiles_in, (size_t)2 * d.n_tiles_in)) return rc;
   if (int rc = upload(P->allocs, const_cast<int64_t**>(&cz.tout), d.tiles_out, (size_t)2 * d.n_tiles_out)) return rc;
   cz.log2len = lg;
@@ -218,7 +220,6 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     const size_t nk = (size_t)d.length * d.n_tiles_in * d.n_tiles_out;
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, nk)) return rc;
   }
-  if (d.m_count > 1) P->part_elems_per_vec = std::max<int64_t>(P->part_elems_per_vec, d.m_count * d.count);
   if (lg >= 14) {
     const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
     std::vector<double2> hi((size_t)nhi), lo(4096);
@@ -553,15 +554,32 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
     W.yacc = (double*)p;
     bytes += N1 * batch * 8;
   }
-  if (P->part_elems_per_vec > 0) {
-    if (int rc = dalloc(W.allocs, &p, (size_t)(P->part_elems_per_vec * batch) * 8)) return rc;
-    W.czpart = (double*)p;
-    bytes += P->part_elems_per_vec * batch * 8;
-  }
   if (P->scratch_elems_per_vec > 0) {
     if (int rc = dalloc(W.allocs, &p, (size_t)(P->scratch_elems_per_vec * batch) * 16)) return rc;
     W.scratch = (double2*)p;
     bytes += P->scratch_elems_per_vec * batch * 16;
+  }
+  int64_t cz_part = 0, cz_spec = 0;
+  {
+    std::vector<const ChirpZDev*> czs;
+    if (P->edge.length > 0) czs.push_back(&P->edge);
+    for (const ChirpZDev& cz : P->blocks) czs.push_back(&cz);
+    for (const ChirpZDev* cz : czs) {
+      int64_t pe, se;
+      chirpz_workspace(*cz, batch, &pe, &se);
+      cz_part = std::max(cz_part, pe);
+      cz_spec = std::max(cz_spec, se);
+    }
+  }
+  if (cz_part > 0) {
+    if (int rc = dalloc(W.allocs, &p, (size_t)cz_part * 8)) return rc;
+    W.czpart = (double*)p;
+    bytes += cz_part * 8;
+  }
+  if (cz_spec > 0) {
+    if (int rc = dalloc(W.allocs, &p, (size_t)cz_spec * 16)) return rc;
+    W.spec = (double2*)p;
+    bytes += cz_spec * 16;
   }
   if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
   W.io_in = (double*)p;
@@ -607,19 +625,19 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
     }
     if (blk)
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, W.spec, st, &launches))
           return rc;
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, W.vals, G1, out, N1, batch, W.scratch, W.czpart, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, W.vals, G1, out, N1, batch, W.scratch, W.czpart, W.spec, st, &launches))
         return rc;
   } else {
     if (edge)
-      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, st, &launches))
+      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, W.spec, st, &launches))
         return rc;
     if (blk && !P->blocks.empty()) {
       CJT_CUDA_TRY(cudaMemsetAsync(W.yacc, 0, (size_t)(N1 * batch) * 8, st));
       for (const ChirpZDev& cz : P->blocks)
-        if (int rc = launch_chirpz(cz, P->tw8192, W.vals, G1, W.yacc, N1, batch, W.scratch, W.czpart, st, &launches))
+        if (int rc = launch_chirpz(cz, P->tw8192, W.vals, G1, W.yacc, N1, batch, W.scratch, W.czpart, W.spec, st, &launches))
           return rc;
     }
     if (rec && P->two_pass) {

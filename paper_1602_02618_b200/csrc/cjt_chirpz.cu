@@ -23,6 +23,7 @@
 //              inverse FFT fused in one pass; column inverse FFTs with the
 //              output diagonal and the sum over m fused into the store.
 #include <cooperative_groups.h>
+#include <climits>
 #include <cstdlib>
 
 #include "cjt_internal.cuh"
@@ -34,100 +35,217 @@ namespace {
 template <int LOGL>
 struct FusedCfg {
   static constexpr int L = 1 << LOGL;
-  static constexpr int LEPT = LOGL == 13 ? 5 : 4;   // radix-32 passes for 8192: 3 passes, not 4
+#ifndef CJT_FUSED13_LEPT
+#define CJT_FUSED13_LEPT 4
+#endif
+  // 8192 with radix-16 passes: 512 threads (16 warps) hide the global-load
+  // latency of the fused first / last passes better than radix-32 with 8 warps
+  static constexpr int LEPT = LOGL == 13 ? CJT_FUSED13_LEPT : 4;
   static constexpr int EPT = 1 << LEPT;             // elements per thread
   static constexpr int E = (L >= 4096) ? L : 4096;  // complex elements per CTA
   static constexpr int NG = E / L;                  // vectors per CTA
   static constexpr int T = E / EPT;                 // threads per CTA
-  static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8;
+  // 8192: the FFT buffer and accumulator leave ~23 KB of L1, less than the
+  // global twiddle table's working set -> twiddles from shared memory
+  static constexpr bool TW_SMEM = LOGL == 13;
+  static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8 + (TW_SMEM ? 1024 * 16 : 0);
 };
 
-// grid: (vector groups, output tiles, m groups).  Each CTA accumulates its
-// output tile over its m range and over all input tiles in shared memory.
-// part == nullptr: write out (= or +=); else plain-store the m-group partial
-// to part[z][b][offset + s] for the fixed-order combine kernel.
-template <int LOGL>
-__global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
-    k_chirpz_fused(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
-                   int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch,
-                   double* __restrict__ part, int m_per_cta) {
+// Schedule of a fused chirp-z launch.  Work unit u = (vector group, output
+// tile j, term m), u = (grp * n_out + j) * M + m; each unit is n_in forward
+// FFTs (one per input tile, spectra summed) and one inverse FFT.
+//   direct:   grid (groups, n_out), one CTA per (grp, j) runs all m and
+//             accumulates the output tile in shared memory;
+//   stream-K: P CTAs each take a contiguous range of the F = U * n_in
+//             forward FFTs (f -> unit f / n_in, tile f % n_in); a unit cut by
+//             a range boundary is finished by each CTA on its part (one extra
+//             inverse FFT).  Every (CTA, unit) segment writes its output tile
+//             to a partial slot; a fixed-order combine sums slots and terms
+//             (deterministic).  Removes the wave-quantisation tail of small
+//             grids (e.g. 448 CTAs on 148 SMs at one CTA per SM).
+struct FusedSched {
+  int streamk;       // 0: direct
+  int64_t U, F;      // units, forward FFTs
+  int64_t P;         // CTAs (stream-K)
+  int64_t S;         // partial slots per CTA (stream-K)
+  __host__ __device__ int64_t start(int64_t c) const { return F * c / P; }
+  // CTA whose range holds forward FFT f
+  __host__ __device__ int64_t cta_of(int64_t f) const { return ((f + 1) * P + F - 1) / F - 1; }
+};
+
+template <int LOGL, class TW, class Sink>
+__device__ __forceinline__ void fused_unit(const ChirpZDev& cz, const TW& tw, double2* s, int t,
+                                           bool valid, const double* xb, int j, int m, int ti0,
+                                           int ti1, double2* specb, const Sink& sink) {
   using Cfg = FusedCfg<LOGL>;
   constexpr int L = Cfg::L;
-  constexpr int EPT = Cfg::EPT;
-  constexpr int TPG = L / EPT;
-  extern __shared__ double2 smem[];
-  const int grp = threadIdx.x / TPG;
-  const int t = threadIdx.x % TPG;
+  const double2* pre = cz.pre + (int64_t)m * cz.width;
+  for (int ti = ti0; ti < ti1; ++ti) {
+    const int64_t to = cz.tin[2 * ti], tn = cz.tin[2 * ti + 1];
+    // forward FFT straight from global: x * pre (zero padded)
+    auto load_x = [&](int e) -> double2 {
+      if (valid && e < tn) {
+        const double xv = __ldg(xb + to + e);
+        const double2 p = __ldg(pre + to + e);
+        return make_double2(xv * p.x, xv * p.y);
+      }
+      return make_double2(0.0, 0.0);
+    };
+    // spectrum product fused into the last pass.  Input tiles are summed in
+    // the frequency domain (one inverse FFT per unit, not per input tile):
+    // the running sum lives in the L2-resident spec buffer, each element
+    // owned by one thread (the last pass's output positions are fixed), and
+    // the final tile writes the total into shared memory.
+    const double2* kh = cz.khat + ((int64_t)j * cz.n_in + ti) * L;
+    const bool first = ti == ti0, last = ti == ti1 - 1;
+    auto store_spec = [&](int e, double2 v) {
+      double2 y = cmul(v, __ldg(kh + e));
+      if (!first && valid) {
+        const double2 a = __ldcg(specb + e);
+        y.x += a.x;
+        y.y += a.y;
+      }
+      if (last)
+        s[pad16(e)] = y;
+      else if (valid)
+        __stcg(specb + e, y);
+    };
+    fft_smem_io<LOGL, -1, decltype(load_x), decltype(store_spec), Cfg::LEPT>(s, t, tw, load_x, store_spec);
+  }
+  // inverse FFT: output diagonal fused into the last pass, value to the sink
+  const int64_t so = cz.tout[2 * j], sc = cz.tout[2 * j + 1];
+  const double2* post = cz.post + (int64_t)m * cz.count + so;
+  auto store_out = [&](int e, double2 y) {
+    if (e < sc) {
+      const double2 q = __ldg(post + e);
+      sink(e, fma(q.x, y.x, -q.y * y.y));
+    }
+  };
+  fft_smem_io<LOGL, +1, SmemLoad, decltype(store_out), Cfg::LEPT>(s, t, tw, SmemLoad{s}, store_out);
+}
+
+template <int LOGL, class TW>
+__device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, double2* s, double* acc,
+                                             int t, int grp, const double* __restrict__ x, int64_t ldx,
+                                             double* __restrict__ out, int64_t ldo, int64_t batch,
+                                             double2* __restrict__ spec) {
+  using Cfg = FusedCfg<LOGL>;
+  constexpr int L = Cfg::L;
+  constexpr int TPG = L / Cfg::EPT;
   const int64_t b = (int64_t)blockIdx.x * Cfg::NG + grp;
   const bool valid = b < batch;
-  double2* s = smem + grp * padded_len(L);
-  double* acc = reinterpret_cast<double*>(smem + Cfg::NG * padded_len(L)) + grp * L;
   const double* xb = x + (valid ? b : 0) * ldx + cz.p0;
   const int j = blockIdx.y;
   const int64_t so = cz.tout[2 * j], sc = cz.tout[2 * j + 1];
-  const int m0 = blockIdx.z * m_per_cta;
-  const int m1 = min(m0 + m_per_cta, (int)cz.m_count);
+  double2* specb = (cz.n_in > 1 && valid) ? spec + ((int64_t)blockIdx.x * gridDim.y + j) * Cfg::NG * L +
+                                                 (int64_t)grp * L
+                                          : nullptr;
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) acc[t + i * TPG] = 0.0;
-
-  for (int m = m0; m < m1; ++m) {
-    const double2* pre = cz.pre + (int64_t)m * cz.width;
-    const double2* post = cz.post + (int64_t)m * cz.count + so;
-    for (int ti = 0; ti < cz.n_in; ++ti) {
-      const int64_t to = cz.tin[2 * ti], tn = cz.tin[2 * ti + 1];
-      // forward FFT straight from global: x * pre (zero padded)
-      auto load_x = [&](int e) -> double2 {
-        if (valid && e < tn) {
-          const double xv = __ldg(xb + to + e);
-          const double2 p = __ldg(pre + to + e);
-          return make_double2(xv * p.x, xv * p.y);
-        }
-        return make_double2(0.0, 0.0);
-      };
-      fft_smem_io<LOGL, -1, decltype(load_x), SmemStore, Cfg::LEPT>(s, t, tw, load_x, SmemStore{s});
-      // inverse FFT: spectrum product fused into the first pass, output
-      // diagonal and the sum over (m, input tile) fused into the last pass
-      const double2* kh = cz.khat + ((int64_t)j * cz.n_in + ti) * L;
-      auto load_spec = [&](int e) -> double2 { return cmul(s[pad16(e)], __ldg(kh + e)); };
-      auto store_out = [&](int e, double2 y) {
-        if (e < sc) {
-          const double2 q = __ldg(post + e);
-          acc[e] += fma(q.x, y.x, -q.y * y.y);
-        }
-      };
-      fft_smem_io<LOGL, +1, decltype(load_spec), decltype(store_out), Cfg::LEPT>(s, t, tw, load_spec, store_out);
-    }
-  }
+  for (int i = 0; i < Cfg::EPT; ++i) acc[t + i * TPG] = 0.0;
+  auto sink = [&](int e, double v) { acc[e] += v; };
+  for (int m = 0; m < cz.m_count; ++m) fused_unit<LOGL>(cz, tw, s, t, valid, xb, j, m, 0, cz.n_in, specb, sink);
   __syncthreads();
   if (!valid) return;
-  if (part) {
-    double* pb = part + ((int64_t)blockIdx.z * batch + b) * cz.count + so;
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = t + i * TPG;
-      if (e < sc) pb[e] = acc[e];
-    }
-    return;
-  }
   double* ob = out + b * ldo + cz.q0 + so;
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) {
+  for (int i = 0; i < Cfg::EPT; ++i) {
     const int e = t + i * TPG;
     if (e < sc) ob[e] = cz.accumulate ? ob[e] + acc[e] : acc[e];
   }
 }
 
-// out[b][q0 + s] (+)= sum_z part[z][b][s], z in fixed order
-__global__ void k_chirpz_combine(const double* __restrict__ part, int nz, int64_t count,
-                                 int accumulate, double* __restrict__ out, int64_t ldo,
-                                 int64_t q0, int64_t batch) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t b = blockIdx.y;
-  if (s >= count) return;
-  double acc = 0.0;
-  for (int z = 0; z < nz; ++z) acc += part[((int64_t)z * batch + b) * count + s];
-  double* o = out + b * ldo + q0 + s;
-  *o = accumulate ? *o + acc : acc;
+template <int LOGL, class TW>
+__device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw, double2* s, int t,
+                                              int grp, const double* __restrict__ x, int64_t ldx,
+                                              int64_t batch, double* __restrict__ part,
+                                              double2* __restrict__ spec, const FusedSched& sk) {
+  using Cfg = FusedCfg<LOGL>;
+  constexpr int L = Cfg::L;
+  const int64_t c = blockIdx.x;
+  const int64_t f0 = sk.start(c), f1 = sk.start(c + 1);
+  const int64_t u_first = f0 / cz.n_in;
+  double2* specb = spec + (c * Cfg::NG + grp) * L;
+  const int M = cz.m_count;
+  for (int64_t f = f0; f < f1;) {
+    const int64_t u = f / cz.n_in;
+    const int ti0 = (int)(f % cz.n_in);
+    const int ti1 = (int)min((int64_t)cz.n_in, (int64_t)ti0 + (f1 - f));
+    const int64_t gj = u / M;
+    const int m = (int)(u % M);
+    const int64_t g = gj / cz.n_out;
+    const int j = (int)(gj % cz.n_out);
+    const int64_t b = g * Cfg::NG + grp;
+    const bool valid = b < batch;
+    const double* xb = x + (valid ? b : 0) * ldx + cz.p0;
+    double* slot = part + (((c * sk.S + (u - u_first)) * Cfg::NG) + grp) * cz.count_max;
+    auto sink = [&](int e, double v) {
+      if (valid) slot[e] = v;
+    };
+    fused_unit<LOGL>(cz, tw, s, t, valid, xb, j, m, ti0, ti1, specb, sink);
+    f += ti1 - ti0;
+  }
+}
+
+// grid: direct (groups, n_out) or stream-K (P); see FusedSched.
+template <int LOGL>
+__global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
+    k_chirpz_fused(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
+                   int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch,
+                   double* __restrict__ part, double2* __restrict__ spec, FusedSched sk) {
+  using Cfg = FusedCfg<LOGL>;
+  constexpr int L = Cfg::L;
+  constexpr int TPG = L / Cfg::EPT;
+  extern __shared__ double2 smem[];
+  const int grp = threadIdx.x / TPG;
+  const int t = threadIdx.x % TPG;
+  double2* s = smem + grp * padded_len(L);
+  double* acc = reinterpret_cast<double*>(smem + Cfg::NG * padded_len(L)) + grp * L;
+  if constexpr (Cfg::TW_SMEM) {
+    const TwSmem tws = tw_smem_init(reinterpret_cast<double2*>(acc + Cfg::E), tw);
+    if (sk.streamk)
+      fused_streamk<LOGL>(cz, tws, s, t, grp, x, ldx, batch, part, spec, sk);
+    else
+      fused_direct<LOGL>(cz, tws, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
+  } else {
+    if (sk.streamk)
+      fused_streamk<LOGL>(cz, tw, s, t, grp, x, ldx, batch, part, spec, sk);
+    else
+      fused_direct<LOGL>(cz, tw, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
+  }
+}
+
+// stream-K combine: out[b][q0 + so_j + e] (+)= sum over m, then over the
+// CTAs that cut unit (grp, j, m), of the partial slots (fixed order).
+// grid (e chunks, n_out, batch); slot ranges computed once per block.
+constexpr int COMBINE_MMAX = 64;
+__global__ void __launch_bounds__(256) k_chirpz_combine_sk(ChirpZDev cz, const double* __restrict__ part,
+                                                           FusedSched sk, int ng, double* __restrict__ out,
+                                                           int64_t ldo) {
+  __shared__ int64_t ca[COMBINE_MMAX], cb[COMBINE_MMAX], ka[COMBINE_MMAX];
+  const int j = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int64_t g = b / ng, gi = b % ng;
+  const int M = cz.m_count;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const int64_t u = (g * cz.n_out + j) * M + m;
+    ca[m] = sk.cta_of(u * cz.n_in);
+    cb[m] = sk.cta_of(u * cz.n_in + cz.n_in - 1);
+    ka[m] = u - sk.start(ca[m]) / cz.n_in;
+  }
+  __syncthreads();
+  const int64_t so = __ldg(cz.tout + 2 * j), sc = __ldg(cz.tout + 2 * j + 1);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= sc) return;
+  const int64_t stride = (int64_t)ng * cz.count_max;
+  const double* pe = part + gi * cz.count_max + e;
+  double v = 0.0;
+  for (int m = 0; m < M; ++m) {
+    // the first CTA holds the unit at slot k_a; later ones start inside it (slot 0)
+    v += pe[(ca[m] * sk.S + ka[m]) * stride];
+    for (int64_t c = ca[m] + 1; c <= cb[m]; ++c) v += pe[c * sk.S * stride];
+  }
+  double* o = out + b * ldo + cz.q0 + so + e;
+  *o = cz.accumulate ? *o + v : v;
 }
 
 // W_L^t = exp(-2 pi i t / L) from the two-level table (t < L)
@@ -383,27 +501,57 @@ int set_smem(K kernel, int bytes) {
   return CJT_OK;
 }
 
+int fused_groups(int lg) { return lg >= 12 ? 1 : (1 << (12 - lg)); }
+
+// direct unless stream-K shortens the modelled critical path by > 10 %
+// (time in forward-FFT units, inverse FFT ~ one unit; partial traffic ignored)
+FusedSched fused_sched(const ChirpZDev& cz, int64_t batch) {
+  const int ng = fused_groups(cz.log2len);
+  const int64_t slots = 148 * (cz.log2len <= 12 ? 2 : 1);
+  const int64_t gn = (batch + ng - 1) / ng * cz.n_out;
+  FusedSched sk{0, gn * cz.m_count, gn * cz.m_count * cz.n_in, 0, 0};
+  const int64_t t_direct = (gn + slots - 1) / slots * cz.m_count * (cz.n_in + 1);
+  const int64_t P = std::min(slots, sk.F);
+  const int64_t per = (sk.F + P - 1) / P;
+  const int64_t segs = per / cz.n_in + 2;   // units a CTA range touches (upper bound)
+  const int64_t t_sk = per + std::min(segs, per);
+  // $CJT_FUSED_SCHED (experiments): 1 forces direct, 2 stream-K
+  static const int force = [] {
+    const char* e = getenv("CJT_FUSED_SCHED");
+    return e ? atoi(e) : 0;
+  }();
+  const bool pick = force ? force == 2 : 10 * t_sk < 9 * t_direct;
+  if (pick && cz.m_count <= COMBINE_MMAX && batch <= 65535) {
+    sk.streamk = 1;
+    sk.P = P;
+    sk.S = segs;
+  }
+  return sk;
+}
+
 template <int LOGL>
 int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t ldx, double* out,
-              int64_t ldo, int64_t batch, double* part, cudaStream_t st, int* launches) {
+              int64_t ldo, int64_t batch, double* part, double2* spec, cudaStream_t st, int* launches) {
   using Cfg = FusedCfg<LOGL>;
+  static_assert(Cfg::NG == (LOGL >= 12 ? 1 : (1 << (12 - LOGL))), "fused_groups out of sync");
   static bool init = false;
   if (!init) {
     if (int rc = set_smem(k_chirpz_fused<LOGL>, Cfg::SMEM)) return rc;
     init = true;
   }
+  const FusedSched sk = fused_sched(cz, batch);
+  if (sk.streamk && (cz.m_count > COMBINE_MMAX || batch > 65535))
+    return fail(CJT_EINVAL, "chirp-z stream-K schedule out of range");
+  if (cz.n_in > 1 && !spec) return fail(CJT_EINVAL, "chirp-z without spectrum workspace");
+  if (sk.streamk && !part) return fail(CJT_EINVAL, "chirp-z without partial workspace");
   const int64_t groups = (batch + Cfg::NG - 1) / Cfg::NG;
-  // split the m terms over CTAs when the grid would not fill the GPU twice
-  const int msplit = (part && cz.m_count > 1 && groups * cz.n_out < 2 * 148) ? cz.m_count : 1;
-  dim3 grid((unsigned)groups, (unsigned)cz.n_out, (unsigned)msplit);
-  k_chirpz_fused<LOGL><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch,
-                                                         msplit > 1 ? part : nullptr,
-                                                         msplit > 1 ? 1 : cz.m_count);
+  dim3 grid = sk.streamk ? dim3((unsigned)sk.P) : dim3((unsigned)groups, (unsigned)cz.n_out);
+  k_chirpz_fused<LOGL><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch, part, spec, sk);
   CJT_CUDA_TRY(cudaGetLastError());
   *launches += 1;
-  if (msplit > 1) {
-    dim3 g2((unsigned)((cz.count + 255) / 256), (unsigned)batch);
-    k_chirpz_combine<<<g2, 256, 0, st>>>(part, msplit, cz.count, cz.accumulate, out, ldo, cz.q0, batch);
+  if (sk.streamk) {
+    dim3 g2((unsigned)((cz.count_max + 255) / 256), (unsigned)cz.n_out, (unsigned)batch);
+    k_chirpz_combine_sk<<<g2, 256, 0, st>>>(cz, part, sk, Cfg::NG, out, ldo);
     CJT_CUDA_TRY(cudaGetLastError());
     *launches += 1;
   }
@@ -486,6 +634,22 @@ int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, dou
 
 }  // namespace
 
+void chirpz_workspace(const ChirpZDev& cz, int64_t batch, int64_t* part_elems, int64_t* spec_elems) {
+  // sized for every execution batch up to the reserved one
+  *part_elems = *spec_elems = 0;
+  if (cz.length <= 0 || cz.log2len > 13) return;
+  const int ng = fused_groups(cz.log2len);
+  for (int64_t bb = 1; bb <= batch; ++bb) {
+    const FusedSched sk = fused_sched(cz, bb);
+    if (sk.streamk) {
+      *part_elems = std::max(*part_elems, sk.P * sk.S * ng * cz.count_max);
+      if (cz.n_in > 1) *spec_elems = std::max(*spec_elems, sk.P * ng * cz.length);
+    } else if (cz.n_in > 1) {
+      *spec_elems = std::max(*spec_elems, (bb + ng - 1) / ng * ng * cz.n_out * cz.length);
+    }
+  }
+}
+
 bool cluster_enabled() {
   static const bool on = [] {
     const char* e = getenv("CJT_CLUSTER");
@@ -496,12 +660,12 @@ bool cluster_enabled() {
 
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
                   double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
-                  cudaStream_t st, int* launches) {
+                  double2* spec, cudaStream_t st, int* launches) {
   if (batch <= 0) return CJT_OK;
   const int lg = cz.log2len;
   if (lg <= 13) {
     switch (lg) {
-#define CJT_FUSED(K) case K: return run_fused<K>(cz, tw8192, x, ldx, out, ldo, batch, part, st, launches);
+#define CJT_FUSED(K) case K: return run_fused<K>(cz, tw8192, x, ldx, out, ldo, batch, part, spec, st, launches);
       CJT_FUSED(4) CJT_FUSED(5) CJT_FUSED(6) CJT_FUSED(7) CJT_FUSED(8) CJT_FUSED(9) CJT_FUSED(10)
       CJT_FUSED(11) CJT_FUSED(12) CJT_FUSED(13)
 #undef CJT_FUSED

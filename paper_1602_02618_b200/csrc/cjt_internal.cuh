@@ -161,16 +161,48 @@ __device__ __forceinline__ void dft_reg(double2* v) {
 #define CJT_TW_MODE 1
 #endif
 
-// v[r] *= w^r for r = 1..R-1 with w = tw[u] (conjugated for DIR > 0);
+// Twiddle sources: W^u = exp(-2 pi i u / 8192), 0 <= u < 8192.
+// A plain pointer is the 8192-entry global table (read through L1).
+__device__ __forceinline__ double2 tw_at(const double2* __restrict__ tw, int u) { return __ldg(&tw[u]); }
+
+// TwSmem: 1024 entries W^r in shared memory and an octant rotation,
+// W^(1024 o + r) = exp(-i pi o / 4) W^r.  For kernels whose shared memory
+// leaves too little L1 to hold the global table's working set (an L2 round
+// trip per twiddle otherwise dominates).
+struct TwSmem {
+  const double2* tab;
+  __device__ __forceinline__ double2 operator()(int u) const {
+    double2 a = tab[u & 1023];
+    const int o = u >> 10;
+    if (o & 1) {   // times (1 - i) / sqrt 2
+      constexpr double c = 0.70710678118654752440;
+      a = make_double2((a.x + a.y) * c, (a.y - a.x) * c);
+    }
+    const int q = o >> 1;   // times (-i)^q
+    if (q & 1) a = make_double2(a.y, -a.x);
+    if (q & 2) a = make_double2(-a.x, -a.y);
+    return a;
+  }
+};
+__device__ __forceinline__ double2 tw_at(const TwSmem& tw, int u) { return tw(u); }
+
+// copy W^r, r < 1024, into shared memory (all threads of the CTA; syncs)
+__device__ __forceinline__ TwSmem tw_smem_init(double2* tab, const double2* __restrict__ tw) {
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) tab[i] = __ldg(&tw[i]);
+  __syncthreads();
+  return TwSmem{tab};
+}
+
+// v[r] *= w^r for r = 1..R-1 with w = W^u (conjugated for DIR > 0);
 // w^(2^j) are read from the table (u 2^j < 8192 since r k < NS R <= 8192).
-template <int R, int DIR>
-__device__ __forceinline__ void twiddle_powers(double2* v, const double2* __restrict__ tw, int u) {
+template <int R, int DIR, class TW>
+__device__ __forceinline__ void twiddle_powers(double2* v, const TW& tw, int u) {
   double2 p[32];
-  p[1] = __ldg(&tw[u]);
-  if constexpr (R > 2) p[2] = __ldg(&tw[2 * u]);
-  if constexpr (R > 4) p[4] = __ldg(&tw[4 * u]);
-  if constexpr (R > 8) p[8] = __ldg(&tw[8 * u]);
-  if constexpr (R > 16) p[16] = __ldg(&tw[16 * u]);
+  p[1] = tw_at(tw, u);
+  if constexpr (R > 2) p[2] = tw_at(tw, 2 * u);
+  if constexpr (R > 4) p[4] = tw_at(tw, 4 * u);
+  if constexpr (R > 8) p[8] = tw_at(tw, 8 * u);
+  if constexpr (R > 16) p[16] = tw_at(tw, 16 * u);
   if constexpr (DIR > 0) {
 #pragma unroll
     for (int j = 1; j < R; j <<= 1) p[j].y = -p[j].y;
@@ -205,8 +237,8 @@ struct SmemStore {
   __device__ __forceinline__ void operator()(int e, double2 v) const { s[pad16(e)] = v; }
 };
 
-template <int LOGL, int DIR, int LEPT, int PASS, class LoadF, class StoreF>
-__device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __restrict__ tw,
+template <int LOGL, int DIR, int LEPT, int PASS, class LoadF, class StoreF, class TW>
+__device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
                                          const LoadF& first_load, const StoreF& last_store) {
   constexpr int NP = (LOGL + LEPT - 1) / LEPT;
   if constexpr (PASS < NP) {
@@ -241,7 +273,7 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __res
 #if CJT_TW_MODE == 0
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          double2 w = __ldg(&tw[(r * k) << SH]);
+          double2 w = tw_at(tw, (r * k) << SH);
           if (DIR > 0) w.y = -w.y;
           v[q * R + r] = cmul(v[q * R + r], w);
         }
@@ -266,15 +298,15 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const double2* __res
   }
 }
 
-template <int LOGL, int DIR, int LEPT = 4>
-__device__ __forceinline__ void fft_smem(double2* s, int t, const double2* __restrict__ tw) {
+template <int LOGL, int DIR, int LEPT = 4, class TW>
+__device__ __forceinline__ void fft_smem(double2* s, int t, const TW& tw) {
   static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
   fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, SmemLoad{s}, SmemStore{s});
 }
 
 // FFT with a custom first-pass source and last-pass sink (see SmemLoad/SmemStore)
-template <int LOGL, int DIR, class LoadF, class StoreF, int LEPT = 4>
-__device__ __forceinline__ void fft_smem_io(double2* s, int t, const double2* __restrict__ tw,
+template <int LOGL, int DIR, class LoadF, class StoreF, int LEPT = 4, class TW>
+__device__ __forceinline__ void fft_smem_io(double2* s, int t, const TW& tw,
                                             const LoadF& ld, const StoreF& st) {
   static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
   fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, ld, st);
@@ -293,6 +325,7 @@ struct ChirpZDev {
   const double2* tw_hi;     // multipass: exp(-2 pi i (a 4096) / L)
   const double2* tw_lo;     // multipass: exp(-2 pi i b / L), b < 4096
   int32_t n_in, n_out;      // tiling (fused path only; 1 x 1 otherwise)
+  int64_t count_max;        // largest output tile
   const int64_t* tin;       // [n_in][2] (offset, width)
   const int64_t* tout;      // [n_out][2] (offset, count)
 };
@@ -344,10 +377,14 @@ inline int pick_vt(int64_t batch) {
 // ---------------------------------------------------------------------------
 // launchers (host)
 // scratch: multi-pass buffer (batch x m x L complex); part: m-split partial
-// sums (m x batch x count doubles), used when too few CTAs would run.
+// sums (m x batch x count doubles), used when too few CTAs would run; spec:
+// per-CTA spectrum sums of input-tiled fused chirp-z (chirpz_spec_elems).
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
                   double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
-                  cudaStream_t st, int* launches);
+                  double2* spec, cudaStream_t st, int* launches);
+// workspace of one chirp-z at this batch: partial outputs (doubles) and
+// spectrum sums (complex elements)
+void chirpz_workspace(const ChirpZDev& cz, int64_t batch, int64_t* part_elems, int64_t* spec_elems);
 
 int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        double2* ck, cudaStream_t st);

@@ -537,14 +537,15 @@ FUSED_MAX = 8192        # largest Bluestein length kept entirely in one CTA's sh
 
 
 def _cost_per_point(length: int) -> float:
-    """Measured B200 cost (ps per point per term per vector, config-2 launch
-    list, profiles/) of one Bluestein convolution of this length: on-chip
-    fused tiles vs the multi-pass (HBM round-trip) path."""
+    """Measured B200 cost (ps per point per term per vector, per forward +
+    inverse FFT pair; config-2 launch lists, profiles/) of one Bluestein
+    convolution of this length: on-chip fused tiles (stream-K scheduled) vs the
+    multi-pass (HBM round-trip) path."""
     if length <= 4096:
-        return 16.5
+        return 20.7
     if length <= FUSED_MAX:
-        return 19.0
-    return 32.0
+        return 22.0
+    return 32.5
 
 
 def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
@@ -562,6 +563,9 @@ def _split(n: int, parts: int) -> np.ndarray:
     return np.stack([edges[:-1], edges[1:] - edges[:-1]], axis=1)
 
 
+KHAT_MAX_POINTS = 1 << 24    # tile spectra stored per chirp-z (x 16 B)
+
+
 def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     """Choose (length, n_in, n_out) for a width x count chirp-z: one untiled
     power-of-two Bluestein, or a grid of on-chip tiles, by measured cost."""
@@ -569,14 +573,15 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     best = (whole * _cost_per_point(whole), whole, 1, 1)
     lc = 1024
     while lc <= fused_max:
-        for n_in in range(1, 65):
+        n_min = -(-width // (lc - 1))
+        for n_in in range(n_min, 8 * n_min + 64):
             wc = -(-width // n_in)
-            if wc >= lc:
-                continue
             n_out = -(-count // (lc - wc + 1))
-            if n_in * n_out > 256:
+            if n_in * n_out * lc > KHAT_MAX_POINTS:
                 continue
-            cost = n_in * n_out * lc * _cost_per_point(lc)
+            # one forward FFT per input tile and one inverse FFT per output
+            # tile (input tiles are summed in the frequency domain)
+            cost = n_out * (n_in + 1) * 0.5 * lc * _cost_per_point(lc)
             if cost < best[0]:
                 best = (cost, lc, n_in, n_out)
         lc *= 2
