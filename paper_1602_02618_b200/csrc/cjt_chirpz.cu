@@ -404,6 +404,118 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
   }
 }
 
+// Short columns (L1 <= 32): one thread per column n2, the L1-point DFT in
+// registers -- no shared memory, no barriers; x and the twiddles W_L^{n2 k1}
+// are loaded once and reused for every term m.  Loads and stores of
+// consecutive threads are consecutive n2 (coalesced).
+constexpr int COLR_T = 128;
+
+// W_L^{n2 k}, k < R, from W_L^{n2 2^j} (at most three rounded products each)
+template <int R>
+__device__ __forceinline__ void column_twiddles(const ChirpZDev& cz, int64_t n2, double2* w) {
+  w[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int j = 1; j < R; j <<= 1) w[j] = twiddle_L(cz, n2 * j);
+#pragma unroll
+  for (int k = 3; k < R; ++k) {
+    if ((k & (k - 1)) != 0) {
+      const int hi = 1 << (31 - __clz(k));
+      w[k] = cmul(w[hi], w[k - hi]);
+    }
+  }
+}
+
+template <int LOG1>
+__global__ void __launch_bounds__(COLR_T)
+    k_chirpz_cols_fwd_reg(ChirpZDev cz, const double* __restrict__ x, int64_t ldx,
+                          double2* __restrict__ buf) {
+  constexpr int L1 = 1 << LOG1;
+  const int64_t L2 = (int64_t)1 << cz.log2;
+  const int64_t L = cz.length;
+  const int64_t n2 = (int64_t)blockIdx.y * COLR_T + threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const double* xb = x + b * ldx + cz.p0;
+  double xv[L1];
+#pragma unroll
+  for (int r = 0; r < L1; ++r) {
+    const int64_t pidx = r * L2 + n2;
+    xv[r] = pidx < cz.width ? __ldg(xb + pidx) : 0.0;
+  }
+  double2 w[L1];
+  column_twiddles<L1>(cz, n2, w);
+  for (int m = 0; m < cz.m_count; ++m) {
+    const double2* pre = cz.pre + (int64_t)m * cz.width;
+    double2 v[L1];
+#pragma unroll
+    for (int r = 0; r < L1; ++r) {
+      const int64_t pidx = r * L2 + n2;
+      const double2 p = pidx < cz.width ? __ldg(pre + pidx) : make_double2(0.0, 0.0);
+      v[r] = make_double2(xv[r] * p.x, xv[r] * p.y);
+    }
+    dft_reg<L1, -1>(v);
+    double2* bm = buf + (b * cz.m_count + m) * L + n2;
+#pragma unroll
+    for (int k = 0; k < L1; ++k) bm[k * L2] = cmul(v[k], w[k]);
+  }
+}
+
+template <int LOG1>
+__global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
+    k_chirpz_cols_inv_reg(ChirpZDev cz, const double2* __restrict__ buf, double* __restrict__ out,
+                          int64_t ldo) {
+  constexpr int L1 = 1 << LOG1;
+  const int64_t L2 = (int64_t)1 << cz.log2;
+  const int64_t L = cz.length;
+  const int64_t n2 = (int64_t)blockIdx.y * COLR_T + threadIdx.x;
+  const int64_t b = blockIdx.x;
+  double acc[L1];
+#pragma unroll
+  for (int r = 0; r < L1; ++r) acc[r] = 0.0;
+  // per term: the column and the output diagonal are loaded together (one
+  // latency per term).  Twiddles W_L^{-n2 k} = conj(W^{4 n2 (k >> 2)} W^{n2 (k & 3)})
+  // from six values kept in registers (one product per element)
+  double2 w1[4], w4[4];
+  w1[0] = w4[0] = make_double2(1.0, 0.0);
+  w1[1] = twiddle_L(cz, n2);
+  w4[1] = twiddle_L(cz, 4 * n2);
+  w1[2] = cmul(w1[1], w1[1]);
+  w1[3] = cmul(w1[2], w1[1]);
+  w4[2] = cmul(w4[1], w4[1]);
+  w4[3] = cmul(w4[2], w4[1]);
+  const double2* bcol = buf + b * cz.m_count * L + n2;
+  for (int m = 0; m < cz.m_count; ++m) {
+    const double2* post = cz.post + (int64_t)m * cz.count;
+    double2 v[L1], pq[L1];
+#pragma unroll
+    for (int k = 0; k < L1; ++k) v[k] = __ldcs(bcol + (int64_t)m * L + k * L2);
+#pragma unroll
+    for (int r = 0; r < L1; ++r) {
+      const int64_t q = r * L2 + n2;
+      pq[r] = q < cz.count ? __ldg(post + q) : make_double2(0.0, 0.0);
+    }
+    // keep the six base twiddles opaque per iteration: otherwise the compiler
+    // hoists all L1 products out of the m loop (32 more live registers)
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+      asm volatile("" : "+d"(w1[i].x), "+d"(w1[i].y), "+d"(w4[i].x), "+d"(w4[i].y));
+#pragma unroll
+    for (int k = 1; k < L1; ++k) {
+      double2 w = (k & 3) == 0 ? w4[(k >> 2) & 3] : ((k >> 2) & 3) == 0 ? w1[k & 3] : cmul(w4[(k >> 2) & 3], w1[k & 3]);
+      if (k >= 16) w = cmul(w, twiddle_L(cz, 16 * n2 * (k >> 4)));
+      v[k] = cmul(v[k], make_double2(w.x, -w.y));
+    }
+    dft_reg<L1, +1>(v);
+#pragma unroll
+    for (int r = 0; r < L1; ++r) acc[r] += fma(pq[r].x, v[r].x, -pq[r].y * v[r].y);
+  }
+  double* ob = out + b * ldo + cz.q0;
+#pragma unroll
+  for (int r = 0; r < L1; ++r) {
+    const int64_t q = r * L2 + n2;
+    if (q < cz.count) ob[q] = cz.accumulate ? ob[q] + acc[r] : acc[r];
+  }
+}
+
 template <int LOG2>
 struct RowCfg {
   static constexpr int L2 = 1 << LOG2;
@@ -419,7 +531,7 @@ struct RowCfg {
 // (global load fused into the first forward pass, the spectrum product into
 // the first inverse pass, the global store into the last inverse pass)
 template <int LOG2>
-__global__ void __launch_bounds__(RowCfg<LOG2>::T)
+__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ tw, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
   constexpr int L2 = Cfg::L2, NR = Cfg::NR;
@@ -595,6 +707,12 @@ int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_
     init = true;
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
+  if constexpr (LOG1 <= 5) {
+    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T));
+    k_chirpz_cols_fwd_reg<LOG1><<<grid, COLR_T, 0, st>>>(cz, x, ldx, buf);
+    CJT_CUDA_TRY(cudaGetLastError());
+    return CJT_OK;
+  }
   dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
   k_chirpz_cols_fwd<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, buf);
   CJT_CUDA_TRY(cudaGetLastError());
@@ -626,6 +744,12 @@ int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, dou
     init = true;
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
+  if constexpr (LOG1 <= 5) {
+    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T));
+    k_chirpz_cols_inv_reg<LOG1><<<grid, COLR_T, 0, st>>>(cz, buf, out, ldo);
+    CJT_CUDA_TRY(cudaGetLastError());
+    return CJT_OK;
+  }
   dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
   k_chirpz_cols_inv<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf, out, ldo);
   CJT_CUDA_TRY(cudaGetLastError());
