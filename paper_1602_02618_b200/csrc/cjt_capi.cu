@@ -231,7 +231,11 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (lg >= 14 && !cluster) {
     // longest on-chip rows (8192, radix-32 passes) and short columns: wide,
     // coalesced column tiles (E / L1 columns) in passes 1 and 3
-    const int l2 = std::min(13, lg - 4);
+    static const int l2max = [] {   // $CJT_MP_L2MAX (experiments): longest on-chip row
+      const char* e = getenv("CJT_MP_L2MAX");
+      return e ? std::max(10, std::min(13, atoi(e))) : 13;
+    }();
+    const int l2 = std::min(l2max, lg - 4);
     const int l1 = lg - l2;
     cz.log1 = l1;
     cz.log2 = l2;

@@ -361,7 +361,7 @@ struct ColCfg {
 
 // pass 1: x (real slice) * pre_m -> column FFTs over n1 -> * W_L^{n2 k1} -> buf[b][m][k1][n2]
 template <int LOG1>
-__global__ void __launch_bounds__(ColCfg<LOG1>::T)
+__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
     k_chirpz_cols_fwd(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
                       int64_t ldx, double2* __restrict__ buf) {
   using Cfg = ColCfg<LOG1>;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
   const int t = threadIdx.x % (L1 / 16);
   for (int m = 0; m < cz.m_count; ++m) {
     const double2* pre = cz.pre + (int64_t)m * cz.width;
-#pragma unroll 4
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int idx = threadIdx.x + i * T;
       const int c = idx % NC, n1 = idx / NC;
@@ -393,12 +393,18 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
     __syncthreads();
     fft_smem<LOG1, -1>(smem + grp * CS, t, tw);
     double2* bm = buf + (b * cz.m_count + m) * L;
-#pragma unroll 4
+    // this thread's column n2 is fixed and k1 = k1_0 + i T/NC: twiddles
+    // W_L^{n2 k1} by a running product from two table values
+    const int c = threadIdx.x % NC;
+    const int64_t n2 = c0 + c;
+    const int k10 = threadIdx.x / NC;
+    double2 w = twiddle_L(cz, n2 * k10);
+    const double2 ws = twiddle_L(cz, n2 * (T / NC));
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int idx = threadIdx.x + i * T;
-      const int c = idx % NC, k1 = idx / NC;
-      const int64_t n2 = c0 + c;
-      bm[(int64_t)k1 * L2 + n2] = cmul(smem[c * CS + pad16(k1)], twiddle_L(cz, n2 * k1));
+      const int k1 = k10 + i * (T / NC);
+      bm[(int64_t)k1 * L2 + n2] = cmul(smem[c * CS + pad16(k1)], w);
+      w = cmul(w, ws);
     }
     __syncthreads();
   }
@@ -554,7 +560,7 @@ __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
 
 // pass 3: columns n2: * W_L^{-n2 k1} -> inverse FFT over k1 -> sum_m Re(post_m * y) -> out
 template <int LOG1>
-__global__ void __launch_bounds__(ColCfg<LOG1>::T)
+__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
     k_chirpz_cols_inv(ChirpZDev cz, const double2* __restrict__ tw,
                       const double2* __restrict__ buf, double* __restrict__ out, int64_t ldo) {
   using Cfg = ColCfg<LOG1>;
@@ -571,14 +577,18 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T)
   for (int i = 0; i < 16; ++i) acc[i] = 0.0;
   for (int m = 0; m < cz.m_count; ++m) {
     const double2* bm = buf + (b * cz.m_count + m) * L;
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const int idx = threadIdx.x + i * T;
-      const int c = idx % NC, k1 = idx / NC;
+    {
+      const int c = threadIdx.x % NC;
       const int64_t n2 = c0 + c;
-      double2 w = twiddle_L(cz, n2 * k1);
-      w.y = -w.y;
-      smem[c * CS + pad16(k1)] = cmul(bm[(int64_t)k1 * L2 + n2], w);
+      const int k10 = threadIdx.x / NC;
+      double2 w = twiddle_L(cz, n2 * k10);
+      const double2 ws = twiddle_L(cz, n2 * (T / NC));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k1 = k10 + i * (T / NC);
+        smem[c * CS + pad16(k1)] = cmul(bm[(int64_t)k1 * L2 + n2], make_double2(w.x, -w.y));
+        w = cmul(w, ws);
+      }
     }
     __syncthreads();
     fft_smem<LOG1, +1>(smem + grp * CS, t, tw);
