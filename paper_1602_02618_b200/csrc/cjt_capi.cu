@@ -155,6 +155,27 @@ int upload(std::vector<void*>& list, T** dst, const T* src, size_t count) {
   return CJT_OK;
 }
 
+// Device recurrence tables: the reference's seven (A, B, C, rf+-, 1/rf+-) and
+// the FMA-form Reinsch tables A/rf+-, C/rf+- (products with the tabulated
+// reciprocals) used by the generation kernels.
+int upload_tables(std::vector<void*>& A, const double* const src[7], size_t tl, RecTablesDev* tab) {
+  double* t[7];
+  for (int k = 0; k < 7; ++k)
+    if (int rc = upload(A, &t[k], src[k], tl)) return rc;
+  *tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
+  std::vector<double> prod(tl);
+  const double* num[4] = {src[0], src[0], src[2], src[2]};
+  const double* den[4] = {src[5], src[6], src[5], src[6]};
+  const double** dst[4] = {&tab->Ap, &tab->Am, &tab->Cp, &tab->Cm};
+  for (int k = 0; k < 4; ++k) {
+    for (size_t i = 0; i < tl; ++i) prod[i] = num[k][i] * den[k][i];
+    double* d = nullptr;
+    if (int rc = upload(A, &d, prod.data(), tl)) return rc;
+    *dst[k] = d;
+  }
+  return CJT_OK;
+}
+
 // exp(-2 pi i num / den), long-double accurate
 inline void unit_root(int64_t num, int64_t den, double* re, double* im) {
   num %= den;
@@ -740,11 +761,8 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   if (int rc = upload(A, &cut, d->cuts, nr)) return rc;
   P->rows = RecRowsDev{x, xm, reg, cut, nr};
   const size_t tl = (size_t)d->table_len;
-  double* t[7];
   const double* src[7] = {d->A, d->B, d->C, d->rf_plus, d->rf_minus, d->rf_plus_inv, d->rf_minus_inv};
-  for (int k = 0; k < 7; ++k)
-    if (int rc = upload(A, &t[k], src[k], tl)) return rc;
-  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
+  if (int rc = upload_tables(A, src, tl, &P->tab)) return rc;
 
   // recurrence checkpoints every CK degrees
   std::vector<int64_t> off((size_t)nr);
@@ -964,11 +982,8 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   if (int rc = upload(Al, &dcut, cuts, (size_t)n_points)) return rc;
   P->rows = RecRowsDev{dx, dxm, dreg, dcut, n_points};
   const size_t tl = (size_t)std::max<int64_t>(maxcut, 1);
-  double* t[7];
   const double* src[7] = {A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv};
-  for (int k = 0; k < 7; ++k)
-    if (int rc = upload(Al, &t[k], src[k], tl)) return rc;
-  P->tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
+  if (int rc = upload_tables(Al, src, tl, &P->tab)) return rc;
   std::vector<int64_t> off((size_t)n_points);
   int64_t tot = 0;
   for (int64_t i = 0; i < n_points; ++i) {

@@ -341,7 +341,10 @@ struct RecRowsDev {
 struct RecTablesDev {
   const double *A, *B, *C, *rfp, *rfm, *rfpi, *rfmi;
   int64_t n_tab;   // entries per table
+  // FMA-form Reinsch tables (A, C scaled by 1/rf+-), see rec_step_fast
+  const double *Ap = nullptr, *Am = nullptr, *Cp = nullptr, *Cm = nullptr;
 };
+constexpr int REC_WIN_ROWS = 9;   // A, B, C, rf+, rf-, A/rf+, A/rf-, C/rf+, C/rf-
 
 // forward split-K work item: rows [row0, row0+nrows) x degrees [n_begin, n_end)
 struct FwdItem {

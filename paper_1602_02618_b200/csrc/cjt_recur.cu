@@ -73,34 +73,71 @@ __device__ __forceinline__ void load_state(const RecRowsDev& rows, const int64_t
   }
 }
 
+// Generation arithmetic of the contraction kernels (FMA form).  The
+// reference's rounding (rec_step) is kept where its exact values are the
+// contract: plan-time checkpoints and the Clenshaw plugin.  The P values the
+// transforms contract with are generated with the same recurrences in FMA
+// form, whose dependency chain is two operations per degree instead of five
+// (Reinsch) or two instead of three (three-term), with a' = A / rf, c' = C / rf
+// tabulated per degree:
+//   three-term: p_{n+1} = fma(fma(A x, 1, B), p_n, -(C p_{n-1}))
+//   Reinsch:    d = fma(a' xm, s0, c' s1);  s0 <- fma(rf, d, rf s0);  s1 <- d
+// (algebraically identical to _kernels_cy.pyx:144-147 / 186-188; differs by
+// rounding only, well inside the transform tolerance).
+__device__ __forceinline__ void rec_step_fast(int reg, double x, double xm, const RecTablesDev& t,
+                                              int64_t n, double& s0, double& s1) {
+  if (reg == 0) {
+    const double a = __ldg(t.A + n), bb = __ldg(t.B + n), c = __ldg(t.C + n);
+    const double pn = fma(fma(a, x, bb), s1, -(c * s0));
+    s0 = s1;
+    s1 = pn;
+  } else {
+    const double ap = __ldg((reg > 0 ? t.Ap : t.Am) + n);
+    const double cp = __ldg((reg > 0 ? t.Cp : t.Cm) + n);
+    const double rf = __ldg((reg > 0 ? t.rfp : t.rfm) + n);
+    const double d = fma(ap * xm, s0, cp * s1);
+    s0 = fma(rf, d, rf * s0);
+    s1 = d;
+  }
+}
+
 // Recurrence tables of a degree window staged in shared memory:
-// rows 0..6 = A, B, C, rf+, rf-, 1/rf+, 1/rf-, each `span` entries from n_lo.
+// rows 0..8 = A, B, C, rf+, rf-, A/rf+, A/rf-, C/rf+, C/rf- (REC_WIN_ROWS),
+// each `span` entries from n_lo.
 __device__ __forceinline__ const double* table_row(const RecTablesDev& t, int r) {
-  return r == 0 ? t.A : r == 1 ? t.B : r == 2 ? t.C : r == 3 ? t.rfp : r == 4 ? t.rfm : r == 5 ? t.rfpi : t.rfmi;
+  switch (r) {
+    case 0: return t.A;
+    case 1: return t.B;
+    case 2: return t.C;
+    case 3: return t.rfp;
+    case 4: return t.rfm;
+    case 5: return t.Ap;
+    case 6: return t.Am;
+    case 7: return t.Cp;
+    default: return t.Cm;
+  }
 }
 struct TabWin {
-  const double* t;   // [7][span]
+  const double* t;   // [REC_WIN_ROWS][span]
   int span;
 };
-// degree n_lo + nl -> n_lo + nl + 1 with window tables (same rounding as rec_step)
+// degree n_lo + nl -> n_lo + nl + 1 with window tables (rec_step_fast arithmetic)
 __device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w, int nl,
                                              double& s0, double& s1) {
 #ifdef CJT_FAKE_GEN
   s0 = s0 * 0.5 + xx; s1 = s0; return;
 #endif
-  const double a = w.t[nl];
-  const double c = w.t[2 * w.span + nl];
   if (reg == 0) {
-    const double bb = w.t[w.span + nl];
-    const double pn = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(a, xx), bb), s1), __dmul_rn(c, s0));
+    const double a = w.t[nl], bb = w.t[w.span + nl], c = w.t[2 * w.span + nl];
+    const double pn = fma(fma(a, xx, bb), s1, -(c * s0));
     s0 = s1;
     s1 = pn;
   } else {
-    const int o = reg > 0 ? 3 : 4;
-    const double rf = w.t[o * w.span + nl];
-    const double rfi = w.t[(o + 2) * w.span + nl];
-    const double d = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, xx), s0), __dmul_rn(c, s1)), rfi);
-    s0 = __dmul_rn(__dadd_rn(s0, d), rf);
+    const int o = reg > 0 ? 0 : 1;
+    const double rf = w.t[(3 + o) * w.span + nl];
+    const double ap = w.t[(5 + o) * w.span + nl], cp = w.t[(7 + o) * w.span + nl];
+    const double d = fma(ap * xx, s0, cp * s1);
+    s0 = fma(rf, d, rf * s0);
     s1 = d;
   }
 }
@@ -223,8 +260,8 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
   double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + W::NBUF * FWD_KS * PT);
-  double(*Ts)[7 * FWD_KS] =
-      reinterpret_cast<double(*)[7 * FWD_KS]>(smem_rec + W::NBUF * FWD_KS * PT + W::NBUF * VT * CS);
+  double(*Ts)[REC_WIN_ROWS * FWD_KS] =
+      reinterpret_cast<double(*)[REC_WIN_ROWS * FWD_KS]>(smem_rec + W::NBUF * FWD_KS * PT + W::NBUF * VT * CS);
   const FwdItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -244,7 +281,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
     }
     auto stage_tables = [&](int buf, int64_t n0) {
-      for (int idx = p; idx < 7 * FWD_KS; idx += W::NP) {
+      for (int idx = p; idx < REC_WIN_ROWS * FWD_KS; idx += W::NP) {
         const int r = idx / FWD_KS, k = idx % FWD_KS;
         const int64_t n = n0 + k;
         const bool ok = n < tab.n_tab;
@@ -357,7 +394,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
-  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NBUF * VT * WS;   // [7][SPAN]
+  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NBUF * VT * WS;   // [REC_WIN_ROWS][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -366,7 +403,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     // ------------------------------ producer ------------------------------
     const int p = tid - W::NC;
     const int grow = p >> 2, gq = p & 3;
-    for (int idx = p; idx < 7 * SPAN; idx += W::NP) {
+    for (int idx = p; idx < REC_WIN_ROWS * SPAN; idx += W::NP) {
       const int r = idx / SPAN, k = idx % SPAN;
       const bool ok = it.n0 + k < tab.n_tab;
       const double* src = table_row(tab, r);
@@ -548,7 +585,7 @@ __global__ void __launch_bounds__(128)
     for (int k = 0; k < FWD_KS; ++k) {
       const int64_t n = n0 + k;
       out[k * FWD_ROWS] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-      if (n + 1 < cut) rec_step(reg, x, xm, tab, n, s0, s1);
+      if (n + 1 < cut) rec_step_fast(reg, x, xm, tab, n, s0, s1);
     }
   }
 }
@@ -572,7 +609,7 @@ __global__ void __launch_bounds__(128)
     for (int k = 0; k < CK; ++k) {
       const int64_t n = nstart + k;
       out[k * INV_RT] = (n < cut) ? rec_value(reg, st.s0, st.s1) : 0.0;
-      if (n + 1 < cut) rec_step(reg, x, xm, tab, n, st.s0, st.s1);
+      if (n + 1 < cut) rec_step_fast(reg, x, xm, tab, n, st.s0, st.s1);
     }
   }
 }
@@ -707,7 +744,7 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
 #define CJT_FWD(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + R * V * (FWD_KS + 4) + 2 * 7 * FWD_KS);  \
+    const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + R * V * (FWD_KS + 4) + 2 * REC_WIN_ROWS * FWD_KS);  \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V>,                                     \
@@ -757,7 +794,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + 7 * INV_DT);         \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + REC_WIN_ROWS * INV_DT);         \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
