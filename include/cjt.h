@@ -104,7 +104,7 @@ typedef struct {
     int64_t workspace_bytes;
     int64_t reserved_batch;
     double rec_flops_per_vector;    /* 2 flop per (row, degree) contraction */
-    double fft_points_per_vector;   /* sum of Bluestein lengths x log2(length) x 2 */
+    double fft_points_per_vector;   /* sum over executed FFTs of length x log2(length) */
 } cjt_plan_stats;
 
 int cjt_version(void);

@@ -267,7 +267,9 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
     P->scratch_elems_per_vec = std::max<int64_t>(P->scratch_elems_per_vec, d.length * d.m_count);
   }
-  P->fft_points += 2.0 * d.m_count * d.n_tiles_in * d.n_tiles_out * (double)d.length * lg;
+  // FFTs executed per vector: per term, one forward FFT per input tile and one
+  // inverse FFT per output tile (tiles' spectra are summed before inverting)
+  P->fft_points += (double)d.m_count * d.n_tiles_out * (d.n_tiles_in + 1) * (double)d.length * lg;
   *out = cz;
   return CJT_OK;
 }

@@ -72,6 +72,23 @@ def launches(path):
     print("|---|---|---|")
     for i, n, t in items:
         print(f"| {i} | {n} | {t:.1f} |")
+    # per-execution share by kernel: plan-time kernels excluded, the profile run
+    # executes the transform pair `execs` times (one per k_inverse_finish launch)
+    plan_time = ("k_checkpoints", "k_build_inv_gen", "k_fp64_probe")
+    execs = max(1, sum(1 for _, n, _ in items if n.startswith("k_inverse_finish")))
+    agg = {}
+    for _, n, t in items:
+        if n.startswith(plan_time) or not n.startswith("k_"):
+            continue
+        base = n.split("<")[0]
+        agg[base] = agg.get(base, 0.0) + t / execs
+    tot = sum(agg.values())
+    print(f"\n## per execution of (forward, inverse), by kernel ({execs} executions; plan-time kernels excluded)\n")
+    print("| kernel | us | share |")
+    print("|---|---|---|")
+    for n, t in sorted(agg.items(), key=lambda kv: -kv[1]):
+        print(f"| {n} | {t:.1f} | {t / tot:.3f} |")
+    print(f"| total | {tot:.1f} | 1.000 |")
 
 
 if __name__ == "__main__":
