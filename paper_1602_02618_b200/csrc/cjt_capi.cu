@@ -237,9 +237,20 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   const double2* kh = reinterpret_cast<const double2*>(d.kernel_hat);
   const bool cluster = lg >= 14 && lg <= 17 && cluster_enabled();
   if (lg <= 13 || cluster) {
-    // fused / cluster paths read the spectra in natural order
+    // cluster / short fused tiles read the spectra in natural order; the
+    // two-level FFT (fft2_used) in the permuted order k1 S + k2 <- k1 + 16 k2
     const size_t nk = (size_t)d.length * d.n_tiles_in * d.n_tiles_out;
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, nk)) return rc;
+    if (lg <= 13 && fft2_used(lg)) {
+      const int64_t L = d.length, S = L / 16;
+      std::vector<double2> perm(nk);
+      for (size_t tile = 0; tile < nk / (size_t)L; ++tile)
+        for (int64_t k1 = 0; k1 < 16; ++k1)
+          for (int64_t k2 = 0; k2 < S; ++k2)
+            perm[tile * L + (size_t)(k1 * S + k2)] = kh[tile * L + (size_t)(k1 + 16 * k2)];
+      if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), nk)) return rc;
+    } else {
+      if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, nk)) return rc;
+    }
   }
   if (lg >= 14) {
     const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
@@ -262,8 +273,14 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     cz.log2 = l2;
     const int64_t L1 = int64_t(1) << l1, L2 = int64_t(1) << l2;
     std::vector<double2> perm((size_t)d.length);
+    const bool f2 = fft2_used(l2);
+    const int64_t S2 = L2 / 16;
     for (int64_t k1 = 0; k1 < L1; ++k1)
-      for (int64_t k2 = 0; k2 < L2; ++k2) perm[(size_t)(k1 * L2 + k2)] = kh[k1 + L1 * k2];
+      for (int64_t k2 = 0; k2 < L2; ++k2) {
+        // row k1, row spectrum index k2 (natural) or its two-level position
+        const int64_t pos = f2 ? (k2 % 16) * S2 + k2 / 16 : k2;
+        perm[(size_t)(k1 * L2 + pos)] = kh[k1 + L1 * k2];
+      }
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
     P->scratch_elems_per_vec = std::max<int64_t>(P->scratch_elems_per_vec, d.length * d.m_count);
   }

@@ -73,10 +73,81 @@ struct FusedSched {
   __host__ __device__ int64_t cta_of(int64_t f) const { return ((f + 1) * P + F - 1) / F - 1; }
 };
 
-template <int LOGL, class TW, class Sink>
+// two-level FFT (Fft2) for L >= 512; khat and the spectrum sums are then in
+// the permuted order p = k1 S + k2 <-> natural k1 + 16 k2 (capi permutes khat)
+template <int LOGL>
+__host__ __device__ constexpr bool fused_fft2() { return fft2_used(LOGL); }
+
+template <int LOGL, bool MULTI, class TW, class Sink>
+__device__ __forceinline__ void fused_unit2(const ChirpZDev& cz, const TW& tw, double2* s, int t,
+                                            bool valid, const double* xb, int j, int m, int ti0,
+                                            int ti1, double2* specb, const Sink& sink) {
+  using F = Fft2<LOGL>;
+  constexpr int L = F::L;
+  const double2* pre = cz.pre + (int64_t)m * cz.width;
+  const int k1 = t / F::TPS;
+  double2* reg = s + k1 * F::PS;
+  double2* spr = specb ? specb + k1 * F::S : nullptr;
+  for (int ti = ti0; ti < ti1; ++ti) {
+    const int64_t to = cz.tin[2 * ti], tn = cz.tin[2 * ti + 1];
+    auto load_x = [&](int e) -> double2 {
+      if (valid && e < tn) {
+        const double xv = __ldg(xb + to + e);
+        const double2 p = __ldg(pre + to + e);
+        return make_double2(xv * p.x, xv * p.y);
+      }
+      return make_double2(0.0, 0.0);
+    };
+    __syncthreads();   // previous readers of s are done
+    fft2_first<LOGL>(s, t, tw, load_x);
+    __syncthreads();
+    const double2* kh = cz.khat + ((int64_t)j * cz.n_in + ti) * L + k1 * F::S;
+    if constexpr (MULTI) {
+      // spectrum product summed over the unit's tiles: running sum in spec
+      // (L2), the last tile writes the total into shared memory
+      const bool first = ti == ti0, last = ti == ti1 - 1;
+      auto store_spec = [&](int e, double2 v) {
+        double2 y = cmul(v, __ldg(kh + e));
+        if (!first && valid) {
+          const double2 a = __ldcg(spr + e);
+          y.x += a.x;
+          y.y += a.y;
+        }
+        if (last)
+          reg[pad16(e)] = y;
+        else if (valid)
+          __stcg(spr + e, y);
+      };
+      fft2_sub<LOGL, -1>(s, t, tw, SmemLoad{reg}, store_spec);
+    } else {
+      // single-tile units: forward sub-FFT, spectrum product, inverse sub-FFT
+      // with the forward's last pass and the inverse's first pass fused in
+      // registers (a separate instantiation from the multi-tile code)
+      auto spec_op = [&](int e, double2 v) -> double2 { return cmul(v, __ldg(kh + e)); };
+      sub_conv<F::LOGS>(reg, t % F::TPS, tw, spec_op);
+    }
+  }
+  if constexpr (MULTI) fft2_sub<LOGL, +1>(s, t, tw, SmemLoad{reg}, SmemStore{reg});
+  __syncthreads();
+  const int64_t so = cz.tout[2 * j], sc = cz.tout[2 * j + 1];
+  const double2* post = cz.post + (int64_t)m * cz.count + so;
+  auto store_out = [&](int e, double2 y) {
+    if (e < sc) {
+      const double2 q = __ldg(post + e);
+      sink(e, fma(q.x, y.x, -q.y * y.y));
+    }
+  };
+  fft2_last_inv<LOGL>(s, t, tw, store_out);
+}
+
+template <int LOGL, bool MULTI, class TW, class Sink>
 __device__ __forceinline__ void fused_unit(const ChirpZDev& cz, const TW& tw, double2* s, int t,
                                            bool valid, const double* xb, int j, int m, int ti0,
                                            int ti1, double2* specb, const Sink& sink) {
+  if constexpr (fused_fft2<LOGL>()) {
+    fused_unit2<LOGL, MULTI>(cz, tw, s, t, valid, xb, j, m, ti0, ti1, specb, sink);
+    return;
+  }
   using Cfg = FusedCfg<LOGL>;
   constexpr int L = Cfg::L;
   const double2* pre = cz.pre + (int64_t)m * cz.width;
@@ -124,7 +195,7 @@ __device__ __forceinline__ void fused_unit(const ChirpZDev& cz, const TW& tw, do
   fft_smem_io<LOGL, +1, SmemLoad, decltype(store_out), Cfg::LEPT>(s, t, tw, SmemLoad{s}, store_out);
 }
 
-template <int LOGL, class TW>
+template <int LOGL, bool MULTI, class TW>
 __device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, double2* s, double* acc,
                                              int t, int grp, const double* __restrict__ x, int64_t ldx,
                                              double* __restrict__ out, int64_t ldo, int64_t batch,
@@ -143,7 +214,7 @@ __device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, 
 #pragma unroll
   for (int i = 0; i < Cfg::EPT; ++i) acc[t + i * TPG] = 0.0;
   auto sink = [&](int e, double v) { acc[e] += v; };
-  for (int m = 0; m < cz.m_count; ++m) fused_unit<LOGL>(cz, tw, s, t, valid, xb, j, m, 0, cz.n_in, specb, sink);
+  for (int m = 0; m < cz.m_count; ++m) fused_unit<LOGL, MULTI>(cz, tw, s, t, valid, xb, j, m, 0, cz.n_in, specb, sink);
   __syncthreads();
   if (!valid) return;
   double* ob = out + b * ldo + cz.q0 + so;
@@ -154,7 +225,7 @@ __device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, 
   }
 }
 
-template <int LOGL, class TW>
+template <int LOGL, bool MULTI, class TW>
 __device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw, double2* s, int t,
                                               int grp, const double* __restrict__ x, int64_t ldx,
                                               int64_t batch, double* __restrict__ part,
@@ -181,13 +252,13 @@ __device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw,
     auto sink = [&](int e, double v) {
       if (valid) slot[e] = v;
     };
-    fused_unit<LOGL>(cz, tw, s, t, valid, xb, j, m, ti0, ti1, specb, sink);
+    fused_unit<LOGL, MULTI>(cz, tw, s, t, valid, xb, j, m, ti0, ti1, specb, sink);
     f += ti1 - ti0;
   }
 }
 
 // grid: direct (groups, n_out) or stream-K (P); see FusedSched.
-template <int LOGL>
+template <int LOGL, bool MULTI>
 __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
     k_chirpz_fused(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
                    int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch,
@@ -203,14 +274,14 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
   if constexpr (Cfg::TW_SMEM) {
     const TwSmem tws = tw_smem_init(reinterpret_cast<double2*>(acc + Cfg::E), tw);
     if (sk.streamk)
-      fused_streamk<LOGL>(cz, tws, s, t, grp, x, ldx, batch, part, spec, sk);
+      fused_streamk<LOGL, MULTI>(cz, tws, s, t, grp, x, ldx, batch, part, spec, sk);
     else
-      fused_direct<LOGL>(cz, tws, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
+      fused_direct<LOGL, MULTI>(cz, tws, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
   } else {
     if (sk.streamk)
-      fused_streamk<LOGL>(cz, tw, s, t, grp, x, ldx, batch, part, spec, sk);
+      fused_streamk<LOGL, MULTI>(cz, tw, s, t, grp, x, ldx, batch, part, spec, sk);
     else
-      fused_direct<LOGL>(cz, tw, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
+      fused_direct<LOGL, MULTI>(cz, tw, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
   }
 }
 
@@ -525,7 +596,7 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
 template <int LOG2>
 struct RowCfg {
   static constexpr int L2 = 1 << LOG2;
-  static constexpr int LEPT = LOG2 == 13 ? 5 : 4;
+  static constexpr int LEPT = (LOG2 == 13 && !fft2_used(LOG2)) ? 5 : 4;   // Fft2: 16 per thread
   static constexpr int EPT = 1 << LEPT;
   static constexpr int E = (L2 >= 4096) ? L2 : 4096;
   static constexpr int NR = E / L2;
@@ -552,6 +623,20 @@ __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
   const double2* kh = cz.khat + k1 * L2;
   double2* s = smem + grp * padded_len(L2);
   auto load_row = [&](int e) -> double2 { return row[e]; };
+  if constexpr (fft2_used(LOG2)) {
+    // two-level FFT: khat rows are in the permuted order (capi)
+    using F = Fft2<LOG2>;
+    fft2_first<LOG2>(s, t, tw, load_row);
+    __syncthreads();
+    double2* reg = s + (t / F::TPS) * F::PS;
+    const double2* khr = kh + (t / F::TPS) * F::S;
+    auto mul_spec = [&](int e, double2 v) -> double2 { return cmul(v, __ldg(khr + e)); };
+    sub_conv<F::LOGS>(reg, t % F::TPS, tw, mul_spec);
+    __syncthreads();
+    auto store_row2 = [&](int e, double2 v) { row[e] = v; };
+    fft2_last_inv<LOG2>(s, t, tw, store_row2);
+    return;
+  }
   fft_smem_io<LOG2, -1, decltype(load_row), SmemStore, Cfg::LEPT>(s, t, tw, load_row, SmemStore{s});
   auto load_spec = [&](int e) -> double2 { return cmul(s[pad16(e)], __ldg(kh + e)); };
   auto store_row = [&](int e, double2 v) { row[e] = v; };
@@ -658,7 +743,8 @@ int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t l
   static_assert(Cfg::NG == (LOGL >= 12 ? 1 : (1 << (12 - LOGL))), "fused_groups out of sync");
   static bool init = false;
   if (!init) {
-    if (int rc = set_smem(k_chirpz_fused<LOGL>, Cfg::SMEM)) return rc;
+    if (int rc = set_smem(k_chirpz_fused<LOGL, false>, Cfg::SMEM)) return rc;
+    if (int rc = set_smem(k_chirpz_fused<LOGL, true>, Cfg::SMEM)) return rc;
     init = true;
   }
   const FusedSched sk = fused_sched(cz, batch);
@@ -668,7 +754,10 @@ int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t l
   if (sk.streamk && !part) return fail(CJT_EINVAL, "chirp-z without partial workspace");
   const int64_t groups = (batch + Cfg::NG - 1) / Cfg::NG;
   dim3 grid = sk.streamk ? dim3((unsigned)sk.P) : dim3((unsigned)groups, (unsigned)cz.n_out);
-  k_chirpz_fused<LOGL><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch, part, spec, sk);
+  if (cz.n_in > 1)
+    k_chirpz_fused<LOGL, true><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch, part, spec, sk);
+  else
+    k_chirpz_fused<LOGL, false><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, out, ldo, batch, part, spec, sk);
   CJT_CUDA_TRY(cudaGetLastError());
   *launches += 1;
   if (sk.streamk) {

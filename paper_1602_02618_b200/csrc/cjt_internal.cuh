@@ -237,7 +237,16 @@ struct SmemStore {
   __device__ __forceinline__ void operator()(int e, double2 v) const { s[pad16(e)] = v; }
 };
 
-template <int LOGL, int DIR, int LEPT, int PASS, class LoadF, class StoreF, class TW>
+// Barrier policy of an FFT's passes: the whole CTA, or only the warp (for
+// sub-FFTs owned by one warp or by a fraction of one)
+struct SyncCTA {
+  static __device__ __forceinline__ void sync() { __syncthreads(); }
+};
+struct SyncWarp {
+  static __device__ __forceinline__ void sync() { __syncwarp(); }
+};
+
+template <int LOGL, int DIR, int LEPT, int PASS, class LoadF, class StoreF, class TW, class SY = SyncCTA>
 __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
                                          const LoadF& first_load, const StoreF& last_store) {
   constexpr int NP = (LOGL + LEPT - 1) / LEPT;
@@ -263,7 +272,7 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
           v[q * R + r] = s[pad16(j + r * STRIDE)];
       }
     }
-    __syncthreads();
+    SY::sync();
 #pragma unroll
     for (int q = 0; q < NBF; ++q) {
       const int j = t + q * TPG;
@@ -293,8 +302,8 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
           s[pad16(base + r * NS)] = v[q * R + r];
       }
     }
-    __syncthreads();
-    fft_pass<LOGL, DIR, LEPT, PASS + 1>(s, t, tw, first_load, last_store);
+    SY::sync();
+    fft_pass<LOGL, DIR, LEPT, PASS + 1, LoadF, StoreF, TW, SY>(s, t, tw, first_load, last_store);
   }
 }
 
@@ -310,6 +319,162 @@ __device__ __forceinline__ void fft_smem_io(double2* s, int t, const TW& tw,
                                             const LoadF& ld, const StoreF& st) {
   static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
   fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, ld, st);
+}
+
+// ---------------------------------------------------------------------------
+// Two-level FFT of length L = 16 S (512 <= L <= 8192, T = S threads per FFT):
+//   fft2_first:    CTA-wide radix-16 DIF pass: thread n2 loads x[n2 + S n1]
+//                  (n1 < 16) through the hook, DFT over n1, twiddle W_L^{n2 k1},
+//                  writes sub-sequence k1 at region k1 (contiguous, padded);
+//   sub-FFTs:      16 independent S-point FFTs over n2, one per region, each
+//                  owned by S/16 consecutive threads (a warp or part of one) and
+//                  synchronised with __syncwarp only;  X[k1 + 16 k2] = region
+//                  k1 position k2 ("permuted" spectrum order);
+//   fft2_last_inv: CTA-wide radix-16 DIT inverse pass from the permuted
+//                  spectrum after the inverse sub-FFTs: thread n2 gathers
+//                  region k1 position n2, twiddle W_L^{-n2 k1}, IDFT over k1,
+//                  value y[n2 + S n1] to the hook.
+// A forward FFT, spectrum product and inverse FFT thus need two CTA barriers
+// instead of two per pass; warps drift apart and overlap shared-memory and
+// FP64 phases.
+#ifndef CJT_FFT2
+#define CJT_FFT2 1
+#endif
+// lengths that run the two-level FFT (fused tiles and multi-pass rows); their
+// spectra (khat) are stored in the permuted order k1 S + k2 <-> k1 + 16 k2
+__host__ __device__ constexpr bool fft2_used(int lg) { return CJT_FFT2 && lg >= 9; }
+
+template <int LOGL>
+struct Fft2 {
+  static constexpr int L = 1 << LOGL;
+  static constexpr int LOGS = LOGL - 4;
+  static constexpr int S = L / 16;
+  static constexpr int PS = padded_len(S);   // region stride
+  static constexpr int TPS = S / 16;         // threads per sub-FFT
+};
+
+template <int LOGL, class LoadF, class TW>
+__device__ __forceinline__ void fft2_first(double2* s, int n2, const TW& tw, const LoadF& ld) {
+  using F = Fft2<LOGL>;
+  double2 v[16];
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) v[n1] = ld(n2 + F::S * n1);
+  dft_reg<16, -1>(v);
+  twiddle_powers<16, -1>(v, tw, n2 << (13 - LOGL));
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) s[k1 * F::PS + pad16(n2)] = v[k1];
+}
+
+template <int LOGL, class StoreF, class TW>
+__device__ __forceinline__ void fft2_last_inv(const double2* s, int n2, const TW& tw, const StoreF& st) {
+  using F = Fft2<LOGL>;
+  double2 v[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) v[k1] = s[k1 * F::PS + pad16(n2)];
+  twiddle_powers<16, +1>(v, tw, n2 << (13 - LOGL));
+  dft_reg<16, +1>(v);
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) st(n2 + F::S * n1, v[n1]);
+}
+
+// One warp-synchronous Stockham pass of radix 2^LR over an N = 2^LOGN region
+// (LNS = log2 of the product of the previous radices), 16 elements per thread.
+template <int LOGN, int DIR, int LR, int LNS, class LoadF, class StoreF, class TW>
+__device__ __forceinline__ void sub_pass(double2* s, int t, const TW& tw, const LoadF& ld,
+                                         const StoreF& st) {
+  constexpr int N = 1 << LOGN, R = 1 << LR, NS = 1 << LNS;
+  constexpr int NBF = 16 / R, STRIDE = N / R, TPG = N / 16;
+  double2 v[16];
+#pragma unroll
+  for (int q = 0; q < NBF; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q * R + r] = ld(t + q * TPG + r * STRIDE);
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < NBF; ++q) {
+    const int j = t + q * TPG;
+    const int k = j & (NS - 1);
+    if constexpr (LNS > 0) twiddle_powers<R, DIR>(&v[q * R], tw, k << (13 - (LNS + LR)));
+    dft_reg<R, DIR>(&v[q * R]);
+    const int base = ((j - k) << LR) + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) st(base + r * NS, v[q * R + r]);
+  }
+  __syncwarp();
+}
+
+// COUNT consecutive passes of radix 2^LR starting at LNS (shared-memory in place)
+template <int LOGN, int DIR, int LR, int LNS, int COUNT, class TW>
+__device__ __forceinline__ void sub_passes(double2* s, int t, const TW& tw) {
+  if constexpr (COUNT > 0) {
+    sub_pass<LOGN, DIR, LR, LNS>(s, t, tw, SmemLoad{s}, SmemStore{s});
+    sub_passes<LOGN, DIR, LR, LNS + LR, COUNT - 1>(s, t, tw);
+  }
+}
+
+// Sub-FFT pass plan for N = 2^LOGN: FULL passes of radix 16, then a remainder
+// radix 2^REM.  The inverse runs the radices in reverse order, so the forward's
+// last pass and the inverse's first pass touch the same elements in the same
+// thread: sub_middle does both in registers around the spectrum operation.
+template <int LOGN>
+struct SubPlan {
+  static constexpr int FULL = (LOGN - 1) / 4;
+  static constexpr int REM = LOGN - 4 * FULL;   // 1..4
+};
+
+// forward last pass (radix 2^REM at LNS = 4 FULL) -> op(e, X_e) at spectrum
+// index e -> inverse first pass (radix 2^REM, no twiddle) -> shared memory
+template <int LOGN, class SpecF, class TW>
+__device__ __forceinline__ void sub_middle(double2* s, int t, const TW& tw, const SpecF& op) {
+  constexpr int LR = SubPlan<LOGN>::REM, LNS = 4 * SubPlan<LOGN>::FULL;
+  constexpr int N = 1 << LOGN, R = 1 << LR, NS = 1 << LNS;
+  constexpr int NBF = 16 / R, TPG = N / 16;
+  static_assert(NS * R == N, "sub_middle: pass plan");
+  double2 v[16];
+#pragma unroll
+  for (int q = 0; q < NBF; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q * R + r] = s[pad16(t + q * TPG + r * NS)];
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < NBF; ++q) {
+    const int j = t + q * TPG;   // j < NS: this butterfly's outputs are j + r NS
+    if constexpr (LNS > 0) twiddle_powers<R, -1>(&v[q * R], tw, j << (13 - (LNS + LR)));
+    dft_reg<R, -1>(&v[q * R]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q * R + r] = op(j + r * NS, v[q * R + r]);
+    dft_reg<R, +1>(&v[q * R]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pad16((j << LR) + r)] = v[q * R + r];
+  }
+  __syncwarp();
+}
+
+// forward sub-FFT with the last pass's outputs sent to st(e, X_e) (natural e)
+template <int LOGN, class StoreF, class TW>
+__device__ __forceinline__ void sub_fft_fwd_to(double2* s, int t, const TW& tw, const StoreF& st) {
+  using SP = SubPlan<LOGN>;
+  sub_passes<LOGN, -1, 4, 0, SP::FULL>(s, t, tw);
+  sub_pass<LOGN, -1, SP::REM, 4 * SP::FULL>(s, t, tw, SmemLoad{s}, st);
+}
+
+// forward sub-FFT, X_e <- op(e, X_e), inverse sub-FFT, natural order in place
+template <int LOGN, class SpecF, class TW>
+__device__ __forceinline__ void sub_conv(double2* s, int t, const TW& tw, const SpecF& op) {
+  using SP = SubPlan<LOGN>;
+  sub_passes<LOGN, -1, 4, 0, SP::FULL>(s, t, tw);
+  sub_middle<LOGN>(s, t, tw, op);
+  sub_passes<LOGN, +1, 4, SP::REM, SP::FULL>(s, t, tw);
+}
+
+// the sub-FFT of region k1 = n2 / TPS, local thread n2 % TPS (warp-synchronous)
+template <int LOGL, int DIR, class LoadF, class StoreF, class TW>
+__device__ __forceinline__ void fft2_sub(double2* s, int n2, const TW& tw, const LoadF& ld,
+                                         const StoreF& st) {
+  using F = Fft2<LOGL>;
+  static_assert(F::TPS >= 1 && F::TPS <= 32, "sub-FFT must fit one warp");
+  fft_pass<F::LOGS, DIR, 4, 0, LoadF, StoreF, TW, SyncWarp>(s + (n2 / F::TPS) * F::PS, n2 % F::TPS, tw,
+                                                           ld, st);
 }
 
 // ---------------------------------------------------------------------------
