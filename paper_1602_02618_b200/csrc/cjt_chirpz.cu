@@ -226,35 +226,56 @@ __device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, 
 }
 
 template <int LOGL, bool MULTI, class TW>
-__device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw, double2* s, int t,
-                                              int grp, const double* __restrict__ x, int64_t ldx,
+__device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw, double2* s, double* acc,
+                                              int t, int grp, const double* __restrict__ x, int64_t ldx,
                                               int64_t batch, double* __restrict__ part,
                                               double2* __restrict__ spec, const FusedSched& sk) {
   using Cfg = FusedCfg<LOGL>;
   constexpr int L = Cfg::L;
+  constexpr int TPG = L / Cfg::EPT;
   const int64_t c = blockIdx.x;
   const int64_t f0 = sk.start(c), f1 = sk.start(c + 1);
-  const int64_t u_first = f0 / cz.n_in;
-  double2* specb = spec + (c * Cfg::NG + grp) * L;
   const int M = cz.m_count;
+  const int64_t gj_first = f0 / cz.n_in / M;
+  double2* specb = spec ? spec + (c * Cfg::NG + grp) * L : nullptr;
+  // the output tile of one (group, j) accumulates over its terms m in shared
+  // memory and is written once per (CTA, (group, j)) segment
+#pragma unroll
+  for (int i = 0; i < Cfg::EPT; ++i) acc[t + i * TPG] = 0.0;
+  auto flush = [&](int64_t gj) {
+    __syncthreads();
+    const int j = (int)(gj % cz.n_out);
+    const int64_t b = gj / cz.n_out * Cfg::NG + grp;
+    const int64_t sc = cz.tout[2 * j + 1];
+    double* slot = part + (((c * sk.S + (gj - gj_first)) * Cfg::NG) + grp) * cz.count_max;
+#pragma unroll
+    for (int i = 0; i < Cfg::EPT; ++i) {
+      const int e = t + i * TPG;
+      if (e < sc && b < batch) slot[e] = acc[e];
+      acc[e] = 0.0;
+    }
+  };
+  int64_t cur = f0 / cz.n_in / M;
   for (int64_t f = f0; f < f1;) {
     const int64_t u = f / cz.n_in;
     const int ti0 = (int)(f % cz.n_in);
     const int ti1 = (int)min((int64_t)cz.n_in, (int64_t)ti0 + (f1 - f));
     const int64_t gj = u / M;
     const int m = (int)(u % M);
+    if (gj != cur) {
+      flush(cur);
+      cur = gj;
+    }
     const int64_t g = gj / cz.n_out;
     const int j = (int)(gj % cz.n_out);
     const int64_t b = g * Cfg::NG + grp;
     const bool valid = b < batch;
     const double* xb = x + (valid ? b : 0) * ldx + cz.p0;
-    double* slot = part + (((c * sk.S + (u - u_first)) * Cfg::NG) + grp) * cz.count_max;
-    auto sink = [&](int e, double v) {
-      if (valid) slot[e] = v;
-    };
+    auto sink = [&](int e, double v) { acc[e] += v; };
     fused_unit<LOGL, MULTI>(cz, tw, s, t, valid, xb, j, m, ti0, ti1, specb, sink);
     f += ti1 - ti0;
   }
+  flush(cur);
 }
 
 // grid: direct (groups, n_out) or stream-K (P); see FusedSched.
@@ -274,46 +295,38 @@ __global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
   if constexpr (Cfg::TW_SMEM) {
     const TwSmem tws = tw_smem_init(reinterpret_cast<double2*>(acc + Cfg::E), tw);
     if (sk.streamk)
-      fused_streamk<LOGL, MULTI>(cz, tws, s, t, grp, x, ldx, batch, part, spec, sk);
+      fused_streamk<LOGL, MULTI>(cz, tws, s, acc, t, grp, x, ldx, batch, part, spec, sk);
     else
       fused_direct<LOGL, MULTI>(cz, tws, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
   } else {
     if (sk.streamk)
-      fused_streamk<LOGL, MULTI>(cz, tw, s, t, grp, x, ldx, batch, part, spec, sk);
+      fused_streamk<LOGL, MULTI>(cz, tw, s, acc, t, grp, x, ldx, batch, part, spec, sk);
     else
       fused_direct<LOGL, MULTI>(cz, tw, s, acc, t, grp, x, ldx, out, ldo, batch, spec);
   }
 }
 
-// stream-K combine: out[b][q0 + so_j + e] (+)= sum over m, then over the
-// CTAs that cut unit (grp, j, m), of the partial slots (fixed order).
-// grid (e chunks, n_out, batch); slot ranges computed once per block.
-constexpr int COMBINE_MMAX = 64;
+// stream-K combine: out[b][q0 + so_j + e] (+)= sum over the CTAs whose
+// ranges cover (group, j) of their slot for it (fixed order).
+// grid (e chunks, n_out, batch).
 __global__ void __launch_bounds__(256) k_chirpz_combine_sk(ChirpZDev cz, const double* __restrict__ part,
                                                            FusedSched sk, int ng, double* __restrict__ out,
                                                            int64_t ldo) {
-  __shared__ int64_t ca[COMBINE_MMAX], cb[COMBINE_MMAX], ka[COMBINE_MMAX];
   const int j = blockIdx.y;
   const int64_t b = blockIdx.z;
   const int64_t g = b / ng, gi = b % ng;
-  const int M = cz.m_count;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    const int64_t u = (g * cz.n_out + j) * M + m;
-    ca[m] = sk.cta_of(u * cz.n_in);
-    cb[m] = sk.cta_of(u * cz.n_in + cz.n_in - 1);
-    ka[m] = u - sk.start(ca[m]) / cz.n_in;
-  }
-  __syncthreads();
   const int64_t so = __ldg(cz.tout + 2 * j), sc = __ldg(cz.tout + 2 * j + 1);
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= sc) return;
+  const int64_t gj = g * cz.n_out + j;
+  const int64_t per_gj = (int64_t)cz.m_count * cz.n_in;   // forward FFTs of one (group, j)
+  const int64_t ca = sk.cta_of(gj * per_gj), cb = sk.cta_of(gj * per_gj + per_gj - 1);
   const int64_t stride = (int64_t)ng * cz.count_max;
   const double* pe = part + gi * cz.count_max + e;
   double v = 0.0;
-  for (int m = 0; m < M; ++m) {
-    // the first CTA holds the unit at slot k_a; later ones start inside it (slot 0)
-    v += pe[(ca[m] * sk.S + ka[m]) * stride];
-    for (int64_t c = ca[m] + 1; c <= cb[m]; ++c) v += pe[c * sk.S * stride];
+  for (int64_t c = ca; c <= cb; ++c) {
+    const int64_t k = gj - sk.start(c) / cz.n_in / cz.m_count;
+    v += pe[(c * sk.S + k) * stride];
   }
   double* o = out + b * ldo + cz.q0 + so + e;
   *o = cz.accumulate ? *o + v : v;
@@ -722,16 +735,17 @@ FusedSched fused_sched(const ChirpZDev& cz, int64_t batch) {
   const int64_t per = (sk.F + P - 1) / P;
   const int64_t segs = per / cz.n_in + 2;   // units a CTA range touches (upper bound)
   const int64_t t_sk = per + std::min(segs, per);
+  const int64_t gsegs = segs / cz.m_count + 2;   // (group, j) segments a CTA range touches
   // $CJT_FUSED_SCHED (experiments): 1 forces direct, 2 stream-K
   static const int force = [] {
     const char* e = getenv("CJT_FUSED_SCHED");
     return e ? atoi(e) : 0;
   }();
   const bool pick = force ? force == 2 : 10 * t_sk < 9 * t_direct;
-  if (pick && cz.m_count <= COMBINE_MMAX && batch <= 65535) {
+  if (pick && batch <= 65535) {
     sk.streamk = 1;
     sk.P = P;
-    sk.S = segs;
+    sk.S = gsegs;
   }
   return sk;
 }
@@ -748,8 +762,7 @@ int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t l
     init = true;
   }
   const FusedSched sk = fused_sched(cz, batch);
-  if (sk.streamk && (cz.m_count > COMBINE_MMAX || batch > 65535))
-    return fail(CJT_EINVAL, "chirp-z stream-K schedule out of range");
+  if (sk.streamk && batch > 65535) return fail(CJT_EINVAL, "chirp-z stream-K schedule out of range");
   if (cz.n_in > 1 && !spec) return fail(CJT_EINVAL, "chirp-z without spectrum workspace");
   if (sk.streamk && !part) return fail(CJT_EINVAL, "chirp-z without partial workspace");
   const int64_t groups = (batch + Cfg::NG - 1) / Cfg::NG;

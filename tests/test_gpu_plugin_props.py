@@ -84,9 +84,12 @@ def test_reexecution_bit_identical(cuda):
     f2 = cj.forward_batched(fp, c)
     i2 = cj.inverse_batched(ip, f2)
     assert torch.equal(f1, f2) and torch.equal(i1, i2)
-    # batch composition does not change any vector's result (no cross-vector reduction)
+    # batch composition changes a vector's result by rounding only: there is no
+    # cross-vector reduction, but the stream-K chirp-z schedule (and with it
+    # the order of the sums over terms / input tiles) depends on the batch
     f3 = cj.forward_batched(fp, c[3:4].contiguous())
-    assert torch.equal(f3[0], f1[3])
+    ref = f1[3].cpu().numpy()
+    assert np.max(np.abs(f3[0].cpu().numpy() - ref)) <= 1e-15 * np.sum(np.abs(c[3].cpu().numpy()))
 
 
 def test_config3_full_batch_slice_vs_golden_and_roundtrip(cuda):
