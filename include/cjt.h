@@ -152,6 +152,11 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
 int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n,
                     double* x, double* xm);
 
+/* Plan-time host helper: Jacobi moments mu_0..mu_g by the reference's
+ * three-term recurrence (quadrature.py:35-53), same operation order, given
+ * mu_0 (the Gamma-function ratio, computed by the caller). */
+int cjt_host_moments(double alpha, double beta, double mu0, int64_t g, double* mu);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,10 +85,11 @@ def lib():
     L.cjt_clenshaw_points.argtypes = [_p] * 8 + [_i64, _p, _p, _p, _p, _i64]
     L.cjt_transpose_accumulate.argtypes = [_p] * 12 + [_i64, _i64, _i64]
     L.cjt_host_angles.argtypes = [_p, _p, _i64, _p, _p]
+    L.cjt_host_moments.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, _i64, _p]
     for name in ("cjt_device_count", "cjt_plan_create", "cjt_plan_destroy", "cjt_plan_reserve",
                  "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host", "cjt_clenshaw_points",
-                 "cjt_transpose_accumulate", "cjt_host_angles", "cjt_execute_stage",
-                 "cjt_probe_fp64_peak"):
+                 "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
+                 "cjt_execute_stage", "cjt_probe_fp64_peak"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -97,8 +98,8 @@ def lib():
 EXPORTED_SYMBOLS = (
     "cjt_version", "cjt_last_error", "cjt_device_count", "cjt_plan_create", "cjt_plan_destroy",
     "cjt_plan_reserve", "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host",
-    "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_execute_stage",
-    "cjt_probe_fp64_peak",
+    "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
+    "cjt_execute_stage", "cjt_probe_fp64_peak",
 )
 STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7
 

@@ -913,6 +913,21 @@ int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, in
   return CJT_OK;
 }
 
+int cjt_host_moments(double alpha, double beta, double mu0, int64_t g, double* mu) {
+  if (g < 0 || !mu) return fail(CJT_EINVAL, "bad argument");
+  // host code is compiled with -ffp-contract=off: every operation rounds as
+  // in the reference's Python loop
+  const double s = alpha + beta;
+  mu[0] = mu0;
+  if (g >= 1) mu[1] = (beta - alpha) / (s + 2.0) * mu0;
+  const double two_d = 2.0 * (alpha - beta);
+  for (int64_t k = 1; k < g; ++k) {
+    const double kd = (double)k;
+    mu[k + 1] = -(two_d * mu[k] + (s - kd + 2.0) * mu[k - 1]) / (s + kd + 2.0);
+  }
+  return CJT_OK;
+}
+
 int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n, double* x, double* xm) {
   if (n < 0 || (n > 0 && (!thetas || !regions || !x || !xm))) return fail(CJT_EINVAL, "null argument");
   for (int64_t i = 0; i < n; ++i) {

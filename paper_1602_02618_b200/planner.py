@@ -41,6 +41,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import functools
+
 import numpy as np
 import scipy.fft
 
@@ -450,12 +452,11 @@ def moments(p: JacobiParameters, g: int) -> np.ndarray:
     a, b = p.alpha, p.beta
     s = a + b
     mu = np.empty(g + 1)
-    mu[0] = 2.0 ** (s + 1.0) * math.gamma(a + 1.0) * math.gamma(b + 1.0) / math.gamma(s + 2.0)
-    if g >= 1:
-        mu[1] = (b - a) / (s + 2.0) * mu[0]
-    two_d = 2.0 * (a - b)
-    for k in range(1, g):
-        mu[k + 1] = -(two_d * mu[k] + (s - k + 2.0) * mu[k - 1]) / (s + k + 2.0)
+    mu0 = 2.0 ** (s + 1.0) * math.gamma(a + 1.0) * math.gamma(b + 1.0) / math.gamma(s + 2.0)
+    # the serial recurrence (quadrature.py:35-53) runs in the native library,
+    # same operation order and rounding as the reference's loop
+    from . import _native as nat
+    nat.check(nat.lib().cjt_host_moments(a, b, mu0, g, mu.ctypes.data), "moments")
     return mu
 
 
@@ -485,12 +486,27 @@ def cc_weights(p: JacobiParameters, g: int, mu: np.ndarray) -> np.ndarray:
 _PI_LD = np.longdouble("3.14159265358979323846264338327950288419716939937510")
 
 
+_PHASE_B = 2048
+
+
+@functools.lru_cache(maxsize=32)
+def _phase_tables(den: int):
+    """exp(2 pi i a B / den) and exp(2 pi i b / den), b < B, in 80-bit extended."""
+    def tab(idx):
+        ang = (2 * _PI_LD) * idx.astype(np.longdouble) / np.longdouble(den)
+        return np.cos(ang) + np.clongdouble(1j) * np.sin(ang)
+    hi = tab(np.arange(den // _PHASE_B + 1, dtype=np.int64) * _PHASE_B)
+    lo = tab(np.arange(_PHASE_B, dtype=np.int64))
+    return hi, lo
+
+
 def unit_phase(num, den: int) -> np.ndarray:
-    """exp(2 pi i num/den) for integer num, rounded from 80-bit extended."""
+    """exp(2 pi i num/den) for integer num: num reduced exactly mod den, the
+    phase as the 80-bit product of two tabulated 80-bit phases, rounded to
+    double (|error| <= ~0.5 ulp + 2^-63)."""
     r = np.mod(np.asarray(num, dtype=np.int64), den)
-    r = np.where(2 * r > den, r - den, r).astype(np.longdouble)
-    ang = (2 * _PI_LD) * r / np.longdouble(den)
-    return np.cos(ang).astype(np.float64) + 1j * np.sin(ang).astype(np.float64)
+    hi, lo = _phase_tables(int(den))
+    return (hi[r // _PHASE_B] * lo[r % _PHASE_B]).astype(np.complex128)
 
 
 def chirp(k, g: int) -> np.ndarray:
@@ -638,6 +654,18 @@ class HostPlan:
     scalings: np.ndarray | None = None
 
 
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures as cf
+        import os
+        _POOL = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _POOL
+
+
 def build(direction: str, p: JacobiParameters, n: int,
           m_terms: int = DEFAULT_M, eps: float = DEFAULT_EPS) -> HostPlan:
     """Plan one direction (engine.py:96-130) and lay out its device work."""
@@ -666,21 +694,23 @@ def build(direction: str, p: JacobiParameters, n: int,
         v[:, 0] = v[:, -1] = 0.0
         ccols = cnm_table(p, g, m_terms)
         w_uv = u - 1j * v
+        jobs = []
         for (lo, hi), blk in zip(layout.column_strips(), layout.blocks):
             rows = slice(blk.i1, blk.i2 + 1)
             if direction == "forward":
                 # values[rows] += u_m DCT(C_m c)[rows] + v_m DST(C_m c)[rows]
-                hp.blocks.append(chirpz(
-                    g, lo, hi - lo + 1, blk.i1, blk.i2 - blk.i1 + 1,
-                    ccols[lo:hi + 1, :].T, w_uv[:, rows], accumulate=True))
+                jobs.append((g, lo, hi - lo + 1, blk.i1, blk.i2 - blk.i1 + 1,
+                             ccols[lo:hi + 1, :].T, w_uv[:, rows], True))
             else:
                 # out[strip] += C_m (DCT(u_m wv) + DST(v_m wv)); degrees > N dropped
                 top = min(hi, n)
                 if lo > top:
                     continue
-                hp.blocks.append(chirpz(
-                    g, blk.i1, blk.i2 - blk.i1 + 1, lo, top - lo + 1,
-                    w_uv[:, rows], ccols[lo:top + 1, :].T, accumulate=True))
+                jobs.append((g, blk.i1, blk.i2 - blk.i1 + 1, lo, top - lo + 1,
+                             w_uv[:, rows], ccols[lo:top + 1, :].T, True))
+        # blocks are independent: their chirp / spectrum tables are built
+        # concurrently (NumPy releases the GIL in the large array kernels)
+        hp.blocks = list(_pool().map(lambda a: chirpz(*a), jobs))
 
     if direction == "forward":
         # chebyshev_analysis (trig.py:53-63): scipy DCT-I of 0.5 v, i.e. the
