@@ -152,6 +152,20 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
 int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n,
                     double* x, double* xm);
 
+/* Integer parameter shifts of Jacobi coefficient vectors (engine.py:232-292),
+ * device pointers, in/out: [batch][n+1] float64 (may not alias), (alpha,
+ * beta) = the SOURCE parameters; the result is in the shifted basis
+ * (beta+1, beta-1, alpha+1, alpha-1).  Increments are bit-identical to the
+ * reference; decrements are its back-substitution run as a chunked
+ * first-order recurrence (rounding differs at chunk boundaries only).
+ * Target parameters must stay > -1 (CJT_EINVAL otherwise). */
+#define CJT_SHIFT_INC_BETA 0
+#define CJT_SHIFT_DEC_BETA 1
+#define CJT_SHIFT_INC_ALPHA 2
+#define CJT_SHIFT_DEC_ALPHA 3
+int cjt_jacobi_shift(int32_t op, double alpha, double beta, const double* in, double* out,
+                     int64_t n, int64_t batch, void* stream);
+
 /* Plan-time host helper: Jacobi moments mu_0..mu_g by the reference's
  * three-term recurrence (quadrature.py:35-53), same operation order, given
  * mu_0 (the Gamma-function ratio, computed by the caller). */

@@ -2,7 +2,7 @@
 
 Drop-in for the forward / inverse transform path of the reference package
 ``chebjac`` (plan / forward / inverse on coefficient vectors and (alpha, beta)),
-plus batched variants.  Planning runs on the host (bit-compatible with the
+its integer parameter shifts and jacobi_to_jacobi, plus batched variants.  Planning runs on the host (bit-compatible with the
 reference planner); execution runs in hand-written sm_100a kernels behind the
 C ABI of include/cjt.h.  See DESIGN.md.
 """
@@ -24,6 +24,19 @@ from .engine import (
     plan,
 )
 from .planner import DEFAULT_EPS, DEFAULT_M, JacobiParameters, ParameterRangeError
+from .shifts import (
+    decrement_alpha,
+    decrement_beta,
+    from_core,
+    from_core_batched,
+    increment_alpha,
+    increment_beta,
+    jacobi_to_jacobi,
+    jacobi_to_jacobi_batched,
+    shift_batched,
+    to_core,
+    to_core_batched,
+)
 
 __version__ = "0.1.0"
 
@@ -32,4 +45,7 @@ __all__ = [
     "JacobiParameters", "ParameterRangeError", "TransformPlan", "available_backends",
     "chebyshev", "forward", "forward_batched", "inverse", "inverse_batched", "jacobi",
     "kernel_backend", "pipeline", "plan", "register_with", "set_kernel_backend",
+    "decrement_alpha", "decrement_beta", "from_core", "from_core_batched", "increment_alpha",
+    "increment_beta", "jacobi_to_jacobi", "jacobi_to_jacobi_batched", "shift_batched", "to_core",
+    "to_core_batched",
 ]

@@ -913,6 +913,19 @@ int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, in
   return CJT_OK;
 }
 
+int cjt_jacobi_shift(int32_t op, double alpha, double beta, const double* in, double* out,
+                     int64_t n, int64_t batch, void* stream) {
+  if (n < 0 || batch < 0 || (batch > 0 && (!in || !out))) return fail(CJT_EINVAL, "bad argument");
+  if (batch > 65535 && (op == CJT_SHIFT_DEC_BETA || op == CJT_SHIFT_DEC_ALPHA))
+    return fail(CJT_EINVAL, "decrement batch must be <= 65535 per call");
+  const double ta = op == CJT_SHIFT_INC_ALPHA ? alpha + 1.0 : op == CJT_SHIFT_DEC_ALPHA ? alpha - 1.0 : alpha;
+  const double tb = op == CJT_SHIFT_INC_BETA ? beta + 1.0 : op == CJT_SHIFT_DEC_BETA ? beta - 1.0 : beta;
+  if (!(alpha > -1.0 && beta > -1.0 && ta > -1.0 && tb > -1.0))
+    return fail(CJT_EINVAL, "inadmissible shift target: parameters must stay > -1");
+  if (in == out && batch > 0) return fail(CJT_EINVAL, "in and out must not alias");
+  return launch_shift(op, alpha, beta, in, out, n, batch, (cudaStream_t)stream);
+}
+
 int cjt_host_moments(double alpha, double beta, double mu0, int64_t g, double* mu) {
   if (g < 0 || !mu) return fail(CJT_EINVAL, "bad argument");
   // host code is compiled with -ffp-contract=off: every operation rounds as

@@ -550,6 +550,9 @@ inline int pick_vt(int64_t batch) {
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
                   double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
                   double2* spec, cudaStream_t st, int* launches);
+// integer parameter shifts (cjt_shift.cu); op = CJT_SHIFT_*
+int launch_shift(int op, double alpha, double beta, const double* in, double* out, int64_t n,
+                 int64_t batch, cudaStream_t st);
 // workspace of one chirp-z at this batch: partial outputs (doubles) and
 // spectrum sums (complex elements)
 void chirpz_workspace(const ChirpZDev& cz, int64_t batch, int64_t* part_elems, int64_t* spec_elems);
