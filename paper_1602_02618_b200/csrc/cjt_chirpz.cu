@@ -562,16 +562,7 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
 #pragma unroll
   for (int r = 0; r < L1; ++r) acc[r] = 0.0;
   // per term: the column and the output diagonal are loaded together (one
-  // latency per term).  Twiddles W_L^{-n2 k} = conj(W^{4 n2 (k >> 2)} W^{n2 (k & 3)})
-  // from six values kept in registers (one product per element)
-  double2 w1[4], w4[4];
-  w1[0] = w4[0] = make_double2(1.0, 0.0);
-  w1[1] = twiddle_L(cz, n2);
-  w4[1] = twiddle_L(cz, 4 * n2);
-  w1[2] = cmul(w1[1], w1[1]);
-  w1[3] = cmul(w1[2], w1[1]);
-  w4[2] = cmul(w4[1], w4[1]);
-  w4[3] = cmul(w4[2], w4[1]);
+  // latency per term); the twiddle W_L^{-n2 k1} was applied by the row pass
   const double2* bcol = buf + b * cz.m_count * L + n2;
   for (int m = 0; m < cz.m_count; ++m) {
     const double2* post = cz.post + (int64_t)m * cz.count;
@@ -582,17 +573,6 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
     for (int r = 0; r < L1; ++r) {
       const int64_t q = r * L2 + n2;
       pq[r] = q < cz.count ? __ldg(post + q) : make_double2(0.0, 0.0);
-    }
-    // keep the six base twiddles opaque per iteration: otherwise the compiler
-    // hoists all L1 products out of the m loop (32 more live registers)
-#pragma unroll
-    for (int i = 1; i < 4; ++i)
-      asm volatile("" : "+d"(w1[i].x), "+d"(w1[i].y), "+d"(w4[i].x), "+d"(w4[i].y));
-#pragma unroll
-    for (int k = 1; k < L1; ++k) {
-      double2 w = (k & 3) == 0 ? w4[(k >> 2) & 3] : ((k >> 2) & 3) == 0 ? w1[k & 3] : cmul(w4[(k >> 2) & 3], w1[k & 3]);
-      if (k >= 16) w = cmul(w, twiddle_L(cz, 16 * n2 * (k >> 4)));
-      v[k] = cmul(v[k], make_double2(w.x, -w.y));
     }
     dft_reg<L1, +1>(v);
 #pragma unroll
@@ -646,8 +626,22 @@ __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
     auto mul_spec = [&](int e, double2 v) -> double2 { return cmul(v, __ldg(khr + e)); };
     sub_conv<F::LOGS>(reg, t % F::TPS, tw, mul_spec);
     __syncthreads();
-    auto store_row2 = [&](int e, double2 v) { row[e] = v; };
-    fft2_last_inv<LOG2>(s, t, tw, store_row2);
+    if (cz.log1 <= 5) {
+      // the four-step inverse twiddle W_L^{-k1 e} of the register column pass
+      // is applied here: this thread stores e = t + S n1 for n1 = 0, 1, ...,
+      // so W^{-k1 t} (W^{-k1 S})^{n1} is a running product from two lookups
+      double2 w = twiddle_L(cz, k1 * t), ws = twiddle_L(cz, k1 * F::S);
+      w.y = -w.y;
+      ws.y = -ws.y;
+      auto store_tw = [&](int e, double2 v) {
+        row[e] = cmul(v, w);
+        w = cmul(w, ws);
+      };
+      fft2_last_inv<LOG2>(s, t, tw, store_tw);
+    } else {
+      auto store_row2 = [&](int e, double2 v) { row[e] = v; };
+      fft2_last_inv<LOG2>(s, t, tw, store_row2);
+    }
     return;
   }
   fft_smem_io<LOG2, -1, decltype(load_row), SmemStore, Cfg::LEPT>(s, t, tw, load_row, SmemStore{s});
@@ -919,6 +913,8 @@ int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, i
   }
   *launches += 3;
   int rc = CJT_OK;
+  // register column passes rely on the row pass applying the inverse twiddle
+  if (cz.log1 <= 5 && !fft2_used(cz.log2)) return fail(CJT_EINVAL, "multi-pass split unsupported");
   switch (cz.log1) {
 #define CJT_COLF(K) case K: rc = run_cols_fwd<K>(cz, tw8192, x, ldx, scratch, batch, st); break;
     CJT_COLF(4) CJT_COLF(5) CJT_COLF(6) CJT_COLF(7) CJT_COLF(8) CJT_COLF(9) CJT_COLF(10) CJT_COLF(11)
