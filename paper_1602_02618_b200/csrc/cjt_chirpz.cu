@@ -475,7 +475,8 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
       smem[c * CS + pad16(n1)] = v;
     }
     __syncthreads();
-    fft_smem<LOG1, -1>(smem + grp * CS, t, tw);
+    fft_smem<LOG1, -1, 4, FftSync<LOG1, 4>>(smem + grp * CS, t, tw);
+    __syncthreads();   // the transposed store reads other warps' columns
     double2* bm = buf + (b * cz.m_count + m) * L;
     // this thread's column n2 is fixed and k1 = k1_0 + i T/NC: twiddles
     // W_L^{n2 k1} by a running product from two table values
@@ -683,7 +684,8 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
       }
     }
     __syncthreads();
-    fft_smem<LOG1, +1>(smem + grp * CS, t, tw);
+    fft_smem<LOG1, +1, 4, FftSync<LOG1, 4>>(smem + grp * CS, t, tw);
+    __syncthreads();   // the transposed store reads other warps' columns
     const double2* post = cz.post + (int64_t)m * cz.count;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

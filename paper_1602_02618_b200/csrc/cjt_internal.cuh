@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/cjt.h"
@@ -307,11 +308,14 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
   }
 }
 
-template <int LOGL, int DIR, int LEPT = 4, class TW>
+template <int LOGL, int DIR, int LEPT = 4, class SY = SyncCTA, class TW>
 __device__ __forceinline__ void fft_smem(double2* s, int t, const TW& tw) {
   static_assert(LOGL >= LEPT && LOGL <= 13, "smem FFT length out of range");
-  fft_pass<LOGL, DIR, LEPT, 0>(s, t, tw, SmemLoad{s}, SmemStore{s});
+  fft_pass<LOGL, DIR, LEPT, 0, SmemLoad, SmemStore, TW, SY>(s, t, tw, SmemLoad{s}, SmemStore{s});
 }
+// FFTs whose L / 2^LEPT threads sit inside one warp synchronise the warp only
+template <int LOGL, int LEPT>
+using FftSync = std::conditional_t<(LOGL - LEPT <= 5), SyncWarp, SyncCTA>;
 
 // FFT with a custom first-pass source and last-pass sink (see SmemLoad/SmemStore)
 template <int LOGL, int DIR, class LoadF, class StoreF, int LEPT = 4, class TW>
