@@ -261,13 +261,17 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
   }
   if (lg >= 14 && !cluster) {
-    // longest on-chip rows (8192, radix-32 passes) and short columns: wide,
+    // on-chip rows (two-level FFT) and short columns: wide,
     // coalesced column tiles (E / L1 columns) in passes 1 and 3
-    static const int l2max = [] {   // $CJT_MP_L2MAX (experiments): longest on-chip row
+    // rows: 8192 points (1 CTA/SM) while the columns stay short (<= 16
+    // points, register passes); from 2^20 on, 4096-point rows at 2 CTAs/SM
+    // overlap their HBM and FFT phases and win despite longer columns
+    // (config-4 launch lists).  $CJT_MP_L2MAX (experiments) caps the row length.
+    static const int l2max = [] {
       const char* e = getenv("CJT_MP_L2MAX");
       return e ? std::max(10, std::min(13, atoi(e))) : 13;
     }();
-    const int l2 = std::min(l2max, lg - 4);
+    const int l2 = std::min({l2max, lg - 4, lg >= 20 ? 12 : 13});
     const int l1 = lg - l2;
     cz.log1 = l1;
     cz.log2 = l2;
