@@ -552,16 +552,21 @@ class ChirpZ:
 FUSED_MAX = 8192        # largest Bluestein length kept entirely in one CTA's shared memory
 
 
-def _cost_per_point(length: int) -> float:
-    """Measured B200 cost (ps per point per term per vector, per forward +
-    inverse FFT pair; config-2 launch lists, profiles/) of one Bluestein
-    convolution of this length: on-chip fused tiles (stream-K scheduled) vs the
-    multi-pass (HBM round-trip) path."""
-    if length <= 4096:
-        return 20.7
+# Measured B200 costs (ps per point per term per vector; config-2 launch
+# lists, profiles/): an on-chip tile costs a forward FFT per input tile (with
+# the fused loads and the spectrum sum) plus an inverse FFT per output tile;
+# tiles up to 4096 points run 2 CTAs/SM, 8192-point tiles one.  An untiled
+# multi-pass Bluestein (HBM round trips) costs _MULTIPASS per point: 18.5 ps
+# with register column passes (L <= 2^17), ~29 ps with shared-memory columns
+# (config-4 launch lists).
+_TILE_COST = {4096: (9.7, 6.5), 8192: (10.9, 7.1)}   # (forward, inverse)
+
+
+def _cost(length: int, n_in: int, n_out: int) -> float:
     if length <= FUSED_MAX:
-        return 22.0
-    return 32.5
+        fwd, inv = _TILE_COST[max(4096, length)]
+        return n_out * length * (fwd * n_in + inv)
+    return length * (18.5 if length <= 1 << 17 else 29.0)
 
 
 def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
@@ -586,7 +591,7 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     """Choose (length, n_in, n_out) for a width x count chirp-z: one untiled
     power-of-two Bluestein, or a grid of on-chip tiles, by measured cost."""
     whole = _next_pow2(width + count - 1)
-    best = (whole * _cost_per_point(whole), whole, 1, 1)
+    best = (_cost(whole, 1, 1), whole, 1, 1)
     lc = 1024
     while lc <= fused_max:
         n_min = -(-width // (lc - 1))
@@ -597,7 +602,7 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
                 continue
             # one forward FFT per input tile and one inverse FFT per output
             # tile (input tiles are summed in the frequency domain)
-            cost = n_out * (n_in + 1) * 0.5 * lc * _cost_per_point(lc)
+            cost = _cost(lc, n_in, n_out)
             if cost < best[0]:
                 best = (cost, lc, n_in, n_out)
         lc *= 2
