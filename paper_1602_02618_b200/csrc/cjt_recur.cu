@@ -119,7 +119,9 @@ __device__ __forceinline__ const double* table_row(const RecTablesDev& t, int r)
 }
 struct TabWin {
   const double* t;   // [REC_WIN_ROWS][span]
-  int span;
+  int span;          // row stride
+  int pshift;        // entry nl at nl + (nl >> pshift): 5 pads one slot per 32 degrees
+  __device__ __forceinline__ double at(int r, int nl) const { return t[r * span + nl + (nl >> pshift)]; }
 };
 // degree n_lo + nl -> n_lo + nl + 1 with window tables (rec_step_fast arithmetic)
 __device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w, int nl,
@@ -128,14 +130,14 @@ __device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w
   s0 = s0 * 0.5 + xx; s1 = s0; return;
 #endif
   if (reg == 0) {
-    const double a = w.t[nl], bb = w.t[w.span + nl], c = w.t[2 * w.span + nl];
+    const double a = w.at(0, nl), bb = w.at(1, nl), c = w.at(2, nl);
     const double pn = fma(fma(a, xx, bb), s1, -(c * s0));
     s0 = s1;
     s1 = pn;
   } else {
     const int o = reg > 0 ? 0 : 1;
-    const double rf = w.t[(3 + o) * w.span + nl];
-    const double ap = w.t[(5 + o) * w.span + nl], cp = w.t[(7 + o) * w.span + nl];
+    const double rf = w.at(3 + o, nl);
+    const double ap = w.at(5 + o, nl), cp = w.at(7 + o, nl);
     const double d = fma(ap * xx, s0, cp * s1);
     s0 = fma(rf, d, rf * s0);
     s1 = d;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       }
       if (sidx + 1 < nstages) stage_tables(tb ^ 1, n0 + FWD_KS);
       cp_async_commit();
-      const TabWin w{Ts[tb], FWD_KS};
+      const TabWin w{Ts[tb], FWD_KS, 31};
 #pragma unroll 8
       for (int k = 0; k < FWD_KS; ++k) {
         const int64_t n = n0 + k;
@@ -391,6 +393,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
   constexpr int WS = INV_RT + 4;
   constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
+  // window row stride with one pad slot per 32 degrees: the four producer
+  // chunks of a warp (degrees 32 q + k) then read four different banks
+  constexpr int SPANP = SPAN + SPAN / 32;
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
@@ -405,14 +410,15 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     const int grow = p >> 2, gq = p & 3;
     for (int idx = p; idx < REC_WIN_ROWS * SPAN; idx += W::NP) {
       const int r = idx / SPAN, k = idx % SPAN;
+      const int slot = r * SPANP + k + (k >> 5);
       const bool ok = it.n0 + k < tab.n_tab;
       const double* src = table_row(tab, r);
-      cp_async8(&Tw[idx], ok ? src + it.n0 + k : src, ok);
+      cp_async8(&Tw[slot], ok ? src + it.n0 + k : src, ok);
     }
     cp_async_commit();
     cp_async_wait_all();
     named_sync(BAR_PROD, W::NP);
-    const TabWin win{Tw, SPAN};
+    const TabWin win{Tw, SPANP, 5};
     const GenState* gbase = gen + (int64_t)it.t_begin * 128 + p;
     GenState nxt = gbase[0];
     const int nl0 = CK * gq;
@@ -794,7 +800,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + REC_WIN_ROWS * INV_DT);         \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + INV_DT / 32));         \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
