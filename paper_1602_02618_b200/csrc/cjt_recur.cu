@@ -117,30 +117,41 @@ __device__ __forceinline__ const double* table_row(const RecTablesDev& t, int r)
     default: return t.Cm;
   }
 }
-struct TabWin {
-  const double* t;   // [REC_WIN_ROWS][span]
-  int span;          // row stride
-  int pshift;        // entry nl at nl + (nl >> pshift): 5 pads one slot per 32 degrees
-  __device__ __forceinline__ double at(int r, int nl) const { return t[r * span + nl + (nl >> pshift)]; }
-};
-// degree n_lo + nl -> n_lo + nl + 1 with window tables (rec_step_fast arithmetic)
-__device__ __forceinline__ void rec_step_win(int reg, double xx, const TabWin& w, int nl,
-                                             double& s0, double& s1) {
-#ifdef CJT_FAKE_GEN
-  s0 = s0 * 0.5 + xx; s1 = s0; return;
-#endif
+// K consecutive degrees of one recurrence chain from a shared-memory table
+// window (rows A, B, C, rf+, rf-, A/rf+, A/rf-, C/rf+, C/rf- at stride
+// STRIDE, entry k of this chain at tb[r STRIDE + k]): st(k, P_k) for
+// k < K (0 from degree nval on), advancing the state while k + 1 < nval
+// (nval = cut - first degree, clamped to [0, K + 1]: K + 1 hands the state on
+// to the next stage).
+// The region branch is taken once per call and every table read has a
+// compile-time offset: the loop is issue-bound, not latency-bound.
+template <int K, int STRIDE, class Store>
+__device__ __forceinline__ void gen_chain(int reg, double xx, const double* tb, int nval, double& s0,
+                                          double& s1, const Store& st) {
   if (reg == 0) {
-    const double a = w.at(0, nl), bb = w.at(1, nl), c = w.at(2, nl);
-    const double pn = fma(fma(a, xx, bb), s1, -(c * s0));
-    s0 = s1;
-    s1 = pn;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      st(k, k < nval ? s1 : 0.0);
+      if (k + 1 < nval) {
+        const double pn = fma(fma(tb[k], xx, tb[STRIDE + k]), s1, -(tb[2 * STRIDE + k] * s0));
+        s0 = s1;
+        s1 = pn;
+      }
+    }
   } else {
     const int o = reg > 0 ? 0 : 1;
-    const double rf = w.at(3 + o, nl);
-    const double ap = w.at(5 + o, nl), cp = w.at(7 + o, nl);
-    const double d = fma(ap * xx, s0, cp * s1);
-    s0 = fma(rf, d, rf * s0);
-    s1 = d;
+    const double* rf = tb + (3 + o) * STRIDE;
+    const double* ap = tb + (5 + o) * STRIDE;
+    const double* cp = tb + (7 + o) * STRIDE;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      st(k, k < nval ? s0 : 0.0);
+      if (k + 1 < nval) {
+        const double d = fma(ap[k] * xx, s0, cp[k] * s1);
+        s0 = fma(rf[k], d, rf[k] * s0);
+        s1 = d;
+      }
+    }
   }
 }
 
@@ -310,13 +321,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       }
       if (sidx + 1 < nstages) stage_tables(tb ^ 1, n0 + FWD_KS);
       cp_async_commit();
-      const TabWin w{Ts[tb], FWD_KS, 31};
-#pragma unroll 8
-      for (int k = 0; k < FWD_KS; ++k) {
-        const int64_t n = n0 + k;
-        Pt[buf][k][p] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-        if (n + 1 < cut) rec_step_win(reg, xx, w, k, s0, s1);
-      }
+      const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
+      gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1,
+                                [&](int k, double v) { Pt[buf][k][p] = v; });
       cp_async_wait_all();
       named_sync(BAR_PROD, W::NP);            // next stage's tables visible to all producers
       named_arrive(BAR_FULL + buf, W::NTH);   // P^T and c tile of this stage are ready
@@ -418,7 +425,6 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     cp_async_commit();
     cp_async_wait_all();
     named_sync(BAR_PROD, W::NP);
-    const TabWin win{Tw, SPANP, 5};
     const GenState* gbase = gen + (int64_t)it.t_begin * 128 + p;
     GenState nxt = gbase[0];
     const int nl0 = CK * gq;
@@ -441,12 +447,10 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       const int64_t cut = g.cutreg >> 2;
       const int reg = (int)(g.cutreg & 3) - 1;
       double* dst = &Ps[buf][grow][CK * gq + gq];
-#pragma unroll 8
-      for (int k = 0; k < CK; ++k) {
-        const int64_t n = nstart + k;
-        dst[k] = (n < cut) ? rec_value(reg, g.s0, g.s1) : 0.0;
-        if (n + 1 < cut) rec_step_win(reg, g.xx, win, nl0 + k, g.s0, g.s1);
-      }
+      const int nval = (int)max((int64_t)0, min((int64_t)CK + 1, cut - nstart));
+      // this chunk's window: degrees nl0 + k at slot nl0 + k + gq (pad per 32)
+      gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + gq, nval, g.s0, g.s1,
+                           [&](int k, double v) { dst[k] = v; });
       cp_async_wait_all();
       named_arrive(BAR_FULL + buf, W::NTH);
     }
