@@ -39,9 +39,6 @@ __device__ __forceinline__ void rec_init(int reg, double& s0, double& s1) {
     s1 = 0.0;
   }
 }
-__device__ __forceinline__ double rec_value(int reg, double s0, double s1) {
-  return reg == 0 ? s1 : s0;
-}
 // degree n -> n+1 (reference arithmetic, _kernels_cy.pyx:144-147, 186-188)
 __device__ __forceinline__ void rec_step(int reg, double x, double xm, const RecTablesDev& t,
                                          int64_t n, double& s0, double& s1) {
@@ -73,9 +70,9 @@ __device__ __forceinline__ void load_state(const RecRowsDev& rows, const int64_t
   }
 }
 
-// Generation arithmetic of the contraction kernels (FMA form).  The
-// reference's rounding (rec_step) is kept where its exact values are the
-// contract: plan-time checkpoints and the Clenshaw plugin.  The P values the
+// Generation arithmetic of the contraction kernels (FMA form; gen_chain,
+// gen_chain_g below).  The reference's rounding (rec_step) is kept where its
+// exact values are the contract: plan-time checkpoints and the Clenshaw plugin.  The P values the
 // transforms contract with are generated with the same recurrences in FMA
 // form, whose dependency chain is two operations per degree instead of five
 // (Reinsch) or two instead of three (three-term), with a' = A / rf, c' = C / rf
@@ -84,22 +81,6 @@ __device__ __forceinline__ void load_state(const RecRowsDev& rows, const int64_t
 //   Reinsch:    d = fma(a' xm, s0, c' s1);  s0 <- fma(rf, d, rf s0);  s1 <- d
 // (algebraically identical to _kernels_cy.pyx:144-147 / 186-188; differs by
 // rounding only, well inside the transform tolerance).
-__device__ __forceinline__ void rec_step_fast(int reg, double x, double xm, const RecTablesDev& t,
-                                              int64_t n, double& s0, double& s1) {
-  if (reg == 0) {
-    const double a = __ldg(t.A + n), bb = __ldg(t.B + n), c = __ldg(t.C + n);
-    const double pn = fma(fma(a, x, bb), s1, -(c * s0));
-    s0 = s1;
-    s1 = pn;
-  } else {
-    const double ap = __ldg((reg > 0 ? t.Ap : t.Am) + n);
-    const double cp = __ldg((reg > 0 ? t.Cp : t.Cm) + n);
-    const double rf = __ldg((reg > 0 ? t.rfp : t.rfm) + n);
-    const double d = fma(ap * xm, s0, cp * s1);
-    s0 = fma(rf, d, rf * s0);
-    s1 = d;
-  }
-}
 
 // Recurrence tables of a degree window staged in shared memory:
 // rows 0..8 = A, B, C, rf+, rf-, A/rf+, A/rf-, C/rf+, C/rf- (REC_WIN_ROWS),
@@ -149,6 +130,39 @@ __device__ __forceinline__ void gen_chain(int reg, double xx, const double* tb, 
       if (k + 1 < nval) {
         const double d = fma(ap[k] * xx, s0, cp[k] * s1);
         s0 = fma(rf[k], d, rf[k] * s0);
+        s1 = d;
+      }
+    }
+  }
+}
+
+// The same chain with the tables read from global memory (L1-resident
+// windows) from degree n0: pgen kernels of the two-pass contraction.
+template <int K, class Store>
+__device__ __forceinline__ void gen_chain_g(int reg, double xx, const RecTablesDev& t, int64_t n0,
+                                            int nval, double& s0, double& s1, const Store& st) {
+  if (reg == 0) {
+    const double *A = t.A + n0, *B = t.B + n0, *C = t.C + n0;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      st(k, k < nval ? s1 : 0.0);
+      if (k + 1 < nval) {
+        const double pn = fma(fma(__ldg(A + k), xx, __ldg(B + k)), s1, -(__ldg(C + k) * s0));
+        s0 = s1;
+        s1 = pn;
+      }
+    }
+  } else {
+    const double* rf = (reg > 0 ? t.rfp : t.rfm) + n0;
+    const double* ap = (reg > 0 ? t.Ap : t.Am) + n0;
+    const double* cp = (reg > 0 ? t.Cp : t.Cm) + n0;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      st(k, k < nval ? s0 : 0.0);
+      if (k + 1 < nval) {
+        const double r = __ldg(rf + k);
+        const double d = fma(__ldg(ap + k) * xx, s0, __ldg(cp + k) * s1);
+        s0 = fma(r, d, r * s0);
         s1 = d;
       }
     }
@@ -591,12 +605,9 @@ __global__ void __launch_bounds__(128)
         load_state(rows, ck_off, ck, i, n0, reg, s0, s1);
       }
     }
-#pragma unroll 4
-    for (int k = 0; k < FWD_KS; ++k) {
-      const int64_t n = n0 + k;
-      out[k * FWD_ROWS] = (n < cut) ? rec_value(reg, s0, s1) : 0.0;
-      if (n + 1 < cut) rec_step_fast(reg, x, xm, tab, n, s0, s1);
-    }
+    const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
+    gen_chain_g<FWD_KS>(reg, reg == 0 ? x : xm, tab, n0, nval, s0, s1,
+                        [&](int k, double v) { out[k * FWD_ROWS] = v; });
   }
 }
 
@@ -613,14 +624,10 @@ __global__ void __launch_bounds__(128)
     const int64_t cut = st.cutreg >> 2;
     const int reg = (int)(st.cutreg & 3) - 1;
     const int64_t nstart = (int64_t)gn0[g] + CK * q;
-    const double x = reg == 0 ? st.xx : 0.0, xm = reg == 0 ? 0.0 : st.xx;
     double* out = P + (g - gbeg) * (INV_RT * INV_DT) + (CK * q) * INV_RT + row;
-#pragma unroll 4
-    for (int k = 0; k < CK; ++k) {
-      const int64_t n = nstart + k;
-      out[k * INV_RT] = (n < cut) ? rec_value(reg, st.s0, st.s1) : 0.0;
-      if (n + 1 < cut) rec_step_fast(reg, x, xm, tab, n, st.s0, st.s1);
-    }
+    const int nval = (int)max((int64_t)0, min((int64_t)CK + 1, cut - nstart));
+    gen_chain_g<CK>(reg, st.xx, tab, nstart, nval, st.s0, st.s1,
+                    [&](int k, double v) { out[k * INV_RT] = v; });
   }
 }
 
