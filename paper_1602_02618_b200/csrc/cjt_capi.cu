@@ -366,9 +366,10 @@ int build_items(cjt_plan* P, int64_t batch) {
   P->vt = pick_vt(batch);
   P->chunks.clear();
   P->chunk_bytes = 0;
-  // two-pass only pays when each generated P value feeds >= 32 vectors; at
-  // VT = 16 the streamed P makes the GEMM memory-bound (fused kernels win)
-  const int64_t budget_blocks = P->vt >= 32 ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
+  // two-pass (P through HBM, DMMA GEMM without generation on the pipe) only
+  // pays at VT = 128; up to 64 vectors per tile the warp-specialised kernels
+  // (issue-lean producers) win (config-2 / config-3 launch lists)
+  const int64_t budget_blocks = P->vt >= 128 ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
   P->vt = pick_vt(batch);
   const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {

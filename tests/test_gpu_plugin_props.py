@@ -138,11 +138,12 @@ def test_two_pass_chunking_and_fused_fallback(cuda, chunk_mb, monkeypatch):
     a, b, n = -0.25, 0.4, 2047
     p = cj.JacobiParameters(a, b)
     fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
-    c = np.stack([O.seeded_vector(2, v, n) for v in range(70)])
+    # 300 vectors: 128-vector tiles, the two-pass path (generate P, then GEMM)
+    c = np.stack([O.seeded_vector(2, v, n) for v in range(300)])
     f = cj.forward_batched(fp, torch.from_numpy(c).to(cuda))
     i = cj.inverse_batched(ip, f).cpu().numpy()
     f = f.cpu().numpy()
-    for v in (0, 33, 69):
+    for v in (0, 170, 299):
         rf = O.oracle_forward(a, b, c[v])
         assert O.parity(f[v], rf, c[v]) <= 1e-12
         assert O.parity(i[v], O.oracle_inverse(a, b, f[v]), f[v]) <= 1e-12
