@@ -323,11 +323,11 @@ __global__ void __launch_bounds__(256) k_chirpz_combine_sk(ChirpZDev cz, const d
   const int64_t ca = sk.cta_of(gj * per_gj), cb = sk.cta_of(gj * per_gj + per_gj - 1);
   const int64_t stride = (int64_t)ng * cz.count_max;
   const double* pe = part + gi * cz.count_max + e;
-  double v = 0.0;
-  for (int64_t c = ca; c <= cb; ++c) {
-    const int64_t k = gj - sk.start(c) / cz.n_in / cz.m_count;
-    v += pe[(c * sk.S + k) * stride];
-  }
+  // the first CTA may hold earlier segments (slot k_a); every later one
+  // starts inside this (group, j) and holds it in its slot 0
+  const int64_t ka = gj - sk.start(ca) / cz.n_in / cz.m_count;
+  double v = pe[(ca * sk.S + ka) * stride];
+  for (int64_t c = ca + 1; c <= cb; ++c) v += pe[c * sk.S * stride];
   double* o = out + b * ldo + cz.q0 + so + e;
   *o = cz.accumulate ? *o + v : v;
 }

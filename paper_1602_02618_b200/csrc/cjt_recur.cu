@@ -395,6 +395,7 @@ __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
   const int64_t tile = i / FWD_ROWS, lr = i % FWD_ROWS;
   const int32_t s0 = tile_slot0[tile], ns = tile_nslot[tile];
   double acc = 0.0;
+#pragma unroll 8   // independent loads in flight; the sum keeps its fixed order
   for (int s = 0; s < ns; ++s) acc += part[((int64_t)(s0 + s) * batch + b) * FWD_ROWS + lr];
   vals[b * ldv + i] = acc;
 }
@@ -523,6 +524,7 @@ __global__ void k_inverse_finish(const int32_t* __restrict__ dt_slot0,
   const int64_t d = n / INV_DT, k = n % INV_DT;
   const int32_t s0 = dt_slot0[d], ns = dt_nslot[d];
   double acc = blocks_acc ? blocks_acc[b * ldo + n] : 0.0;
+#pragma unroll 8   // independent loads in flight; the sum keeps its fixed order
   for (int s = 0; s < ns; ++s) acc += part[((int64_t)(s0 + s) * batch + b) * INV_DT + k];
   out[b * ldo + n] = acc * scal[n];
 }
