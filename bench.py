@@ -513,7 +513,7 @@ def run_ours5(args, wl):
     y = torch.empty_like(x)
     z = torch.empty_like(x)
     rp.reserve()
-    nstreams = 4
+    nstreams = int(os.environ.get("CJT_RAGGED_STREAMS", "4"))
     streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
     assignment = rp.assign(nstreams)
 

@@ -542,8 +542,11 @@ constexpr int INV_RT = 32;      // grid rows per inverse pipeline stage (= row t
 bool cluster_enabled();
 
 // vectors per CTA tile of the DMMA contractions, chosen from the batch size
+// vector tile: one tile per batch up to 128 vectors (the recurrence is then
+// generated once; the warp-specialised producers, not the DMMA width, bound
+// the small tiles), 128 beyond
 inline int pick_vt(int64_t batch) {
-  return batch >= 256 ? 128 : batch >= 64 ? 64 : (batch >= 32 ? 32 : 16);
+  return batch <= 16 ? 16 : batch <= 32 ? 32 : batch <= 64 ? 64 : 128;
 }
 
 // ---------------------------------------------------------------------------

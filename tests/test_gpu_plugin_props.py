@@ -212,4 +212,7 @@ def test_pipeline_and_concurrent_streams(cuda):
         cj.forward_batched(fp, x[48:].contiguous(), out=y2)
     torch.cuda.synchronize()
     whole = cj.forward_batched(fp, x)
-    assert torch.equal(torch.cat([y1, y2]), whole)
+    # batch 48 vs 96 picks different vector tiles / schedules: equal up to
+    # rounding (same-batch re-execution is bitwise, test_reexecution_bit_identical)
+    diff = (torch.cat([y1, y2]) - whole).abs().max(dim=1).values
+    assert float((diff / x.abs().sum(dim=1)).max()) <= 1e-15
