@@ -152,6 +152,31 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
 int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n,
                     double* x, double* xm);
 
+/* Batched reference-signature Clenshaw-Smith / Reinsch evaluation with DEVICE
+ * pointers (recurrences.py:150-171 evaluate_expansion, over a batch):
+ * out[b*ldo + i] = sum_{n < cuts[i]} coeffs[b*ldc + n] P_n(x_i), plain
+ * Clenshaw-Smith where regions[i] == 0, Reinsch anchored at +-1 otherwise,
+ * x / xm as cjt_host_angles returns them; tables hold >= max(cuts)+1
+ * entries (table_len).  batch <= 65535.  Bit-identical to the reference
+ * kernel per vector.  Stream ordered, no allocation. */
+int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C,
+                            const double* rb_plus, const double* rb_minus,
+                            const double* rb_plus_inv, const double* rb_minus_inv,
+                            int64_t table_len, const double* coeffs, int64_t ldc,
+                            const double* x, const double* xm, const int64_t* cuts,
+                            const int8_t* regions, double* out, int64_t ldo,
+                            int64_t n_points, int64_t batch, void* stream);
+
+/* P_0..P_{n_max} at each angle (recurrences.py:74-112 jacobi_forward /
+ * jacobi_forward_reinsch), host pointers: modes[i] = 0 plain forward
+ * recurrence at cos(theta_i); +1 / -1 Reinsch's modified recurrence anchored
+ * at x0 = +1 / -1 (rf_plus / rf_minus).  out: [n_points][n_max+1], the
+ * reference's operation order (bit-identical).  Tables hold >= n_max entries. */
+int cjt_jacobi_values(const double* A, const double* B, const double* C,
+                      const double* rf_plus, const double* rf_minus, int64_t table_len,
+                      int64_t n_max, const double* thetas, const int8_t* modes,
+                      int64_t n_points, double* out);
+
 /* Integer parameter shifts of Jacobi coefficient vectors (engine.py:232-292),
  * device pointers, in/out: [batch][n+1] float64 (may not alias), (alpha,
  * beta) = the SOURCE parameters; the result is in the shifted basis

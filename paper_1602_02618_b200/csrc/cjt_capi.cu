@@ -997,9 +997,60 @@ int cjt_clenshaw_points(const double* A, const double* B, const double* C, const
   if (int rc = dalloc(tmp, &p, (size_t)n_points * 8)) return rc;
   dout = (double*)p;
   RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr, (int64_t)tl};
-  if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, dx, dxm, dreg, dcut, dout, n_points, 0))
+  if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, 0, dx, dxm, dreg, dcut, dout, 0,
+                                     n_points, 1, 0))
     return rc;
   CJT_CUDA_TRY(cudaMemcpy(out, dout, (size_t)n_points * 8, cudaMemcpyDeviceToHost));
+  return CJT_OK;
+}
+
+int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C, const double* rb_plus,
+                            const double* rb_minus, const double* rb_plus_inv,
+                            const double* rb_minus_inv, int64_t table_len, const double* coeffs,
+                            int64_t ldc, const double* x, const double* xm, const int64_t* cuts,
+                            const int8_t* regions, double* out, int64_t ldo, int64_t n_points,
+                            int64_t batch, void* stream) {
+  if (n_points < 0 || batch < 0 || table_len < 0) return fail(CJT_EINVAL, "negative size");
+  if (n_points == 0 || batch == 0) return CJT_OK;
+  if (!A || !B || !C || !rb_plus || !rb_minus || !rb_plus_inv || !rb_minus_inv || !coeffs || !x ||
+      !xm || !cuts || !regions || !out)
+    return fail(CJT_EINVAL, "null argument");
+  RecTablesDev tab{A, B, C, nullptr, nullptr, nullptr, nullptr, table_len};
+  return launch_clenshaw_points(tab, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv, coeffs, ldc, x, xm,
+                                regions, cuts, out, ldo, n_points, batch, (cudaStream_t)stream);
+}
+
+int cjt_jacobi_values(const double* A, const double* B, const double* C, const double* rf_plus,
+                      const double* rf_minus, int64_t table_len, int64_t n_max,
+                      const double* thetas, const int8_t* modes, int64_t n_points, double* out) {
+  if (n_points < 0 || n_max < 0) return fail(CJT_EINVAL, "negative size");
+  if (n_points == 0) return CJT_OK;
+  if (table_len < n_max) return fail(CJT_EINVAL, "tables shorter than n_max");
+  for (int64_t i = 0; i < n_points; ++i)
+    if (modes[i] < -1 || modes[i] > 1) return fail(CJT_EINVAL, "mode must be -1, 0 or +1");
+  std::vector<double> x((size_t)n_points), xm((size_t)n_points);
+  cjt_host_angles(thetas, modes, n_points, x.data(), xm.data());
+  std::vector<void*> tmp;
+  struct Free {
+    std::vector<void*>* v;
+    ~Free() { for (void* p : *v) cudaFree(p); }
+  } fr{&tmp};
+  const size_t tl = (size_t)std::max<int64_t>(n_max, 1);
+  double *dA, *dB, *dC, *rfp, *rfm, *dx, *dxm;
+  int8_t* dmode;
+  const double* srcs[5] = {A, B, C, rf_plus, rf_minus};
+  double** dsts[5] = {&dA, &dB, &dC, &rfp, &rfm};
+  for (int k = 0; k < 5; ++k)
+    if (int rc = upload(tmp, dsts[k], srcs[k], tl)) return rc;
+  if (int rc = upload(tmp, &dx, x.data(), x.size())) return rc;
+  if (int rc = upload(tmp, &dxm, xm.data(), xm.size())) return rc;
+  if (int rc = upload(tmp, &dmode, modes, (size_t)n_points)) return rc;
+  const size_t nout = (size_t)n_points * (size_t)(n_max + 1);
+  void* p;
+  if (int rc = dalloc(tmp, &p, nout * 8)) return rc;
+  RecTablesDev tab{dA, dB, dC, rfp, rfm, nullptr, nullptr, (int64_t)tl};
+  if (int rc = launch_jacobi_values(tab, n_max, dx, dxm, dmode, (double*)p, n_points, 0)) return rc;
+  CJT_CUDA_TRY(cudaMemcpy(out, p, nout * 8, cudaMemcpyDeviceToHost));
   return CJT_OK;
 }
 

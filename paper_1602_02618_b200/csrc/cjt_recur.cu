@@ -534,12 +534,15 @@ __global__ void k_inverse_finish(const int32_t* __restrict__ dt_slot0,
 __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ rbp,
                                   const double* __restrict__ rbm, const double* __restrict__ rbpi,
                                   const double* __restrict__ rbmi,
-                                  const double* __restrict__ coeffs, const double* __restrict__ xs,
-                                  const double* __restrict__ xms, const int8_t* __restrict__ regs,
-                                  const int64_t* __restrict__ cuts, double* __restrict__ out,
-                                  int64_t npts) {
+                                  const double* __restrict__ coeffs, int64_t ldc,
+                                  const double* __restrict__ xs, const double* __restrict__ xms,
+                                  const int8_t* __restrict__ regs, const int64_t* __restrict__ cuts,
+                                  double* __restrict__ out, int64_t ldo, int64_t npts) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npts) return;
+  // batch: vector blockIdx.y (evaluate_expansion_batched); the plugin uses one
+  coeffs += (int64_t)blockIdx.y * ldc;
+  out += (int64_t)blockIdx.y * ldo;
   const int64_t nc = cuts[i];
   if (nc <= 0) {
     out[i] = 0.0;
@@ -569,6 +572,42 @@ __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ r
     }
     out[i] = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(tab.A[0], xm), u), __dmul_rn(tab.C[1], d)),
                        coeffs[0]);
+  }
+}
+
+// P_0 .. P_{n_max} at one point per thread (recurrences.py:74-112): the plain
+// forward three-term recurrence (mode 0) or Reinsch's modified forward
+// recurrence anchored at +1 / -1 (mode +1 / -1, rf = rf_plus / rf_minus), the
+// reference's operation order and true division, so values are bit-identical.
+// out: [npts][n_max + 1].
+__global__ void k_jacobi_values(RecTablesDev tab, int64_t n_max, const double* __restrict__ xs,
+                                const double* __restrict__ xms, const int8_t* __restrict__ mode,
+                                double* __restrict__ out, int64_t npts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npts) return;
+  double* o = out + i * (n_max + 1);
+  o[0] = 1.0;
+  const int md = mode[i];
+  if (md == 0) {
+    const double x = xs[i];
+    double p_prev = 0.0, p_cur = 1.0;
+    for (int64_t n = 0; n < n_max; ++n) {
+      const double t = __dmul_rn(__dadd_rn(__dmul_rn(tab.A[n], x), tab.B[n]), p_cur);
+      const double p_next = __dsub_rn(t, __dmul_rn(tab.C[n], p_prev));
+      p_prev = p_cur;
+      p_cur = p_next;
+      o[n + 1] = p_cur;
+    }
+  } else {
+    const double xm = xms[i];
+    const double* rf = md > 0 ? tab.rfp : tab.rfm;
+    double pi_cur = 1.0, d = 0.0;
+    for (int64_t n = 0; n < n_max; ++n) {
+      const double num = __dadd_rn(__dmul_rn(__dmul_rn(tab.A[n], xm), pi_cur), __dmul_rn(tab.C[n], d));
+      d = __ddiv_rn(num, rf[n]);
+      pi_cur = __dmul_rn(__dadd_rn(pi_cur, d), rf[n]);
+      o[n + 1] = pi_cur;
+    }
   }
 }
 
@@ -887,12 +926,24 @@ int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int6
 
 int launch_clenshaw_points(const RecTablesDev& tab, const double* rbp, const double* rbm,
                            const double* rbpi, const double* rbmi, const double* coeffs,
-                           const double* x, const double* xm, const int8_t* reg,
-                           const int64_t* cut, double* out, int64_t npts, cudaStream_t st) {
+                           int64_t ldc, const double* x, const double* xm, const int8_t* reg,
+                           const int64_t* cut, double* out, int64_t ldo, int64_t npts,
+                           int64_t batch, cudaStream_t st) {
+  if (npts <= 0 || batch <= 0) return CJT_OK;
+  if (batch > 65535) return fail(CJT_EINVAL, "clenshaw batch must be <= 65535 per call");
+  const int T = 128;
+  dim3 grid((unsigned)((npts + T - 1) / T), (unsigned)batch);
+  k_clenshaw_points<<<grid, T, 0, st>>>(tab, rbp, rbm, rbpi, rbmi, coeffs, ldc, x, xm, reg, cut, out,
+                                        ldo, npts);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int launch_jacobi_values(const RecTablesDev& tab, int64_t n_max, const double* x, const double* xm,
+                         const int8_t* mode, double* out, int64_t npts, cudaStream_t st) {
   if (npts <= 0) return CJT_OK;
   const int T = 128;
-  k_clenshaw_points<<<(unsigned)((npts + T - 1) / T), T, 0, st>>>(tab, rbp, rbm, rbpi, rbmi, coeffs,
-                                                                  x, xm, reg, cut, out, npts);
+  k_jacobi_values<<<(unsigned)((npts + T - 1) / T), T, 0, st>>>(tab, n_max, x, xm, mode, out, npts);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }

@@ -20,6 +20,7 @@ import numpy as np
 from . import _native as nat
 from . import planner as pl
 from .planner import DEFAULT_EPS, DEFAULT_M, JacobiParameters, ParameterRangeError
+from .recurrences import AngleGrid
 
 CHEBYSHEV = "cheb"
 JACOBI = "jac"
@@ -60,15 +61,6 @@ def chebyshev(data) -> CoefficientVector:
 
 def jacobi(p: JacobiParameters, data) -> CoefficientVector:
     return CoefficientVector(JACOBI, np.asarray(data, dtype=float), p)
-
-
-@dataclass(frozen=True)
-class AngleGrid:
-    n: int
-    angles: np.ndarray = field(repr=False)
-
-    def __len__(self):
-        return self.n + 1
 
 
 class _DevicePlan:
