@@ -194,6 +194,38 @@ def run_reference(args, wl):
 # clocks
 
 
+def survey_flops(fhost, ihost, batch: int) -> float:
+    """Algorithmic flops of one forward + inverse of `batch` vectors by the
+    SURVEY.md 8(d) model F (the reference's own per-step constants and
+    layout; a build doing fewer real flops still uses this F):
+      B [6 S_f^int + 8 S_f^end + 2 (S_i^int + S_i^end)
+         + (2 M K_f + 1) 2.5 N log2 N + (2 M K_i + 1) 2.5 (2N) log2 (2N)]
+      + 5 S_i^int + 7 S_i^end      (diagonal scalings, < 2 %, omitted)."""
+    n = fhost.n
+    m = fhost.m_terms
+    fr, fc = fhost.regions, fhost.cuts.astype(np.float64)
+    ir, ic = ihost.regions, np.minimum(ihost.cuts, n + 1).astype(np.float64)
+    sf_int, sf_end = fc[fr == 0].sum(), fc[fr != 0].sum()
+    si_int, si_end = ic[ir == 0].sum(), ic[ir != 0].sum()
+    kf, ki = len(fhost.layout.blocks), len(ihost.layout.blocks)
+    fft = ((2 * m * kf + 1) * 2.5 * n * math.log2(n) if n > 1 else 0.0) \
+        + (2 * m * ki + 1) * 2.5 * (2 * n) * math.log2(2 * n)
+    per_vec = 6 * sf_int + 8 * sf_end + 2 * (si_int + si_end) + fft
+    return batch * per_vec + 5 * si_int + 7 * si_end
+
+
+def step_roofline(flop: float, peak_tflops: float, ms_per_step: float, coeffs: float) -> dict:
+    t_ms = flop / (peak_tflops * 1e12) * 1e3
+    t_hbm_ms = 32.0 * coeffs / 6.5546e12 * 1e3   # read c, write c per direction (SURVEY 8(d) bytes)
+    t_roof = max(t_ms, t_hbm_ms)
+    return {"model": "SURVEY.md 8(d) F: the reference's algorithmic fp64 flops per step",
+            "flop_per_step": float(flop), "t_fp64_ms": float(t_ms), "t_hbm_ms": float(t_hbm_ms),
+            "roofline_coeffs_per_s": float(coeffs / (t_roof * 1e-3)),
+            # capped at 1 (SURVEY 8(d)): the DMMA contraction does fewer real
+            # flops than the reference's per-vector Clenshaw chains
+            "frac": float(min(1.0, t_roof / ms_per_step)), "frac_uncapped": float(t_roof / ms_per_step)}
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -213,6 +245,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi needs a moment to start: wait for its first sample so
+            # that even a millisecond-long timed region is bracketed
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
@@ -223,6 +260,10 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # one more sample after the timed region (-lms 100)
+            n0, t0 = len(self.rows), time.time()
+            while len(self.rows) == n0 and time.time() - t0 < 1.0 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -376,6 +417,9 @@ def run_ours(args, wl):
                 "nominal_peak": NOMINAL_FP64_TFLOPS, "flops_model": unit_note,
                 "stage_ms": {k: round(v, 4) for k, v in stages.items()},
                 "stage_share": {k: round(v / sum(stages.values()), 4) for k, v in stages.items()}}
+
+    roofline["step"] = step_roofline(survey_flops(fp.host, ip.host, batch), peak, ms_per_step,
+                                     float(batch * n1))
 
     # e2e through the public API: pinned host input -> pipeline(forward, inverse)
     # -> pinned host output, copies overlapped with compute across 2 streams
@@ -613,6 +657,8 @@ def run_ours5(args, wl):
                 "flops_model": "2 flop per (point, degree, vector) contraction + 5 flop per (point, degree) generation",
                 "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
                 "stage_share": {k_: round(v / sum(stage_ms.values()), 4) for k_, v in stage_ms.items()}}
+    flop5 = sum(survey_flops(rp.plans[g][0].host, rp.plans[g][1].host, rp.sizes[g]) for g in range(len(rp.keys)))
+    roofline["step"] = step_roofline(flop5, peak, ms_per_step, float(rp.total))
     e2e = None
     if not args.no_e2e:
         pin_in = torch.from_numpy(host).pin_memory()

@@ -167,6 +167,18 @@ int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C,
                             const int8_t* regions, double* out, int64_t ldo,
                             int64_t n_points, int64_t batch, void* stream);
 
+/* The scalar reference helpers clenshaw_smith (modes[i] = 0) and
+ * clenshaw_smith_reinsch (modes[i] = end = +1 / -1) (recurrences.py:115-152),
+ * host pointers: out[i] = sum_{n < n_coeffs} coeffs[n] P_n(cos theta_i) with
+ * the Python helpers' operation order (the Reinsch step DIVIDES by rb[n]
+ * where the Cython plugin multiplies by 1/rb[n]), bit-identical to them.
+ * Tables hold >= n_coeffs + 1 entries. */
+int cjt_clenshaw_smith_points(const double* A, const double* B, const double* C,
+                              const double* rb_plus, const double* rb_minus,
+                              const double* coeffs, int64_t n_coeffs,
+                              const double* thetas, const int8_t* modes,
+                              int64_t n_points, double* out);
+
 /* P_0..P_{n_max} at each angle (recurrences.py:74-112 jacobi_forward /
  * jacobi_forward_reinsch), host pointers: modes[i] = 0 plain forward
  * recurrence at cos(theta_i); +1 / -1 Reinsch's modified recurrence anchored

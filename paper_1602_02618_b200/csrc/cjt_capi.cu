@@ -205,8 +205,9 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (lg < 4 || lg > 26) return fail(CJT_EINVAL, "chirp-z length must be a power of two in [16, 2^26]");
   if (d.width < 1 || d.count < 1 || d.m_count < 1 || d.n_tiles_in < 1 || d.n_tiles_out < 1)
     return fail(CJT_EINVAL, "inconsistent chirp-z descriptor");
-  if ((d.n_tiles_in > 1 || d.n_tiles_out > 1) && lg > 13)
-    return fail(CJT_EINVAL, "tiled chirp-z requires length <= 8192");
+  const bool tiled = d.n_tiles_in > 1 || d.n_tiles_out > 1;
+  if (tiled && lg > 13 && d.n_tiles_in > 1 && d.n_tiles_out > 1)
+    return fail(CJT_EINVAL, "tiled multi-pass chirp-z needs n_tiles_in == 1 or n_tiles_out == 1");
   {
     int64_t wsum = 0, csum = 0, wmax = 0, cmax = 0;
     for (int i = 0; i < d.n_tiles_in; ++i) {
@@ -235,7 +236,7 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (int rc = upload(P->allocs, const_cast<double2**>(&cz.post),
                       reinterpret_cast<const double2*>(d.post), nm * d.count)) return rc;
   const double2* kh = reinterpret_cast<const double2*>(d.kernel_hat);
-  const bool cluster = lg >= 14 && lg <= 17 && cluster_enabled();
+  const bool cluster = lg >= 14 && lg <= 17 && !tiled && cluster_enabled();
   if (lg <= 13 || cluster) {
     // cluster / short fused tiles read the spectra in natural order; the
     // two-level FFT (fft2_used) in the permuted order k1 S + k2 <- k1 + 16 k2
@@ -276,21 +277,28 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     cz.log1 = l1;
     cz.log2 = l2;
     const int64_t L1 = int64_t(1) << l1, L2 = int64_t(1) << l2;
-    std::vector<double2> perm((size_t)d.length);
+    const int64_t ntile = (int64_t)d.n_tiles_in * d.n_tiles_out;
+    std::vector<double2> perm((size_t)(d.length * ntile));
     const bool f2 = fft2_used(l2);
     const int64_t S2 = L2 / 16;
-    for (int64_t k1 = 0; k1 < L1; ++k1)
-      for (int64_t k2 = 0; k2 < L2; ++k2) {
-        // row k1, row spectrum index k2 (natural) or its two-level position
-        const int64_t pos = f2 ? (k2 % 16) * S2 + k2 / 16 : k2;
-        perm[(size_t)(k1 * L2 + pos)] = kh[k1 + L1 * k2];
-      }
+    for (int64_t tile = 0; tile < ntile; ++tile)
+      for (int64_t k1 = 0; k1 < L1; ++k1)
+        for (int64_t k2 = 0; k2 < L2; ++k2) {
+          // row k1, row spectrum index k2 (natural) or its two-level position
+          const int64_t pos = f2 ? (k2 % 16) * S2 + k2 / 16 : k2;
+          perm[(size_t)(tile * d.length + k1 * L2 + pos)] = kh[tile * d.length + k1 + L1 * k2];
+        }
     if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
-    P->scratch_elems_per_vec = std::max<int64_t>(P->scratch_elems_per_vec, d.length * d.m_count);
+    // one slot per input or output tile per (vector, term)
+    P->scratch_elems_per_vec = std::max<int64_t>(
+        P->scratch_elems_per_vec, d.length * d.m_count * std::max(d.n_tiles_in, d.n_tiles_out));
   }
   // FFTs executed per vector: per term, one forward FFT per input tile and one
-  // inverse FFT per output tile (tiles' spectra are summed before inverting)
-  P->fft_points += (double)d.m_count * d.n_tiles_out * (d.n_tiles_in + 1) * (double)d.length * lg;
+  // inverse FFT per output tile; on-chip tiles sum the input tiles' spectra
+  // per output tile, multi-pass tiles share the forward FFT across outputs
+  const double ffts = lg <= 13 ? (double)d.n_tiles_out * (d.n_tiles_in + 1)
+                               : (double)(d.n_tiles_in + d.n_tiles_out);
+  P->fft_points += (double)d.m_count * ffts * (double)d.length * lg;
   *out = cz;
   return CJT_OK;
 }
@@ -964,10 +972,11 @@ int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n, doub
   return CJT_OK;
 }
 
-int cjt_clenshaw_points(const double* A, const double* B, const double* C, const double* rb_plus,
-                        const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
-                        const double* coeffs, int64_t n_coeffs, const double* thetas,
-                        const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points) {
+static int clenshaw_host(const double* A, const double* B, const double* C, const double* rb_plus,
+                         const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
+                         const double* coeffs, int64_t n_coeffs, const double* thetas,
+                         const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points,
+                         int divide) {
   if (n_points < 0 || n_coeffs < 0) return fail(CJT_EINVAL, "negative size");
   if (n_points == 0) return CJT_OK;
   int64_t maxcut = 0;
@@ -998,10 +1007,30 @@ int cjt_clenshaw_points(const double* A, const double* B, const double* C, const
   dout = (double*)p;
   RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr, (int64_t)tl};
   if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, 0, dx, dxm, dreg, dcut, dout, 0,
-                                     n_points, 1, 0))
+                                     n_points, 1, divide != 0, 0))
     return rc;
   CJT_CUDA_TRY(cudaMemcpy(out, dout, (size_t)n_points * 8, cudaMemcpyDeviceToHost));
   return CJT_OK;
+}
+
+int cjt_clenshaw_points(const double* A, const double* B, const double* C, const double* rb_plus,
+                        const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
+                        const double* coeffs, int64_t n_coeffs, const double* thetas,
+                        const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points) {
+  return clenshaw_host(A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv, coeffs, n_coeffs, thetas,
+                       cuts, regions, out, n_points, 0);
+}
+
+int cjt_clenshaw_smith_points(const double* A, const double* B, const double* C, const double* rb_plus,
+                              const double* rb_minus, const double* coeffs, int64_t n_coeffs,
+                              const double* thetas, const int8_t* modes, int64_t n_points, double* out) {
+  if (n_coeffs < 1 || n_points < 0) return fail(CJT_EINVAL, "need >= 1 coefficient");
+  for (int64_t i = 0; i < n_points; ++i)
+    if (modes[i] < -1 || modes[i] > 1) return fail(CJT_EINVAL, "mode must be -1, 0 or +1");
+  std::vector<int64_t> cuts((size_t)n_points, n_coeffs);
+  // the reciprocal tables are unused by the dividing variant
+  return clenshaw_host(A, B, C, rb_plus, rb_minus, rb_plus, rb_minus, coeffs, n_coeffs, thetas,
+                       cuts.data(), modes, out, n_points, 1);
 }
 
 int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C, const double* rb_plus,
@@ -1017,7 +1046,7 @@ int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C, c
     return fail(CJT_EINVAL, "null argument");
   RecTablesDev tab{A, B, C, nullptr, nullptr, nullptr, nullptr, table_len};
   return launch_clenshaw_points(tab, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv, coeffs, ldc, x, xm,
-                                regions, cuts, out, ldo, n_points, batch, (cudaStream_t)stream);
+                                regions, cuts, out, ldo, n_points, batch, false, (cudaStream_t)stream);
 }
 
 int cjt_jacobi_values(const double* A, const double* B, const double* C, const double* rf_plus,

@@ -456,18 +456,21 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
   // consecutive CTAs share a column tile across vectors: the pre table stays in L2
   const int64_t c0 = (int64_t)blockIdx.y * NC;
   const int64_t b = blockIdx.x;
-  const double* xb = x + b * ldx + cz.p0;
+  // input tile blockIdx.z (tiled multi-pass): columns of x[to .. to + tn)
+  const int64_t to = __ldg(cz.tin + 2 * blockIdx.z), tn = __ldg(cz.tin + 2 * blockIdx.z + 1);
+  const int nslot = max(cz.n_in, cz.n_out);
+  const double* xb = x + b * ldx + cz.p0 + to;
   const int grp = threadIdx.x / (L1 / 16);
   const int t = threadIdx.x % (L1 / 16);
   for (int m = 0; m < cz.m_count; ++m) {
-    const double2* pre = cz.pre + (int64_t)m * cz.width;
+    const double2* pre = cz.pre + (int64_t)m * cz.width + to;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int idx = threadIdx.x + i * T;
       const int c = idx % NC, n1 = idx / NC;
       const int64_t pidx = (int64_t)n1 * L2 + c0 + c;
       double2 v = make_double2(0.0, 0.0);
-      if (pidx < cz.width) {
+      if (pidx < tn) {
         const double xv = __ldg(xb + pidx);
         const double2 p = __ldg(pre + pidx);
         v = make_double2(xv * p.x, xv * p.y);
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
     __syncthreads();
     fft_smem<LOG1, -1, 4, FftSync<LOG1, 4>>(smem + grp * CS, t, tw);
     __syncthreads();   // the transposed store reads other warps' columns
-    double2* bm = buf + (b * cz.m_count + m) * L;
+    double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L;
     // this thread's column n2 is fixed and k1 = k1_0 + i T/NC: twiddles
     // W_L^{n2 k1} by a running product from two table values
     const int c = threadIdx.x % NC;
@@ -525,26 +528,29 @@ __global__ void __launch_bounds__(COLR_T)
   const int64_t L = cz.length;
   const int64_t n2 = (int64_t)blockIdx.y * COLR_T + threadIdx.x;
   const int64_t b = blockIdx.x;
-  const double* xb = x + b * ldx + cz.p0;
+  // input tile blockIdx.z (tiled multi-pass): x[to .. to + tn) -> slot blockIdx.z
+  const int64_t to = __ldg(cz.tin + 2 * blockIdx.z), tn = __ldg(cz.tin + 2 * blockIdx.z + 1);
+  const int nslot = max(cz.n_in, cz.n_out);
+  const double* xb = x + b * ldx + cz.p0 + to;
   double xv[L1];
 #pragma unroll
   for (int r = 0; r < L1; ++r) {
     const int64_t pidx = r * L2 + n2;
-    xv[r] = pidx < cz.width ? __ldg(xb + pidx) : 0.0;
+    xv[r] = pidx < tn ? __ldg(xb + pidx) : 0.0;
   }
   double2 w[L1];
   column_twiddles<L1>(cz, n2, w);
   for (int m = 0; m < cz.m_count; ++m) {
-    const double2* pre = cz.pre + (int64_t)m * cz.width;
+    const double2* pre = cz.pre + (int64_t)m * cz.width + to;
     double2 v[L1];
 #pragma unroll
     for (int r = 0; r < L1; ++r) {
       const int64_t pidx = r * L2 + n2;
-      const double2 p = pidx < cz.width ? __ldg(pre + pidx) : make_double2(0.0, 0.0);
+      const double2 p = pidx < tn ? __ldg(pre + pidx) : make_double2(0.0, 0.0);
       v[r] = make_double2(xv[r] * p.x, xv[r] * p.y);
     }
     dft_reg<L1, -1>(v);
-    double2* bm = buf + (b * cz.m_count + m) * L + n2;
+    double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L + n2;
 #pragma unroll
     for (int k = 0; k < L1; ++k) bm[k * L2] = cmul(v[k], w[k]);
   }
@@ -559,31 +565,34 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
   const int64_t L = cz.length;
   const int64_t n2 = (int64_t)blockIdx.y * COLR_T + threadIdx.x;
   const int64_t b = blockIdx.x;
+  // output tile blockIdx.z (tiled multi-pass): slot blockIdx.z -> out[so .. so + sc)
+  const int64_t so = __ldg(cz.tout + 2 * blockIdx.z), sc = __ldg(cz.tout + 2 * blockIdx.z + 1);
+  const int nslot = max(cz.n_in, cz.n_out);
   double acc[L1];
 #pragma unroll
   for (int r = 0; r < L1; ++r) acc[r] = 0.0;
   // per term: the column and the output diagonal are loaded together (one
   // latency per term); the twiddle W_L^{-n2 k1} was applied by the row pass
-  const double2* bcol = buf + b * cz.m_count * L + n2;
+  const double2* bcol = buf + (b * cz.m_count * nslot + blockIdx.z) * L + n2;
   for (int m = 0; m < cz.m_count; ++m) {
-    const double2* post = cz.post + (int64_t)m * cz.count;
+    const double2* post = cz.post + (int64_t)m * cz.count + so;
     double2 v[L1], pq[L1];
 #pragma unroll
-    for (int k = 0; k < L1; ++k) v[k] = __ldcs(bcol + (int64_t)m * L + k * L2);
+    for (int k = 0; k < L1; ++k) v[k] = __ldcs(bcol + (int64_t)m * nslot * L + k * L2);
 #pragma unroll
     for (int r = 0; r < L1; ++r) {
       const int64_t q = r * L2 + n2;
-      pq[r] = q < cz.count ? __ldg(post + q) : make_double2(0.0, 0.0);
+      pq[r] = q < sc ? __ldg(post + q) : make_double2(0.0, 0.0);
     }
     dft_reg<L1, +1>(v);
 #pragma unroll
     for (int r = 0; r < L1; ++r) acc[r] += fma(pq[r].x, v[r].x, -pq[r].y * v[r].y);
   }
-  double* ob = out + b * ldo + cz.q0;
+  double* ob = out + b * ldo + cz.q0 + so;
 #pragma unroll
   for (int r = 0; r < L1; ++r) {
     const int64_t q = r * L2 + n2;
-    if (q < cz.count) ob[q] = cz.accumulate ? ob[q] + acc[r] : acc[r];
+    if (q < sc) ob[q] = cz.accumulate ? ob[q] + acc[r] : acc[r];
   }
 }
 
@@ -600,8 +609,17 @@ struct RowCfg {
 
 // pass 2: rows k1 of buf: FFT over n2 -> * khat[k1][k2] -> inverse FFT over k2
 // (global load fused into the first forward pass, the spectrum product into
-// the first inverse pass, the global store into the last inverse pass)
-template <int LOG2>
+// the first inverse pass, the global store into the last inverse pass).
+// Tiled multi-pass (n_in > 1 or n_out > 1; slots s < max(n_in, n_out) per
+// (vector, term) in buf):
+//   input tiles:  the row FFTs of slots 0..n_in-1 are multiplied by their
+//                 spectra and summed (running sum in slot 0, each element
+//                 owned by one thread), one inverse FFT -> slot 0;
+//   output tiles: one forward FFT, its spectrum kept in slot n_out-1; per
+//                 output tile j, spectrum * khat_j -> inverse FFT -> slot j.
+// TM (tiling mode): 0 untiled, 1 input tiles, 2 output tiles (separate
+// instantiations keep the untiled kernel's register allocation unchanged)
+template <int LOG2, int TM>
 __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ tw, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
@@ -613,42 +631,112 @@ __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
   // consecutive CTAs share spectrum rows across (vector, term): khat stays in L2
   const int64_t k1 = (int64_t)blockIdx.y * NR + grp;
   const int64_t L = cz.length;
-  double2* row = buf + (int64_t)blockIdx.x * L + k1 * L2;
-  const double2* kh = cz.khat + k1 * L2;
+  const int nslot = max(cz.n_in, cz.n_out);
+  double2* row = buf + (int64_t)blockIdx.x * nslot * L + k1 * L2;   // slot s: row + s L
+  const double2* kh = cz.khat + k1 * L2;                             // tile (j, i): kh + (j n_in + i) L
   double2* s = smem + grp * padded_len(L2);
-  auto load_row = [&](int e) -> double2 { return row[e]; };
   if constexpr (fft2_used(LOG2)) {
     // two-level FFT: khat rows are in the permuted order (capi)
     using F = Fft2<LOG2>;
-    fft2_first<LOG2>(s, t, tw, load_row);
-    __syncthreads();
     double2* reg = s + (t / F::TPS) * F::PS;
-    const double2* khr = kh + (t / F::TPS) * F::S;
-    auto mul_spec = [&](int e, double2 v) -> double2 { return cmul(v, __ldg(khr + e)); };
-    sub_conv<F::LOGS>(reg, t % F::TPS, tw, mul_spec);
-    __syncthreads();
-    if (cz.log1 <= 5) {
-      // the four-step inverse twiddle W_L^{-k1 e} of the register column pass
-      // is applied here: this thread stores e = t + S n1 for n1 = 0, 1, ...,
-      // so W^{-k1 t} (W^{-k1 S})^{n1} is a running product from two lookups
-      double2 w = twiddle_L(cz, k1 * t), ws = twiddle_L(cz, k1 * F::S);
-      w.y = -w.y;
-      ws.y = -ws.y;
-      auto store_tw = [&](int e, double2 v) {
-        row[e] = cmul(v, w);
-        w = cmul(w, ws);
-      };
-      fft2_last_inv<LOG2>(s, t, tw, store_tw);
-    } else {
-      auto store_row2 = [&](int e, double2 v) { row[e] = v; };
-      fft2_last_inv<LOG2>(s, t, tw, store_row2);
+    const int kofs = (t / F::TPS) * F::S;
+    // the register column pass (log1 <= 5) expects the four-step inverse
+    // twiddle W_L^{-k1 e} from here: this thread stores e = t + S n1 for
+    // n1 = 0, 1, ..., a running product from two lookups
+    auto store_out = [&](double2* dst) {
+      if (cz.log1 <= 5) {
+        double2 w = twiddle_L(cz, k1 * t), ws = twiddle_L(cz, k1 * F::S);
+        w.y = -w.y;
+        ws.y = -ws.y;
+        auto store_tw = [&](int e, double2 v) {
+          dst[e] = cmul(v, w);
+          w = cmul(w, ws);
+        };
+        fft2_last_inv<LOG2>(s, t, tw, store_tw);
+      } else {
+        auto store_row = [&](int e, double2 v) { dst[e] = v; };
+        fft2_last_inv<LOG2>(s, t, tw, store_row);
+      }
+    };
+    if constexpr (TM == 0) {
+      auto load_row = [&](int e) -> double2 { return row[e]; };
+      fft2_first<LOG2>(s, t, tw, load_row);
+      __syncthreads();
+      const double2* khr = kh + kofs;
+      auto mul_spec = [&](int e, double2 v) -> double2 { return cmul(v, __ldg(khr + e)); };
+      sub_conv<F::LOGS>(reg, t % F::TPS, tw, mul_spec);
+      __syncthreads();
+      store_out(row);
+      return;
+    }
+    if constexpr (TM == 1) {
+      double2* acc = row + kofs;   // running spectrum sum in slot 0 (thread-owned elements)
+      for (int i = 0; i < cz.n_in; ++i) {
+        const double2* src = row + (int64_t)i * L;
+        auto load_row = [&](int e) -> double2 { return src[e]; };
+        __syncthreads();   // previous readers of s are done
+        fft2_first<LOG2>(s, t, tw, load_row);
+        __syncthreads();   // (also: every load of slot 0 precedes the first acc store)
+        const double2* khr = kh + (int64_t)i * L + kofs;
+        const bool first = i == 0, last = i == cz.n_in - 1;
+        auto store_spec = [&](int e, double2 v) {
+          double2 y = cmul(v, __ldg(khr + e));
+          if (!first) {
+            const double2 a = __ldcg(acc + e);
+            y.x += a.x;
+            y.y += a.y;
+          }
+          if (last)
+            reg[pad16(e)] = y;
+          else
+            __stcg(acc + e, y);
+        };
+        fft2_sub<LOG2, -1>(s, t, tw, SmemLoad{reg}, store_spec);
+      }
+      fft2_sub<LOG2, +1>(s, t, tw, SmemLoad{reg}, SmemStore{reg});
+      __syncthreads();
+      store_out(row);
+      return;
+    }
+    // output tiles (TM == 2)
+    {
+      auto load_row = [&](int e) -> double2 { return row[e]; };
+      fft2_first<LOG2>(s, t, tw, load_row);
+      __syncthreads();
+    }
+    double2* keep = row + (int64_t)(cz.n_out - 1) * L + kofs;   // the forward spectrum
+    const double2* kh0 = kh + kofs;
+    auto store_spec0 = [&](int e, double2 v) {
+      __stcg(keep + e, v);
+      reg[pad16(e)] = cmul(v, __ldg(kh0 + e));
+    };
+    fft2_sub<LOG2, -1>(s, t, tw, SmemLoad{reg}, store_spec0);
+    const int lt = t % F::TPS;
+    for (int j = 0; j < cz.n_out; ++j) {
+      if (j > 0) {
+        __syncthreads();   // the previous tile's last pass has read every region
+        const double2* khr = kh + (int64_t)j * cz.n_in * L + kofs;
+        // the region's TPS threads share one warp: reload, then warp-sync
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int e = lt + k * F::TPS;
+          reg[pad16(e)] = cmul(__ldcg(keep + e), __ldg(khr + e));
+        }
+        __syncwarp();
+      }
+      fft2_sub<LOG2, +1>(s, t, tw, SmemLoad{reg}, SmemStore{reg});
+      __syncthreads();
+      store_out(row + (int64_t)j * L);
     }
     return;
-  }
+  } else {
+  // single-level FFT (CJT_FFT2=0 builds): untiled only (capi rejects tiles)
+  auto load_row = [&](int e) -> double2 { return row[e]; };
   fft_smem_io<LOG2, -1, decltype(load_row), SmemStore, Cfg::LEPT>(s, t, tw, load_row, SmemStore{s});
   auto load_spec = [&](int e) -> double2 { return cmul(s[pad16(e)], __ldg(kh + e)); };
   auto store_row = [&](int e, double2 v) { row[e] = v; };
   fft_smem_io<LOG2, +1, decltype(load_spec), decltype(store_row), Cfg::LEPT>(s, t, tw, load_spec, store_row);
+  }
 }
 
 // pass 3: columns n2: * W_L^{-n2 k1} -> inverse FFT over k1 -> sum_m Re(post_m * y) -> out
@@ -663,13 +751,15 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
   const int64_t L = cz.length;
   const int64_t c0 = (int64_t)blockIdx.y * NC;
   const int64_t b = blockIdx.x;
+  const int64_t so = __ldg(cz.tout + 2 * blockIdx.z), sc = __ldg(cz.tout + 2 * blockIdx.z + 1);
+  const int nslot = max(cz.n_in, cz.n_out);
   const int grp = threadIdx.x / (L1 / 16);
   const int t = threadIdx.x % (L1 / 16);
   double acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.0;
   for (int m = 0; m < cz.m_count; ++m) {
-    const double2* bm = buf + (b * cz.m_count + m) * L;
+    const double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L;
     {
       const int c = threadIdx.x % NC;
       const int64_t n2 = c0 + c;
@@ -686,13 +776,13 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
     __syncthreads();
     fft_smem<LOG1, +1, 4, FftSync<LOG1, 4>>(smem + grp * CS, t, tw);
     __syncthreads();   // the transposed store reads other warps' columns
-    const double2* post = cz.post + (int64_t)m * cz.count;
+    const double2* post = cz.post + (int64_t)m * cz.count + so;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int idx = threadIdx.x + i * T;
       const int c = idx % NC, n1 = idx / NC;
       const int64_t sidx = (int64_t)n1 * L2 + c0 + c;
-      if (sidx < cz.count) {
+      if (sidx < sc) {
         const double2 y = smem[c * CS + pad16(n1)];
         const double2 q = __ldg(post + sidx);
         acc[i] += fma(q.x, y.x, -q.y * y.y);
@@ -700,13 +790,13 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
     }
     __syncthreads();
   }
-  double* ob = out + b * ldo + cz.q0;
+  double* ob = out + b * ldo + cz.q0 + so;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int idx = threadIdx.x + i * T;
     const int c = idx % NC, n1 = idx / NC;
     const int64_t sidx = (int64_t)n1 * L2 + c0 + c;
-    if (sidx < cz.count) ob[sidx] = cz.accumulate ? ob[sidx] + acc[i] : acc[i];
+    if (sidx < sc) ob[sidx] = cz.accumulate ? ob[sidx] + acc[i] : acc[i];
   }
 }
 
@@ -816,12 +906,12 @@ int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
   if constexpr (LOG1 <= 5) {
-    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T));
+    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)cz.n_in);
     k_chirpz_cols_fwd_reg<LOG1><<<grid, COLR_T, 0, st>>>(cz, x, ldx, buf);
     CJT_CUDA_TRY(cudaGetLastError());
     return CJT_OK;
   }
-  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
+  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC), (unsigned)cz.n_in);
   k_chirpz_cols_fwd<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, x, ldx, buf);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
@@ -832,12 +922,15 @@ int run_rows(const ChirpZDev& cz, const double2* tw, double2* buf, int64_t batch
   using Cfg = RowCfg<LOG2>;
   static bool init = false;
   if (!init) {
-    if (int rc = set_smem(k_chirpz_rows<LOG2>, Cfg::SMEM)) return rc;
+    if (int rc = set_smem(k_chirpz_rows<LOG2, 0>, Cfg::SMEM)) return rc;
+    if (int rc = set_smem(k_chirpz_rows<LOG2, 1>, Cfg::SMEM)) return rc;
+    if (int rc = set_smem(k_chirpz_rows<LOG2, 2>, Cfg::SMEM)) return rc;
     init = true;
   }
   const int64_t L1 = (int64_t)1 << cz.log1;
   dim3 grid((unsigned)(batch * cz.m_count), (unsigned)(L1 / Cfg::NR));
-  k_chirpz_rows<LOG2><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf);
+  auto kern = cz.n_in > 1 ? k_chirpz_rows<LOG2, 1> : cz.n_out > 1 ? k_chirpz_rows<LOG2, 2> : k_chirpz_rows<LOG2, 0>;
+  kern<<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -853,12 +946,12 @@ int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, dou
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
   if constexpr (LOG1 <= 5) {
-    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T));
+    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)cz.n_out);
     k_chirpz_cols_inv_reg<LOG1><<<grid, COLR_T, 0, st>>>(cz, buf, out, ldo);
     CJT_CUDA_TRY(cudaGetLastError());
     return CJT_OK;
   }
-  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC));
+  dim3 grid((unsigned)batch, (unsigned)(L2 / Cfg::NC), (unsigned)cz.n_out);
   k_chirpz_cols_inv<LOG1><<<grid, Cfg::T, Cfg::SMEM, st>>>(cz, tw, buf, out, ldo);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
@@ -917,6 +1010,8 @@ int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, i
   int rc = CJT_OK;
   // register column passes rely on the row pass applying the inverse twiddle
   if (cz.log1 <= 5 && !fft2_used(cz.log2)) return fail(CJT_EINVAL, "multi-pass split unsupported");
+  if ((cz.n_in > 1 || cz.n_out > 1) && (!fft2_used(cz.log2) || (cz.n_in > 1 && cz.n_out > 1)))
+    return fail(CJT_EINVAL, "tiled multi-pass chirp-z needs n_in == 1 or n_out == 1");
   switch (cz.log1) {
 #define CJT_COLF(K) case K: rc = run_cols_fwd<K>(cz, tw8192, x, ldx, scratch, batch, st); break;
     CJT_COLF(4) CJT_COLF(5) CJT_COLF(6) CJT_COLF(7) CJT_COLF(8) CJT_COLF(9) CJT_COLF(10) CJT_COLF(11)

@@ -595,7 +595,7 @@ int launch_clenshaw_points(const RecTablesDev& tab, const double* rbp, const dou
                            const double* rbpi, const double* rbmi, const double* coeffs,
                            int64_t ldc, const double* x, const double* xm, const int8_t* reg,
                            const int64_t* cut, double* out, int64_t ldo, int64_t npts,
-                           int64_t batch, cudaStream_t st);
+                           int64_t batch, bool divide, cudaStream_t st);
 int launch_jacobi_values(const RecTablesDev& tab, int64_t n_max, const double* x, const double* xm,
                          const int8_t* mode, double* out, int64_t npts, cudaStream_t st);
 

@@ -531,6 +531,9 @@ __global__ void k_inverse_finish(const int32_t* __restrict__ dt_slot0,
 
 // Reference-signature Clenshaw-Smith / Reinsch evaluation, one thread per
 // point, the reference's exact operation order (_kernels_cy.pyx:17-80).
+// DIV: the scalar Python form (recurrences.py:149) divides by rb[n] where
+// the Cython kernel multiplies by the tabulated reciprocal.
+template <bool DIV>
 __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ rbp,
                                   const double* __restrict__ rbm, const double* __restrict__ rbpi,
                                   const double* __restrict__ rbmi,
@@ -568,7 +571,7 @@ __global__ void k_clenshaw_points(RecTablesDev tab, const double* __restrict__ r
       const double t = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(tab.A[n], xm), u),
                                            __dmul_rn(tab.C[n + 1], d)), coeffs[n]);
       d = __dmul_rn(t, rb[n]);
-      u = __dmul_rn(__dadd_rn(u, d), rbi[n]);
+      u = DIV ? __ddiv_rn(__dadd_rn(u, d), rb[n]) : __dmul_rn(__dadd_rn(u, d), rbi[n]);
     }
     out[i] = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(tab.A[0], xm), u), __dmul_rn(tab.C[1], d)),
                        coeffs[0]);
@@ -928,13 +931,13 @@ int launch_clenshaw_points(const RecTablesDev& tab, const double* rbp, const dou
                            const double* rbpi, const double* rbmi, const double* coeffs,
                            int64_t ldc, const double* x, const double* xm, const int8_t* reg,
                            const int64_t* cut, double* out, int64_t ldo, int64_t npts,
-                           int64_t batch, cudaStream_t st) {
+                           int64_t batch, bool divide, cudaStream_t st) {
   if (npts <= 0 || batch <= 0) return CJT_OK;
   if (batch > 65535) return fail(CJT_EINVAL, "clenshaw batch must be <= 65535 per call");
   const int T = 128;
   dim3 grid((unsigned)((npts + T - 1) / T), (unsigned)batch);
-  k_clenshaw_points<<<grid, T, 0, st>>>(tab, rbp, rbm, rbpi, rbmi, coeffs, ldc, x, xm, reg, cut, out,
-                                        ldo, npts);
+  auto kern = divide ? k_clenshaw_points<true> : k_clenshaw_points<false>;
+  kern<<<grid, T, 0, st>>>(tab, rbp, rbm, rbpi, rbmi, coeffs, ldc, x, xm, reg, cut, out, ldo, npts);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }

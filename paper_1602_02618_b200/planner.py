@@ -566,7 +566,10 @@ def _cost(length: int, n_in: int, n_out: int) -> float:
     if length <= FUSED_MAX:
         fwd, inv = _TILE_COST[max(4096, length)]
         return n_out * length * (fwd * n_in + inv)
-    return length * (18.5 if length <= 1 << 17 else 29.0)
+    # multi-pass: half the per-point cost per FFT; tiled multi-pass runs one
+    # forward FFT per input tile and one inverse FFT per output tile (input
+    # spectra summed, or one forward spectrum shared by the output tiles)
+    return length * (18.5 if length <= 1 << 17 else 29.0) * 0.5 * (n_in + n_out)
 
 
 def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
@@ -592,6 +595,16 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     power-of-two Bluestein, or a grid of on-chip tiles, by measured cost."""
     whole = _next_pow2(width + count - 1)
     best = (_cost(whole, 1, 1), whole, 1, 1)
+    # tiled multi-pass: input tiles (n_out = 1) or output tiles (n_in = 1)
+    lm = 2 * fused_max
+    while lm < whole:
+        for n_in, n_out in [(k, 1) for k in range(2, 9)] + [(1, k) for k in range(2, 9)]:
+            if -(-width // n_in) + -(-count // n_out) - 1 > lm or n_in * n_out * lm > KHAT_MAX_POINTS:
+                continue
+            cost = _cost(lm, n_in, n_out)
+            if cost < best[0]:
+                best = (cost, lm, n_in, n_out)
+        lm *= 2
     lc = 1024
     while lc <= fused_max:
         n_min = -(-width // (lc - 1))

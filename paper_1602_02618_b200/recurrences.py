@@ -7,9 +7,11 @@ Mirrors the reference module ``chebjac.recurrences`` (recurrences.py:1-171):
 and exceptions.  Every evaluation runs in libcjt_b200.so:
 
 * ``jacobi_forward[_reinsch]``  -> ``cjt_jacobi_values`` (k_jacobi_values);
-* ``clenshaw_smith[_reinsch]`` and ``evaluate_expansion`` -> the active kernel
-  backend's ``clenshaw_points`` (the GPU plugin, ``cjt_clenshaw_points``),
-  exactly as the reference dispatches (recurrences.py:150-171);
+* ``clenshaw_smith[_reinsch]`` -> ``cjt_clenshaw_smith_points`` (the scalar
+  helpers' operation order: the Reinsch step divides by rb_n);
+* ``evaluate_expansion`` -> the active kernel backend's ``clenshaw_points``
+  (the GPU plugin, ``cjt_clenshaw_points``), exactly as the reference
+  dispatches (recurrences.py:155-171);
 * ``evaluate_expansion_batched`` -> ``cjt_clenshaw_points_dev`` on CUDA
   tensors (B expansions of one degree at once, stream ordered).
 
@@ -117,21 +119,27 @@ def jacobi_forward_reinsch(p: JacobiParameters, n_max: int, theta: float, end: i
     return _values(t, n_max, theta, end)
 
 
-def _clenshaw_one(p, coeffs, theta, region, tables):
+def _clenshaw_one(p, coeffs, theta, mode, tables):
     coeffs = np.asarray(coeffs, dtype=float)
     if coeffs.ndim != 1:
         raise ValueError("coeffs must be a 1-d sequence")
     if coeffs.size == 0:
-        if region == INTERIOR:
+        if mode == INTERIOR:
             return 0.0   # the reference's empty backward loop returns u1 = 0
         raise IndexError("index 0 is out of bounds for axis 0 with size 0")
     n_max = len(coeffs) - 1
     t = tables if tables is not None else recurrence_tables(p, n_max + 1)
+    A, B, C, rbp, rbm = (_f64(v) for v in (t.A, t.B, t.C, t.rb_plus, t.rb_minus))
+    if min(len(A), len(B), len(C), len(rbp), len(rbm)) < n_max + 2:
+        raise ValueError("recurrence tables are shorter than len(coeffs) + 1")
+    c = _f64(coeffs)
+    th = np.array([theta], dtype=np.float64)
+    md = np.array([mode], dtype=np.int8)
     out = np.empty(1)
-    backend.kernels().clenshaw_points(
-        t.A, t.B, t.C, t.rb_plus, t.rb_minus, t.rb_plus_inv, t.rb_minus_inv, coeffs,
-        np.array([theta], dtype=np.float64), np.array([n_max + 1], dtype=np.int64),
-        np.array([region], dtype=np.int8), out)
+    nat.check(nat.lib().cjt_clenshaw_smith_points(A.ctypes.data, B.ctypes.data, C.ctypes.data,
+                                                  rbp.ctypes.data, rbm.ctypes.data, c.ctypes.data,
+                                                  len(c), th.ctypes.data, md.ctypes.data, 1,
+                                                  out.ctypes.data), "cjt_clenshaw_smith_points")
     return float(out[0])
 
 
