@@ -20,6 +20,7 @@
 // while exposing parallelism; partial sums are reduced in a fixed order
 // (deterministic, no atomics).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 
@@ -109,6 +110,54 @@ __device__ __forceinline__ const double* table_row(const RecTablesDev& t, int r)
 template <int K, int STRIDE, class Store>
 __device__ __forceinline__ void gen_chain(int reg, double xx, const double* tb, int nval, double& s0,
                                           double& s1, const Store& st) {
+  if (nval > K) {
+    // full stage (the common case): no predicates, so each 8-degree chunk's
+    // table reads and chain-independent products are issued ahead of the
+    // chain; the dependency chain is one DFMA (three-term) or two (Reinsch)
+    // per degree instead of a shared-memory load latency per degree
+    constexpr int CH = 8;
+    if (reg == 0) {
+#pragma unroll
+      for (int k0 = 0; k0 < K; k0 += CH) {
+        double t[CH], c[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          t[j] = fma(tb[k0 + j], xx, tb[STRIDE + k0 + j]);
+          c[j] = tb[2 * STRIDE + k0 + j];
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          st(k0 + j, s1);
+          const double pn = fma(t[j], s1, -(c[j] * s0));
+          s0 = s1;
+          s1 = pn;
+        }
+      }
+    } else {
+      const int o = reg > 0 ? 0 : 1;
+      const double* rf = tb + (3 + o) * STRIDE;
+      const double* ap = tb + (5 + o) * STRIDE;
+      const double* cp = tb + (7 + o) * STRIDE;
+#pragma unroll
+      for (int k0 = 0; k0 < K; k0 += CH) {
+        double a[CH], c[CH], r[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          a[j] = ap[k0 + j] * xx;
+          c[j] = cp[k0 + j];
+          r[j] = rf[k0 + j];
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          st(k0 + j, s0);
+          const double d = fma(a[j], s0, c[j] * s1);
+          s0 = fma(r[j], d, r[j] * s0);
+          s1 = d;
+        }
+      }
+    }
+    return;
+  }
   if (reg == 0) {
 #pragma unroll 8
     for (int k = 0; k < K; ++k) {
@@ -253,7 +302,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // consumer stages of slack instead of one.
 template <int VT>
 struct WsCfg {
-  static constexpr int NBUF = VT >= 64 ? 3 : 2;      // stage ring depth (small tiles: occupancy)
+  static constexpr int NBUF = VT == 64 ? 3 : 2;      // P stage ring depth (small tiles: occupancy)
+  // operand-tile ring (c / wv): one deeper than the P ring, so the producers
+  // prefetch the next stage's tile while generating this stage's P (its
+  // global-load latency is hidden behind the recurrence chains)
+  static constexpr int NCB = NBUF + 1;
   static constexpr int NCW = VT == 128 ? 8 : 4;      // consumer warps
   static constexpr int NC = 32 * NCW;
   static constexpr int NP = 128;                     // producer threads
@@ -280,7 +333,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     k_rec_forward_ws(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
                      const double2* __restrict__ ck, const FwdItem* __restrict__ items,
                      const double* __restrict__ c, int64_t ldc, int64_t ncoef, int64_t batch,
-                     double* __restrict__ part) {
+                     double* __restrict__ part, int dbg) {
   using W = WsCfg<VT>;
   constexpr int PT = FWD_ROWS + 4;   // P^T row stride (degrees x rows)
   constexpr int CS = FWD_KS + 4;     // staged c row stride (vectors x degrees)
@@ -288,7 +341,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   double(*Pt)[FWD_KS][PT] = reinterpret_cast<double(*)[FWD_KS][PT]>(smem_rec);
   double(*Cs)[VT][CS] = reinterpret_cast<double(*)[VT][CS]>(smem_rec + W::NBUF * FWD_KS * PT);
   double(*Ts)[REC_WIN_ROWS * FWD_KS] =
-      reinterpret_cast<double(*)[REC_WIN_ROWS * FWD_KS]>(smem_rec + W::NBUF * FWD_KS * PT + W::NBUF * VT * CS);
+      reinterpret_cast<double(*)[REC_WIN_ROWS * FWD_KS]>(smem_rec + W::NBUF * FWD_KS * PT + W::NCB * VT * CS);
   const FwdItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -316,7 +369,19 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
         cp_async8(&Ts[buf][idx], ok ? src + n : src, ok);
       }
     };
+    // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[cb]
+    auto stage_c = [&](int cb, int64_t n0) {
+#pragma unroll
+      for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
+        const int idx = p + q * W::NP;
+        const int v = idx / FWD_KS, k = idx % FWD_KS;
+        const int64_t bb = b0 + v, n = n0 + k;
+        const bool ok = bb < batch && n < ncoef;
+        cp_async8(&Cs[cb][v][k], ok ? c + bb * ldc + n : c, ok);
+      }
+    };
     stage_tables(0, it.n_begin);
+    stage_c(0, it.n_begin);
     cp_async_commit();
     cp_async_wait_all();
     named_sync(BAR_PROD, W::NP);
@@ -324,20 +389,17 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       const int buf = sidx % W::NBUF, tb = sidx & 1;
       const int64_t n0 = it.n_begin + (int64_t)sidx * FWD_KS;
       if (sidx >= W::NBUF) named_sync(BAR_EMPTY + buf, W::NTH);
-      // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[buf]
-#pragma unroll
-      for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
-        const int idx = p + q * W::NP;
-        const int v = idx / FWD_KS, k = idx % FWD_KS;
-        const int64_t bb = b0 + v, n = n0 + k;
-        const bool ok = bb < batch && n < ncoef;
-        cp_async8(&Cs[buf][v][k], ok ? c + bb * ldc + n : c, ok);
+      // next stage's c tile and tables (Cs[(sidx+1) % NCB] was last read by
+      // stage sidx + 1 - NCB = sidx - NBUF, released by the EMPTY wait above)
+      if (sidx + 1 < nstages) {
+        stage_c((sidx + 1) % W::NCB, n0 + FWD_KS);
+        stage_tables(tb ^ 1, n0 + FWD_KS);
       }
-      if (sidx + 1 < nstages) stage_tables(tb ^ 1, n0 + FWD_KS);
       cp_async_commit();
       const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
-      gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1,
-                                [&](int k, double v) { Pt[buf][k][p] = v; });
+      if (dbg != 1)
+        gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1,
+                                  [&](int k, double v) { Pt[buf][k][p] = v; });
       cp_async_wait_all();
       named_sync(BAR_PROD, W::NP);            // next stage's tables visible to all producers
       named_arrive(BAR_FULL + buf, W::NTH);   // P^T and c tile of this stage are ready
@@ -355,15 +417,16 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
     for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int sidx = 0; sidx < nstages; ++sidx) {
-    const int buf = sidx % W::NBUF;
+    const int buf = sidx % W::NBUF, cbuf = sidx % W::NCB;
     named_sync(BAR_FULL + buf, W::NTH);
+    if (dbg != 2)
 #pragma unroll
     for (int kk = 0; kk < FWD_KS / 4; ++kk) {
       double a[4], bf[W::NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Pt[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
 #pragma unroll
-      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Cs[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Cs[cbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -421,7 +484,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
-  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NBUF * VT * WS;   // [REC_WIN_ROWS][SPAN]
+  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NCB * VT * WS;   // [REC_WIN_ROWS][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -437,6 +500,19 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       const double* src = table_row(tab, r);
       cp_async8(&Tw[slot], ok ? src + it.n0 + k : src, ok);
     }
+    // stage the wv tile of row tile tt into Ws[wb]
+    auto stage_wv = [&](int wb, int tt) {
+      const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt] * INV_RT;
+#pragma unroll
+      for (int q = 0; q < (VT * INV_RT) / W::NP; ++q) {
+        const int idx = p + q * W::NP;
+        const int v = idx / INV_RT, k = idx % INV_RT;
+        const int64_t bb = b0 + v, i = r0 + k;
+        const bool ok = bb < batch && i < nrows;
+        cp_async8(&Ws[wb][v][k], ok ? wv + bb * ldw + i : wv, ok);
+      }
+    };
+    stage_wv(0, 0);
     cp_async_commit();
     cp_async_wait_all();
     named_sync(BAR_PROD, W::NP);
@@ -449,15 +525,8 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       GenState g = nxt;
       if (tt + 1 < it.t_count) nxt = gbase[(int64_t)(tt + 1) * 128];   // prefetch
       if (tt >= W::NBUF) named_sync(BAR_EMPTY + buf, W::NTH);
-      const int64_t r0 = (int64_t)tile_ids[it.t_begin + tt] * INV_RT;
-#pragma unroll
-      for (int q = 0; q < (VT * INV_RT) / W::NP; ++q) {
-        const int idx = p + q * W::NP;
-        const int v = idx / INV_RT, k = idx % INV_RT;
-        const int64_t bb = b0 + v, i = r0 + k;
-        const bool ok = bb < batch && i < nrows;
-        cp_async8(&Ws[buf][v][k], ok ? wv + bb * ldw + i : wv, ok);
-      }
+      // next tile's wv (Ws[(tt+1) % NCB] last read at stage tt - NBUF, released above)
+      if (tt + 1 < it.t_count) stage_wv((tt + 1) % W::NCB, tt + 1);
       cp_async_commit();
       const int64_t cut = g.cutreg >> 2;
       const int reg = (int)(g.cutreg & 3) - 1;
@@ -483,7 +552,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
     for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   for (int tt = 0; tt < it.t_count; ++tt) {
-    const int buf = tt % W::NBUF;
+    const int buf = tt % W::NBUF, wbuf = tt % W::NCB;
     named_sync(BAR_FULL + buf, W::NTH);
 #pragma unroll
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
@@ -491,7 +560,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
 #pragma unroll
-      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Ws[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Ws[wbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -796,6 +865,15 @@ int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const in
   return CJT_OK;
 }
 
+// $CJT_WS_DBG (experiments only): 1 = producers skip generation, 2 = consumers skip DMMA
+static int ws_debug() {
+  static const int v = [] {
+    const char* e = getenv("CJT_WS_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const FwdItem* items, int64_t n_items, const double* c,
                        int64_t ldc, int64_t ncoef, int64_t batch, int vt, double* part, cudaStream_t st) {
@@ -805,7 +883,7 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
 #define CJT_FWD(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + R * V * (FWD_KS + 4) + 2 * REC_WIN_ROWS * FWD_KS);  \
+    const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + (R + 1) * V * (FWD_KS + 4) + 2 * REC_WIN_ROWS * FWD_KS);  \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V>,                                     \
@@ -813,7 +891,7 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
       init = true;                                                                               \
     }                                                                                            \
     k_rec_forward_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(rows, tab, ck_off, ck, items, c, ldc, \
-                                                           ncoef, batch, part);                  \
+                                                           ncoef, batch, part, ws_debug());      \
     break;                                                                                       \
   }
     CJT_FWD(128) CJT_FWD(64) CJT_FWD(32) CJT_FWD(16)
@@ -855,7 +933,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + R * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + INV_DT / 32));         \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (R + 1) * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + INV_DT / 32));         \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
