@@ -283,6 +283,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const double* src, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(valid ? 8 : 0));
 }
+// 16-byte async copy global -> shared with zero fill beyond `bytes` (0, 8, 16)
+__device__ __forceinline__ void cp_async16z(void* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
@@ -360,24 +365,43 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       cut = rows.cut[gi];
       if (cut > it.n_begin) load_state(rows, ck_off, ck, gi, it.n_begin, reg, s0, s1);
     }
+    // table window: one 16-byte copy (two degrees) per producer thread
+    // p < 144; the row pointer is fixed per thread
+    // (144 copies: thread p copies chunk p and, for p < 16, chunk p + 128)
+    constexpr int TCH = REC_WIN_ROWS * FWD_KS / 2;
+    static_assert(TCH <= 2 * W::NP, "table window copies");
+    const int tk = 2 * (p % (FWD_KS / 2));
+    const int trow0 = p / (FWD_KS / 2), trow1 = (p + W::NP) / (FWD_KS / 2);
+    const double* tsrc0 = table_row(tab, trow0);
+    const double* tsrc1 = table_row(tab, min(trow1, REC_WIN_ROWS - 1));
     auto stage_tables = [&](int buf, int64_t n0) {
-      for (int idx = p; idx < REC_WIN_ROWS * FWD_KS; idx += W::NP) {
-        const int r = idx / FWD_KS, k = idx % FWD_KS;
-        const int64_t n = n0 + k;
-        const bool ok = n < tab.n_tab;
-        const double* src = table_row(tab, r);
-        cp_async8(&Ts[buf][idx], ok ? src + n : src, ok);
-      }
+      const int64_t n = n0 + tk;
+      const int bytes = n + 1 < tab.n_tab ? 16 : n < tab.n_tab ? 8 : 0;
+      cp_async16z(&Ts[buf][trow0 * FWD_KS + tk], bytes ? tsrc0 + n : tsrc0, bytes);
+      if (p + W::NP < TCH) cp_async16z(&Ts[buf][trow1 * FWD_KS + tk], bytes ? tsrc1 + n : tsrc1, bytes);
     };
-    // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[cb]
+    // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[cb]: 16-byte copies when the
+    // rows are 16-byte aligned (even ldc), else 8-byte copies
+    const bool c16 = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
     auto stage_c = [&](int cb, int64_t n0) {
+      if (c16) {
 #pragma unroll
-      for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
-        const int idx = p + q * W::NP;
-        const int v = idx / FWD_KS, k = idx % FWD_KS;
-        const int64_t bb = b0 + v, n = n0 + k;
-        const bool ok = bb < batch && n < ncoef;
-        cp_async8(&Cs[cb][v][k], ok ? c + bb * ldc + n : c, ok);
+        for (int q = 0; q < (VT * FWD_KS / 2) / W::NP; ++q) {
+          const int idx = p + q * W::NP;
+          const int v = idx / (FWD_KS / 2), k = 2 * (idx % (FWD_KS / 2));
+          const int64_t bb = b0 + v, n = n0 + k;
+          const int bytes = bb >= batch ? 0 : n + 1 < ncoef ? 16 : n < ncoef ? 8 : 0;
+          cp_async16z(&Cs[cb][v][k], bytes ? c + bb * ldc + n : c, bytes);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < (VT * FWD_KS) / W::NP; ++q) {
+          const int idx = p + q * W::NP;
+          const int v = idx / FWD_KS, k = idx % FWD_KS;
+          const int64_t bb = b0 + v, n = n0 + k;
+          const bool ok = bb < batch && n < ncoef;
+          cp_async8(&Cs[cb][v][k], ok ? c + bb * ldc + n : c, ok);
+        }
       }
     };
     stage_tables(0, it.n_begin);
