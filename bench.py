@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (1 warm-up + steps)")
+    ap.add_argument("--profile-stage", default=None,
+                    help="ncu --profile-from-start off: one execution of one stage (fwd_rec, fwd_blocks, "
+                         "fwd_edge, inv_rec, inv_blocks, inv_edge) inside cudaProfilerStart/Stop")
     return ap.parse_args()
 
 
@@ -328,6 +331,18 @@ def run_ours(args, wl):
         step()
     torch.cuda.synchronize(dev)
     launches = fdp.stats().launches_per_execute + idp.stats().launches_per_execute
+    if args.profile_stage:
+        d, sname = args.profile_stage.split("_")
+        mask = {"rec": nat.STAGE_REC, "blocks": nat.STAGE_BLOCKS, "edge": nat.STAGE_EDGE}[sname]
+        dp, src, dst = (fdp, c_dev, cheb) if d == "fwd" else (idp, cheb, back)
+        L = nat.lib()
+        nat.check(L.cjt_execute_stage(dp.handle, src.data_ptr(), dst.data_ptr(), batch, mask, stream.cuda_stream))
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.start()
+        nat.check(L.cjt_execute_stage(dp.handle, src.data_ptr(), dst.data_ptr(), batch, mask, stream.cuda_stream))
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.stop()
+        return
 
     def timed(fn, k):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
@@ -345,8 +360,35 @@ def run_ours(args, wl):
             dist.barrier()
         return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
+    # one step captured into a CUDA graph (stream-ordered, allocation-free
+    # executes), replayed per timed step: launch overhead off the small configs
+    graph = None
+    if not os.environ.get("CJT_BENCH_NO_GRAPH"):
+        try:
+            # capture on a stream whose per-stream plan workspaces exist
+            # (warmed up eagerly first; nothing is allocated while capturing)
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(gs):
+                step()
+            gs.synchronize()
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_, stream=gs):
+                step()
+            g_.replay()
+            torch.cuda.synchronize(dev)
+            graph = g_
+        except RuntimeError:
+            graph = None
+            torch.cuda.synchronize(dev)
+    run_step = graph.replay if graph is not None else step
+    for _ in range(2):
+        run_step()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+
     with ClockSampler(local) as clk:
-        step_ms = timed(step, args.steps)
+        step_ms = timed(run_step, args.steps)
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -408,11 +450,13 @@ def run_ours(args, wl):
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(dom)
-        except (ValueError, OSError):
+            t_ = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
+            traffic = None if t_ is None else t_["bytes"]   # DRAM bytes of one stage execution (ncu)
+        except (ValueError, OSError, KeyError, TypeError):
             traffic = None
     roofline = {"bound": "fp64", "kernel": kern, "stage": dom, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                "traffic_note": "ncu dram__bytes_read+write of one execution of this stage (profiles/ncu_traffic.json)",
                 "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains)",
                 "nominal_peak": NOMINAL_FP64_TFLOPS, "flops_model": unit_note,
                 "stage_ms": {k: round(v, 4) for k, v in stages.items()},
@@ -460,7 +504,7 @@ def run_ours(args, wl):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md 8(d))",
-            "config": config_json(wl, args.config, batch, world, "weak"),
+            "config": dict(config_json(wl, args.config, batch, world, "weak"), cuda_graph=graph is not None),
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roofline,
             "cpu_baseline": cpu, "e2e": e2e, "parity_check_vector0": chk,
         }

@@ -264,15 +264,18 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (lg >= 14 && !cluster) {
     // on-chip rows (two-level FFT) and short columns: wide,
     // coalesced column tiles (E / L1 columns) in passes 1 and 3
-    // rows: 8192 points (1 CTA/SM) while the columns stay short (<= 16
-    // points, register passes); from 2^20 on, 4096-point rows at 2 CTAs/SM
-    // overlap their HBM and FFT phases and win despite longer columns
-    // (config-4 launch lists).  $CJT_MP_L2MAX (experiments) caps the row length.
+    // rows: 8192 points (1 CTA/SM) only for 2^14 / 2^15 (columns of 2 / 4
+    // points would be too short otherwise); from 2^16 on, 4096-point rows at
+    // 2 CTAs/SM overlap their HBM and FFT phases and win despite longer
+    // columns.  $CJT_MP_L2MAX (experiments) caps the row length.
     static const int l2max = [] {
       const char* e = getenv("CJT_MP_L2MAX");
       return e ? std::max(10, std::min(13, atoi(e))) : 13;
     }();
-    const int l2 = std::min({l2max, lg - 4, lg >= 20 ? 12 : 13});
+    // (8192-point rows only while the columns would otherwise fall below 16
+    // points: 4096-point rows at 2 CTAs/SM win for 2^16 .. 2^19 too, config-4/5
+    // A/B with CJT_MP_L2MAX: 58.9 -> 57.8 ms, 159.4 -> 155.5 ms)
+    const int l2 = std::min({l2max, lg - 4, lg >= 16 ? 12 : 13});
     const int l1 = lg - l2;
     cz.log1 = l1;
     cz.log2 = l2;
