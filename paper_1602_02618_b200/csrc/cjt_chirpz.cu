@@ -520,7 +520,7 @@ __device__ __forceinline__ void column_twiddles(const ChirpZDev& cz, int64_t n2,
 }
 
 template <int LOG1>
-__global__ void __launch_bounds__(COLR_T)
+__global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
     k_chirpz_cols_fwd_reg(ChirpZDev cz, const double* __restrict__ x, int64_t ldx,
                           double2* __restrict__ buf) {
   constexpr int L1 = 1 << LOG1;
@@ -528,8 +528,12 @@ __global__ void __launch_bounds__(COLR_T)
   const int64_t L = cz.length;
   const int64_t n2 = (int64_t)blockIdx.y * COLR_T + threadIdx.x;
   const int64_t b = blockIdx.x;
-  // input tile blockIdx.z (tiled multi-pass): x[to .. to + tn) -> slot blockIdx.z
-  const int64_t to = __ldg(cz.tin + 2 * blockIdx.z), tn = __ldg(cz.tin + 2 * blockIdx.z + 1);
+  // blockIdx.z = (input tile, term): x[to .. to + tn) * pre_m -> slot (m, tile);
+  // one term per thread keeps the kernel at 4 CTAs / SM (x and the twiddles
+  // are re-read / recomputed per term from L2 instead of held for all terms)
+  const int m = (int)(blockIdx.z % cz.m_count);
+  const int tile = (int)(blockIdx.z / cz.m_count);
+  const int64_t to = __ldg(cz.tin + 2 * tile), tn = __ldg(cz.tin + 2 * tile + 1);
   const int nslot = max(cz.n_in, cz.n_out);
   const double* xb = x + b * ldx + cz.p0 + to;
   double xv[L1];
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(COLR_T)
   }
   double2 w[L1];
   column_twiddles<L1>(cz, n2, w);
-  for (int m = 0; m < cz.m_count; ++m) {
+  {
     const double2* pre = cz.pre + (int64_t)m * cz.width + to;
     double2 v[L1];
 #pragma unroll
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(COLR_T)
       v[r] = make_double2(xv[r] * p.x, xv[r] * p.y);
     }
     dft_reg<L1, -1>(v);
-    double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L + n2;
+    double2* bm = buf + ((b * cz.m_count + m) * nslot + tile) * L + n2;
 #pragma unroll
     for (int k = 0; k < L1; ++k) bm[k * L2] = cmul(v[k], w[k]);
   }
@@ -906,7 +910,7 @@ int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_
   }
   const int64_t L2 = (int64_t)1 << cz.log2;
   if constexpr (LOG1 <= 5) {
-    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)cz.n_in);
+    dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)(cz.n_in * cz.m_count));
     k_chirpz_cols_fwd_reg<LOG1><<<grid, COLR_T, 0, st>>>(cz, x, ldx, buf);
     CJT_CUDA_TRY(cudaGetLastError());
     return CJT_OK;
