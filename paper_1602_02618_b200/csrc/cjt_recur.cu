@@ -918,7 +918,7 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
                                                            ncoef, batch, part, ws_debug());      \
     break;                                                                                       \
   }
-    CJT_FWD(128) CJT_FWD(64) CJT_FWD(32) CJT_FWD(16)
+    CJT_FWD(128) CJT_FWD(64) CJT_FWD(32) CJT_FWD(24) CJT_FWD(16)
 #undef CJT_FWD
     default: return fail(CJT_EINVAL, "bad vector tile");
   }
@@ -968,7 +968,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
                                                            ldw, batch, part);                    \
     break;                                                                                       \
   }
-    CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(16)
+    CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(24) CJT_INV(16)
 #undef CJT_INV
     default: return fail(CJT_EINVAL, "bad vector tile");
   }

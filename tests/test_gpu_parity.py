@@ -46,9 +46,9 @@ def test_golden_single_vector_api(cuda, name):
     assert O.parity(i.data, g["inv"][0], g["fwd"][0]) <= TOL
 
 
-@pytest.mark.parametrize("batch", [1, 17, 40, 70, 129, 300])
+@pytest.mark.parametrize("batch", [1, 17, 24, 30, 40, 70, 129, 300])
 def test_batch_tiles_vs_oracle(cuda, batch):
-    """Every vector-tile width (16/32/64) and ragged batch tails."""
+    """Every vector-tile width (16/24/32/64/128) and ragged batch tails."""
     import torch
     a, b, n = 0.25, -0.2, 1023
     p = cj.JacobiParameters(a, b)
@@ -61,3 +61,22 @@ def test_batch_tiles_vs_oracle(cuda, batch):
         ri = O.oracle_inverse(a, b, f[v])
         assert O.parity(f[v], rf, c[v]) <= TOL
         assert O.parity(i[v], ri, f[v]) <= TOL
+
+
+@pytest.mark.parametrize("batch", [20, 28])
+def test_vector_tile_width_invariance(cuda, batch):
+    """A vector's result does not depend on the tile width it ran in (24 / 32
+    vs 16): the contraction order per output element is the same."""
+    import torch
+    a, b, n = 0.5, 0.5, 1023      # pure recurrence: K = 0
+    p = cj.JacobiParameters(a, b)
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = torch.from_numpy(np.stack([O.seeded_vector(3, v, n) for v in range(batch)])).to(cuda)
+    f = cj.forward_batched(fp, c)
+    i = cj.inverse_batched(ip, f)
+    f1 = cj.forward_batched(fp, c[:8].contiguous())
+    i1 = cj.inverse_batched(ip, f[:8].contiguous())
+    torch.cuda.synchronize()
+    scale = float(c[:8].abs().sum(dim=1).max())
+    assert float((f[:8] - f1).abs().max()) <= 1e-15 * scale
+    assert float((i[:8] - i1).abs().max()) <= 1e-15 * scale
