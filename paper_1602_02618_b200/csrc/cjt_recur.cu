@@ -305,6 +305,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // On B200 DMMA and DMUL/DADD share the fp64 datapath, so the generators'
 // serial chains are slowed by the consumers' DMMAs; NBUF = 3 gives them two
 // consumer stages of slack instead of one.
+#ifndef CJT_NCW8_MIN
+#define CJT_NCW8_MIN 128
+#endif
 template <int VT>
 struct WsCfg {
   static constexpr int NBUF = VT == 64 ? 3 : 2;      // P stage ring depth (small tiles: occupancy)
@@ -312,7 +315,7 @@ struct WsCfg {
   // prefetch the next stage's tile while generating this stage's P (its
   // global-load latency is hidden behind the recurrence chains)
   static constexpr int NCB = NBUF + 1;
-  static constexpr int NCW = VT == 128 ? 8 : 4;      // consumer warps
+  static constexpr int NCW = VT >= CJT_NCW8_MIN ? 8 : 4;   // consumer warps
   static constexpr int NC = 32 * NCW;
   static constexpr int NP = 128;                     // producer threads
   static constexpr int NTH = NC + NP;
