@@ -600,6 +600,12 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
   }
 }
 
+// row FFT twiddles from a 1024-entry shared-memory table (TwSmem) instead
+// of the 8192-entry global table: the global table's scattered per-lane
+// loads cost L1 sectors the row kernels are short of
+#ifndef CJT_ROWS_TWSMEM
+#define CJT_ROWS_TWSMEM 1
+#endif
 template <int LOG2>
 struct RowCfg {
   static constexpr int L2 = 1 << LOG2;
@@ -608,7 +614,10 @@ struct RowCfg {
   static constexpr int E = (L2 >= 4096) ? L2 : 4096;
   static constexpr int NR = E / L2;
   static constexpr int T = E / EPT;
-  static constexpr int SMEM = NR * padded_len(L2) * 16;
+  // (4096 / 8192-point rows only: A/B on configs 2, 4, 5 -- the 1024 / 2048
+  // rows of config 2 lose ~1.5 %, the longer rows of configs 4 / 5 gain 1-3 %)
+  static constexpr bool TWS = CJT_ROWS_TWSMEM && LOG2 >= 12;
+  static constexpr int SMEM = NR * padded_len(L2) * 16 + (TWS ? 1024 * 16 : 0);
 };
 
 // pass 2: rows k1 of buf: FFT over n2 -> * khat[k1][k2] -> inverse FFT over k2
@@ -621,15 +630,29 @@ struct RowCfg {
 //                 owned by one thread), one inverse FFT -> slot 0;
 //   output tiles: one forward FFT, its spectrum kept in slot n_out-1; per
 //                 output tile j, spectrum * khat_j -> inverse FFT -> slot j.
+template <int LOG2, int TM, class TW>
+__device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* __restrict__ buf,
+                                          double2* smem);
+
 // TM (tiling mode): 0 untiled, 1 input tiles, 2 output tiles (separate
 // instantiations keep the untiled kernel's register allocation unchanged)
 template <int LOG2, int TM>
 __global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
-    k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ tw, double2* __restrict__ buf) {
+    k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ twg, double2* __restrict__ buf) {
+  using Cfg = RowCfg<LOG2>;
+  extern __shared__ double2 smem[];
+  if constexpr (Cfg::TWS)
+    rows_impl<LOG2, TM>(cz, tw_smem_init(smem + Cfg::NR * padded_len(Cfg::L2), twg), buf, smem);
+  else
+    rows_impl<LOG2, TM>(cz, twg, buf, smem);
+}
+
+template <int LOG2, int TM, class TW>
+__device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* __restrict__ buf,
+                                          double2* smem) {
   using Cfg = RowCfg<LOG2>;
   constexpr int L2 = Cfg::L2, NR = Cfg::NR;
   constexpr int TPG = L2 / Cfg::EPT;
-  extern __shared__ double2 smem[];
   const int grp = threadIdx.x / TPG;
   const int t = threadIdx.x % TPG;
   // consecutive CTAs share spectrum rows across (vector, term): khat stays in L2
