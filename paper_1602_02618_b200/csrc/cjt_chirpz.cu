@@ -433,6 +433,10 @@ __global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
   }
 }
 
+// column FFT twiddles from the shared-memory table (see CJT_ROWS_TWSMEM)
+#ifndef CJT_COLS_TWSMEM
+#define CJT_COLS_TWSMEM 1
+#endif
 template <int LOG1>
 struct ColCfg {
   static constexpr int L1 = 1 << LOG1;
@@ -440,17 +444,22 @@ struct ColCfg {
   static constexpr int NC = E / L1;                  // columns per CTA
   static constexpr int T = E / 16;
   static constexpr int CS = padded_len(L1) + 1;      // odd column stride (conflict-free transpose)
-  static constexpr int SMEM = NC * CS * 16;
+  static constexpr int SMEM = NC * CS * 16 + (CJT_COLS_TWSMEM ? 1024 * 16 : 0);
 };
 
 // pass 1: x (real slice) * pre_m -> column FFTs over n1 -> * W_L^{n2 k1} -> buf[b][m][k1][n2]
 template <int LOG1>
 __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
-    k_chirpz_cols_fwd(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
+    k_chirpz_cols_fwd(ChirpZDev cz, const double2* __restrict__ twg, const double* __restrict__ x,
                       int64_t ldx, double2* __restrict__ buf) {
   using Cfg = ColCfg<LOG1>;
   constexpr int L1 = Cfg::L1, NC = Cfg::NC, T = Cfg::T, CS = Cfg::CS;
   extern __shared__ double2 smem[];
+#if CJT_COLS_TWSMEM
+  const TwSmem tw = tw_smem_init(smem + NC * CS, twg);
+#else
+  const double2* tw = twg;
+#endif
   const int64_t L2 = (int64_t)1 << cz.log2;
   const int64_t L = cz.length;
   // consecutive CTAs share a column tile across vectors: the pre table stays in L2
@@ -769,11 +778,16 @@ __device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* _
 // pass 3: columns n2: * W_L^{-n2 k1} -> inverse FFT over k1 -> sum_m Re(post_m * y) -> out
 template <int LOG1>
 __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
-    k_chirpz_cols_inv(ChirpZDev cz, const double2* __restrict__ tw,
+    k_chirpz_cols_inv(ChirpZDev cz, const double2* __restrict__ twg,
                       const double2* __restrict__ buf, double* __restrict__ out, int64_t ldo) {
   using Cfg = ColCfg<LOG1>;
   constexpr int L1 = Cfg::L1, NC = Cfg::NC, T = Cfg::T, CS = Cfg::CS;
   extern __shared__ double2 smem[];
+#if CJT_COLS_TWSMEM
+  const TwSmem tw = tw_smem_init(smem + NC * CS, twg);
+#else
+  const double2* tw = twg;
+#endif
   const int64_t L2 = (int64_t)1 << cz.log2;
   const int64_t L = cz.length;
   const int64_t c0 = (int64_t)blockIdx.y * NC;
