@@ -290,6 +290,8 @@ __device__ __forceinline__ void cp_async16z(void* dst, const double* src, int by
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Warp-specialised DMMA contractions (K1, K2).
 //   consumers: NCW warps, 4 along M (32 rows/degrees each) x NCW/4 along N,
@@ -418,16 +420,19 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       if (sidx >= W::NBUF) named_sync(BAR_EMPTY + buf, W::NTH);
       // next stage's c tile and tables (Cs[(sidx+1) % NCB] was last read by
       // stage sidx + 1 - NCB = sidx - NBUF, released by the EMPTY wait above)
-      if (sidx + 1 < nstages) {
-        stage_c((sidx + 1) % W::NCB, n0 + FWD_KS);
-        stage_tables(tb ^ 1, n0 + FWD_KS);
-      }
+      // (two groups: the tables, needed by the producers at the next stage,
+      // then the c tile, needed by the consumers one stage later still)
+      if (sidx + 1 < nstages) stage_tables(tb ^ 1, n0 + FWD_KS);
+      cp_async_commit();
+      if (sidx + 1 < nstages) stage_c((sidx + 1) % W::NCB, n0 + FWD_KS);
       cp_async_commit();
       const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
       if (dbg != 1)
         gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1,
                                   [&](int k, double v) { Pt[buf][k][p] = v; });
-      cp_async_wait_all();
+      // next stage's tables and this stage's c tile landed; the next c tile
+      // (newest group) may stay in flight
+      cp_async_wait<1>();
       named_sync(BAR_PROD, W::NP);            // next stage's tables visible to all producers
       named_arrive(BAR_FULL + buf, W::NTH);   // P^T and c tile of this stage are ready
     }
@@ -500,14 +505,14 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     k_rec_inverse_ws(RecTablesDev tab, const GenState* __restrict__ gen, int64_t nrows,
                      const InvItem* __restrict__ items, const int32_t* __restrict__ tile_ids,
                      const double* __restrict__ wv, int64_t ldw, int64_t batch,
-                     double* __restrict__ part) {
+                     double* __restrict__ part, int dbg) {
   using W = WsCfg<VT>;
   constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
   constexpr int WS = INV_RT + 4;
   constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
-  // window row stride with one pad slot per 32 degrees: the four producer
-  // chunks of a warp (degrees 32 q + k) then read four different banks
-  constexpr int SPANP = SPAN + SPAN / 32;
+  // window row stride with two pad slots per 32 degrees: chunk gq starts at slot 34 gq -- 16-byte
+  // aligned (vector table loads) and in bank pair 2 gq (conflict-free)
+  constexpr int SPANP = SPAN + 2 * (SPAN / 32);
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     const int grow = p >> 2, gq = p & 3;
     for (int idx = p; idx < REC_WIN_ROWS * SPAN; idx += W::NP) {
       const int r = idx / SPAN, k = idx % SPAN;
-      const int slot = r * SPANP + k + (k >> 5);
+      const int slot = r * SPANP + k + 2 * (k >> 5);
       const bool ok = it.n0 + k < tab.n_tab;
       const double* src = table_row(tab, r);
       cp_async8(&Tw[slot], ok ? src + it.n0 + k : src, ok);
@@ -559,10 +564,13 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       const int reg = (int)(g.cutreg & 3) - 1;
       double* dst = &Ps[buf][grow][CK * gq + gq];
       const int nval = (int)max((int64_t)0, min((int64_t)CK + 1, cut - nstart));
-      // this chunk's window: degrees nl0 + k at slot nl0 + k + gq (pad per 32)
-      gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + gq, nval, g.s0, g.s1,
-                           [&](int k, double v) { dst[k] = v; });
-      cp_async_wait_all();
+      // this chunk's window: degrees nl0 + k at slot nl0 + k + 2 gq (pads per 32)
+      if (dbg != 1)
+        gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + 2 * gq, nval, g.s0, g.s1,
+                             [&](int k, double v) { dst[k] = v; });
+      // this stage's wv tile (committed one iteration ago) must have landed;
+      // the next tile's copies (newest group) may stay in flight
+      cp_async_wait<1>();
       named_arrive(BAR_FULL + buf, W::NTH);
     }
     return;
@@ -581,6 +589,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   for (int tt = 0; tt < it.t_count; ++tt) {
     const int buf = tt % W::NBUF, wbuf = tt % W::NCB;
     named_sync(BAR_FULL + buf, W::NTH);
+    if (dbg != 2)
 #pragma unroll
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
       double a[4], bf[W::NT];
@@ -775,8 +784,6 @@ __global__ void __launch_bounds__(128)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
 }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // A block in global memory: AMK = false -> [k 32][m 128] (forward P^T),
 // AMK = true -> [m 128][k 32] (inverse P transposed for coalesced generation);
@@ -960,7 +967,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 #define CJT_INV(V)                                                                               \
   case V: {                                                                                      \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (R + 1) * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + INV_DT / 32));         \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (R + 1) * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + 2 * (INV_DT / 32)));   \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
@@ -968,7 +975,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
       init = true;                                                                               \
     }                                                                                            \
     k_rec_inverse_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(tab, g, nrows, items, tile_ids, wv,   \
-                                                           ldw, batch, part);                    \
+                                                           ldw, batch, part, ws_debug());      \
     break;                                                                                       \
   }
     CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(24) CJT_INV(16)

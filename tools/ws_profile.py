@@ -1,4 +1,5 @@
-"""One forward recurrence stage (K1, VT=16) of (1/2, 1/2), N=32767, for ncu."""
+"""One recurrence stage (K1 or K2, VT=16) of (1/2, 1/2), N=32767, for ncu.
+    python tools/ws_profile.py [forward|inverse]"""
 import sys
 from pathlib import Path
 
@@ -11,9 +12,10 @@ from paper_1602_02618_b200 import _native as nat  # noqa: E402
 
 n, B = 32767, 16
 p = cj.JacobiParameters(0.5, 0.5)
-fp = cj.plan("forward", p, n)
+direction = sys.argv[1] if len(sys.argv) > 1 else "forward"
+fp = cj.plan(direction, p, n)
 x = torch.randn(B, n + 1, dtype=torch.float64, device="cuda")
-y = cj.forward_batched(fp, x)
+y = (cj.forward_batched if direction == "forward" else cj.inverse_batched)(fp, x)
 dp = fp.device_plan(0)
 st = torch.cuda.current_stream().cuda_stream
 torch.cuda.synchronize()
