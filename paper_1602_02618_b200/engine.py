@@ -313,14 +313,23 @@ def inverse_batched(tp: TransformPlan, c, out=None, check_finite: bool = True, s
 _PIPE_CACHE: dict = {}
 
 
+_PIPE_NEXT = {}
+
+
 def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: int = 2,
-             device: int | None = None):
+             device: int | None = None, sync: bool = True):
     """Apply `plans` in sequence (e.g. ``(forward_plan, inverse_plan)``) to a
     (B, N+1) float64 host array, with host<->device copies overlapped with the
     transforms: the batch is cut into chunks that alternate between `streams`
     CUDA streams (H2D of chunk k+1 and D2H of chunk k-1 run under chunk k's
     kernels).  Pinned host memory (e.g. ``torch.empty(..., pin_memory=True)``)
-    is required for the copies to be asynchronous.  Returns host_out."""
+    is required for the copies to be asynchronous.  Returns host_out.
+
+    ``sync=False`` returns as soon as the work is enqueued (host_out is valid
+    after ``torch.cuda.synchronize()``); consecutive calls then continue the
+    stream rotation, so one call's copies overlap the neighbouring calls'
+    transforms (streaming many batches through the GPU).  The caller must
+    not modify host_in / read host_out of a call before synchronizing."""
     import torch
     if not plans:
         raise ValueError("no plans")
@@ -339,7 +348,7 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
     batch = hin.shape[0]
     chunk = batch if chunk is None else max(1, min(int(chunk), batch))
     dev = torch.device("cuda", _current_device() if device is None else device)
-    nstreams = max(1, min(streams, -(-batch // chunk)))
+    nstreams = max(1, min(streams, -(-batch // chunk))) if sync else max(1, streams)
     # streams and device buffers are cached: plan workspaces are per stream, so
     # fresh streams would re-allocate them on every call
     key = (dev.index, nstreams, chunk, n1)
@@ -353,7 +362,8 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
     cur = torch.cuda.current_stream(dev)
     for s in ss:
         s.wait_stream(cur)
-    for k, r0 in enumerate(range(0, batch, chunk)):
+    k0 = _PIPE_NEXT.get(key, 0) if not sync else 0
+    for k, r0 in enumerate(range(0, batch, chunk), start=k0):
         r1 = min(batch, r0 + chunk)
         s = ss[k % nstreams]
         a, b = bufs[k % nstreams]
@@ -364,6 +374,9 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
                 _execute_batched(tp, src, out=dst, check_finite=False)
                 src, dst = dst, src
             hout[r0:r1].copy_(src, non_blocking=True)
+    if not sync:
+        _PIPE_NEXT[key] = (k0 + -(-batch // chunk)) % nstreams
+        return host_out
     for s in ss:
         cur.wait_stream(s)
     torch.cuda.synchronize(dev)

@@ -216,3 +216,20 @@ def test_pipeline_and_concurrent_streams(cuda):
     # rounding (same-batch re-execution is bitwise, test_reexecution_bit_identical)
     diff = (torch.cat([y1, y2]) - whole).abs().max(dim=1).values
     assert float((diff / x.abs().sum(dim=1)).max()) <= 1e-15
+
+
+def test_pipeline_streamed_calls(cuda):
+    """pipeline(sync=False): several batches streamed through two CUDA
+    streams give the same results as synchronous calls."""
+    import torch
+    a, b, n = 0.3, -0.45, 2047
+    p = cj.JacobiParameters(a, b)
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    batches = [np.stack([O.seeded_vector(4, 16 * k + v, n) for v in range(16)]) for k in range(3)]
+    pins = [torch.from_numpy(c).pin_memory() for c in batches]
+    outs = [torch.empty_like(x).pin_memory() for x in pins]
+    for x, y in zip(pins, outs):
+        cj.pipeline((fp, ip), x, y, streams=2, sync=False)
+    torch.cuda.synchronize()
+    for x, y in zip(pins, outs):
+        assert torch.equal(y, cj.pipeline((fp, ip), x, streams=2))
