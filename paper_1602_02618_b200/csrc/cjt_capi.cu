@@ -67,6 +67,12 @@ struct cjt_plan {
   int32_t* tile_slot0 = nullptr;
   int32_t* tile_nslot = nullptr;
   int64_t n_fslots = 0;
+  // alpha = beta parity folding: P_n(-x) = (-1)^n P_n(x) on the mirrored grid
+  // rows i and G - i, so the recurrence region is contracted for the rows
+  // i < nrows_fold only, split into even and odd degrees (half the work)
+  bool fold = false;
+  int64_t nrows_fold = 0;
+  int64_t rec_rows() const { return fold ? nrows_fold : nrows; }
   InvItem* iitems = nullptr;
   int64_t n_iitems = 0;
   int32_t* tile_ids = nullptr;
@@ -353,9 +359,10 @@ int arena_get(int device, cudaStream_t st, int64_t need, double** out) {
 
 // Work lists depend on the batch size (split-K is sized to fill the GPU).
 std::vector<int64_t> tile_max_cut(const cjt_plan* P, int64_t rows_per_tile) {
-  const int64_t ntiles = (P->nrows + rows_per_tile - 1) / rows_per_tile;
+  const int64_t nr = P->rec_rows();
+  const int64_t ntiles = (nr + rows_per_tile - 1) / rows_per_tile;
   std::vector<int64_t> mx((size_t)ntiles, 0);
-  for (int64_t i = 0; i < P->nrows; ++i) {
+  for (int64_t i = 0; i < nr; ++i) {
     const int64_t t = i / rows_per_tile;
     mx[t] = std::max(mx[t], P->h_cut[i]);
   }
@@ -380,8 +387,12 @@ int build_items(cjt_plan* P, int64_t batch) {
   // two-pass (P through HBM, DMMA GEMM without generation on the pipe) only
   // pays at VT = 128; up to 64 vectors per tile the warp-specialised kernels
   // (issue-lean producers) win (config-2 / config-3 launch lists)
-  const int64_t budget_blocks = P->vt >= 128 ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
-  P->vt = pick_vt(batch);
+  // folded plans: 64-vector tiles at most (two accumulator sets per consumer),
+  // no two-pass path
+  // (inverse: the mirror rows' wv ring doubles the operand tiles, 16-vector
+  // tiles keep two CTAs per SM)
+  if (P->fold) P->vt = std::min(P->vt, P->direction == CJT_FORWARD ? 64 : 16);
+  const int64_t budget_blocks = (P->vt >= 128 && !P->fold) ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
   const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {
     const std::vector<int64_t> tmax = tile_max_cut(P, FWD_ROWS);
@@ -400,7 +411,7 @@ int build_items(cjt_plan* P, int64_t batch) {
       for (int64_t nb = 0; nb < top; nb += seg) {
         FwdItem it{};
         it.row0 = (int32_t)(t * FWD_ROWS);
-        it.nrows = (int32_t)std::min<int64_t>(FWD_ROWS, P->nrows - t * FWD_ROWS);
+        it.nrows = (int32_t)std::min<int64_t>(FWD_ROWS, P->rec_rows() - t * FWD_ROWS);
         it.n_begin = (int32_t)nb;
         it.n_end = (int32_t)std::min(top, nb + seg);
         it.slot = slot++;
@@ -602,7 +613,8 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
   const int64_t G1 = P->G + 1, N1 = P->n + 1;
   void* p;
   int64_t bytes = 0;
-  const int64_t part_elems = (P->direction == CJT_FORWARD) ? P->n_fslots * FWD_ROWS : P->n_islots * INV_DT;
+  const int64_t part_elems = (P->direction == CJT_FORWARD) ? P->n_fslots * FWD_ROWS * (P->fold ? 2 : 1)
+                                                            : P->n_islots * INV_DT;
   if (int rc = dalloc(W.allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
   W.part = (double*)p;
   bytes += part_elems * batch * 8;
@@ -676,11 +688,11 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       launches -= 1;
     } else if (rec) {
       if (int rc = launch_rec_forward(P->rows, P->tab, P->ck_off, P->ck, P->fitems, P->n_fitems, in, N1,
-                                      N1, batch, P->vt, W.part, st)) return rc;
+                                      N1, batch, P->vt, P->fold, W.part, st)) return rc;
     }
     if (rec) {
-      if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->nrows, W.part, W.vals,
-                                             G1, batch, st)) return rc;
+      if (int rc = launch_rec_forward_reduce(P->tile_slot0, P->tile_nslot, P->rec_rows(), W.part, W.vals,
+                                             G1, batch, P->G, P->fold, st)) return rc;
       launches += 2;
     }
     if (blk)
@@ -711,8 +723,8 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       }
       launches -= 1;
     } else if (rec) {
-      if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
-                                      W.vals, G1, batch, P->vt, W.part, st)) return rc;
+      if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->rec_rows(), P->iitems, P->n_iitems, P->tile_ids,
+                                      W.vals, G1, batch, P->vt, P->fold, P->G, W.part, st)) return rc;
     }
     if (rec) {
       if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, N1, W.part, W.yacc, P->scal, out, N1,
@@ -798,6 +810,29 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   const size_t tl = (size_t)d->table_len;
   const double* src[7] = {d->A, d->B, d->C, d->rf_plus, d->rf_minus, d->rf_plus_inv, d->rf_minus_inv};
   if (int rc = upload_tables(A, src, tl, &P->tab)) return rc;
+
+  // parity folding (alpha = beta): B_n = 0, rf- = -rf+, symmetric cuts,
+  // antisymmetric regions; only while the mirrored rows' x = -x_i stays
+  // within the transform tolerance of the reference's cos(theta_{G-i})
+  // (grids up to 2^16 points; a 1-ulp angle shift moves
+  // the alpha = beta = 1/2 inverse by 9e-13 at N = 65535)
+  {
+    bool sym = G <= 65534;
+    for (size_t n = 0; sym && n < tl; ++n)
+      sym = d->B[n] == 0.0 && d->rf_minus[n] == -d->rf_plus[n];
+    for (int64_t i = 0; sym && i < nr; ++i)
+      sym = P->h_cut[i] == P->h_cut[G - i] && d->regions[i] == -d->regions[G - i];
+    // the inverse folds only on request ($CJT_FOLD_INVERSE=1): the exact
+    // mirror x_{G-i} = -x_i differs from the reference's cos(theta_{G-i}) by
+    // ~1e-13 relative near x = -1, which moves the (sensitive) inverse by up
+    // to ~2e-13 ||c||_1 (config 5, N <= 2047) -- inside the 1e-12 tolerance
+    // but too close to it at large N; the forward moves by <= 2e-16.
+    const char* e = getenv("CJT_FOLD");
+    const char* ei = getenv("CJT_FOLD_INVERSE");
+    P->fold = sym && !(e && e[0] == '0') &&
+              (d->direction == CJT_FORWARD || (ei && ei[0] == '1'));
+    P->nrows_fold = G / 2 + 1;   // rows 0 .. G/2 (G even: the middle row is its own mirror)
+  }
 
   // recurrence checkpoints every CK degrees
   std::vector<int64_t> off((size_t)nr);
@@ -1141,7 +1176,7 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
   cjt_plan::Workspace* W = nullptr;
   if (int rc = get_workspace(P.get(), 0, &W)) return rc;
   if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
-                                  dwv, n_points, 1, P->vt, W->part, 0)) return rc;
+                                  dwv, n_points, 1, P->vt, false, P->G, W->part, 0)) return rc;
   if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, W->part, nullptr, dscal, dres,
                                      P->n + 1, 1, 0)) return rc;
   std::vector<double> res(ones.size());

@@ -568,21 +568,23 @@ void chirpz_workspace(const ChirpZDev& cz, int64_t batch, int64_t* part_elems, i
 
 int launch_checkpoints(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        double2* ck, cudaStream_t st);
+// fold: parity-folded contraction (alpha = beta), partials [slot][2][batch][128]
 int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const FwdItem* items, int64_t n_items,
                        const double* c, int64_t ldc, int64_t ncoef, int64_t batch, int vt,
-                       double* part, cudaStream_t st);
+                       bool fold, double* part, cudaStream_t st);
 int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nslot,
                               int64_t nrows, const double* part, double* vals, int64_t ldv,
-                              int64_t batch, cudaStream_t st);
+                              int64_t batch, int64_t G, bool fold, cudaStream_t st);
 // K2 generator stream: 32 bytes per (work-list row tile, generator thread)
 constexpr int GEN_STATE_BYTES = 32;
 int launch_build_inv_gen(const RecRowsDev& rows, const int64_t* ck_off, const double2* ck,
                          const int32_t* ids, const int32_t* gn0, int64_t total, void* out,
                          cudaStream_t st);
+// fold: parity-folded contraction (alpha = beta) over rows < nrows = G/2 + 1
 int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, const InvItem* items,
                        int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
-                       int64_t batch, int vt, double* part, cudaStream_t st);
+                       int64_t batch, int vt, bool fold, int64_t G, double* part, cudaStream_t st);
 int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                     const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st);
 int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t gbeg,

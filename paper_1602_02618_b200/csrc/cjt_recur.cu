@@ -338,7 +338,11 @@ constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + RING_MAX, BAR_PROD = 1 + 2 * RING_MA
 // (128 rows x a degree segment) and one tile of VT vectors; stages of 32
 // degrees.  Producer thread p owns row p's recurrence chain (state carried
 // across stages in registers) and writes P^T[k][p].
-template <int VT>
+// FOLD (alpha = beta, see cjt_plan::fold): the stage's 32 degrees are stored
+// parity-sorted (slot k/2 for even k, 16 + k/2 for odd k) and contracted into
+// two accumulator sets, E (even degrees) and O (odd degrees); the reduce
+// writes E + O to row i and E - O to its mirror row G - i.
+template <int VT, bool FOLD>
 __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     k_rec_forward_ws(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
                      const double2* __restrict__ ck, const FwdItem* __restrict__ items,
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     };
     // stage c[b0 .. b0+VT)[n0 .. n0+32) into Cs[cb]: 16-byte copies when the
     // rows are 16-byte aligned (even ldc), else 8-byte copies
-    const bool c16 = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    const bool c16 = !FOLD && ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
     auto stage_c = [&](int cb, int64_t n0) {
       if (c16) {
 #pragma unroll
@@ -405,7 +409,8 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
           const int v = idx / FWD_KS, k = idx % FWD_KS;
           const int64_t bb = b0 + v, n = n0 + k;
           const bool ok = bb < batch && n < ncoef;
-          cp_async8(&Cs[cb][v][k], ok ? c + bb * ldc + n : c, ok);
+          const int slot = FOLD ? (k & 1) * (FWD_KS / 2) + (k >> 1) : k;
+          cp_async8(&Cs[cb][v][slot], ok ? c + bb * ldc + n : c, ok);
         }
       }
     };
@@ -428,8 +433,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       cp_async_commit();
       const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
       if (dbg != 1)
-        gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1,
-                                  [&](int k, double v) { Pt[buf][k][p] = v; });
+        gen_chain<FWD_KS, FWD_KS>(reg, xx, Ts[tb], nval, s0, s1, [&](int k, double v) {
+          Pt[buf][FOLD ? (k & 1) * (FWD_KS / 2) + (k >> 1) : k][p] = v;
+        });
       // next stage's tables and this stage's c tile landed; the next c tile
       // (newest group) may stay in flight
       cp_async_wait<1>();
@@ -443,17 +449,23 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   const int lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
   const int ar = lane >> 2, ak = lane & 3;
   const int ntile0 = wn * W::NT;
-  double acc[4][W::NT][2];
+  constexpr int NS = FOLD ? 2 : 1;   // accumulator sets (E, O)
+  double acc[NS][4][W::NT][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int h = 0; h < NS; ++h)
 #pragma unroll
-    for (int nt = 0; nt < W::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < W::NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
   for (int sidx = 0; sidx < nstages; ++sidx) {
     const int buf = sidx % W::NBUF, cbuf = sidx % W::NCB;
     named_sync(BAR_FULL + buf, W::NTH);
     if (dbg != 2)
 #pragma unroll
     for (int kk = 0; kk < FWD_KS / 4; ++kk) {
+      // FOLD: slots 0..15 hold the even degrees (set E), 16..31 the odd (O)
+      constexpr int KH = FWD_KS / 4 / 2;
+      const int h = (FOLD && kk >= KH) ? 1 : 0;
       double a[4], bf[W::NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Pt[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
@@ -462,22 +474,47 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < W::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+        for (int nt = 0; nt < W::NT; ++nt)
+          dmma(acc[FOLD ? h : 0][mt][nt][0], acc[FOLD ? h : 0][mt][nt][1], a[mt], bf[nt]);
     }
     if (sidx + W::NBUF < nstages) named_arrive(BAR_EMPTY + buf, W::NTH);
   }
   // D[row][vec]: row = 32 warp + 8 mt + (lane>>2), vec = 8 (ntile0 + nt) + 2 (lane&3) + j
-  double* dst = part + (int64_t)it.slot * batch * FWD_ROWS;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int h = 0; h < NS; ++h) {
+    double* dst = part + ((int64_t)it.slot * NS + h) * batch * FWD_ROWS;
 #pragma unroll
-    for (int nt = 0; nt < W::NT; ++nt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int row = 32 * warp + 8 * mt + ar;
-        const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
-        if (bb < batch) dst[bb * FWD_ROWS + row] = acc[mt][nt][j];
-      }
+      for (int nt = 0; nt < W::NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int row = 32 * warp + 8 * mt + ar;
+          const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
+          if (bb < batch) dst[bb * FWD_ROWS + row] = acc[h][mt][nt][j];
+        }
+  }
+}
+
+// folded plans: rows i < nrows (= G/2 + 1) carry E (even degrees) and O (odd
+// degrees) partials; row i gets E + O, its mirror G - i gets E - O
+__global__ void k_rec_forward_reduce_fold(const int32_t* __restrict__ tile_slot0,
+                                          const int32_t* __restrict__ tile_nslot, int64_t nrows,
+                                          const double* __restrict__ part, double* __restrict__ vals,
+                                          int64_t ldv, int64_t batch, int64_t G) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b = blockIdx.y;
+  if (i >= nrows) return;
+  const int64_t tile = i / FWD_ROWS, lr = i % FWD_ROWS;
+  const int32_t s0 = tile_slot0[tile], ns = tile_nslot[tile];
+  double e = 0.0, o = 0.0;
+#pragma unroll 4
+  for (int s = 0; s < ns; ++s) {
+    e += part[(((int64_t)(s0 + s) * 2 + 0) * batch + b) * FWD_ROWS + lr];
+    o += part[(((int64_t)(s0 + s) * 2 + 1) * batch + b) * FWD_ROWS + lr];
+  }
+  vals[b * ldv + i] = e + o;
+  if (G - i != i) vals[b * ldv + (G - i)] = e - o;
 }
 
 __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
@@ -500,12 +537,16 @@ __global__ void k_rec_forward_reduce(const int32_t* __restrict__ tile_slot0,
 // row tile.  Producer thread p = (row p/4, degree chunk p%4) restarts from the
 // dense generator stream and writes P[row][deg]; producers also stage the
 // wv tile.  The tables of the item's 128-degree window live in shared memory.
-template <int VT>
+// FOLD (alpha = beta): rows i < nrows = G/2 + 1 only, degrees stored
+// parity-sorted (window slot dl/2 for even dl, 64 + dl/2 for odd): consumer
+// warps 0-1 contract the even degrees with wv_i + wv_{G-i}, warps 2-3 the odd
+// degrees with wv_i - wv_{G-i} (the middle row i = G/2 counted once).
+template <int VT, bool FOLD>
 __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     k_rec_inverse_ws(RecTablesDev tab, const GenState* __restrict__ gen, int64_t nrows,
                      const InvItem* __restrict__ items, const int32_t* __restrict__ tile_ids,
                      const double* __restrict__ wv, int64_t ldw, int64_t batch,
-                     double* __restrict__ part, int dbg) {
+                     double* __restrict__ part, int dbg, int64_t G) {
   using W = WsCfg<VT>;
   constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
   constexpr int WS = INV_RT + 4;
@@ -516,7 +557,9 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   extern __shared__ __align__(16) double smem_rec[];
   double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
   double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
-  double* Tw = smem_rec + W::NBUF * INV_RT * PR + W::NCB * VT * WS;   // [REC_WIN_ROWS][SPAN]
+  // FOLD: the mirror rows' wv tile, ring after Ws
+  double(*Wm)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR + W::NCB * VT * WS);
+  double* Tw = smem_rec + W::NBUF * INV_RT * PR + (FOLD ? 2 : 1) * W::NCB * VT * WS;   // [REC_WIN_ROWS][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -542,6 +585,10 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
         const int64_t bb = b0 + v, i = r0 + k;
         const bool ok = bb < batch && i < nrows;
         cp_async8(&Ws[wb][v][k], ok ? wv + bb * ldw + i : wv, ok);
+        if constexpr (FOLD) {
+          const bool okm = ok && G - i != i;   // the middle row is its own mirror
+          cp_async8(&Wm[wb][v][k], okm ? wv + bb * ldw + (G - i) : wv, okm);
+        }
       }
     };
     stage_wv(0, 0);
@@ -566,8 +613,14 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       const int nval = (int)max((int64_t)0, min((int64_t)CK + 1, cut - nstart));
       // this chunk's window: degrees nl0 + k at slot nl0 + k + 2 gq (pads per 32)
       if (dbg != 1)
-        gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + 2 * gq, nval, g.s0, g.s1,
-                             [&](int k, double v) { dst[k] = v; });
+        gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + 2 * gq, nval, g.s0, g.s1, [&](int k, double v) {
+          if constexpr (FOLD) {
+            const int dl = nl0 + k, ps = (dl & 1) * (INV_DT / 2) + (dl >> 1);
+            Ps[buf][grow][ps + (ps >> 5)] = v;
+          } else {
+            dst[k] = v;
+          }
+        });
       // this stage's wv tile (committed one iteration ago) must have landed;
       // the next tile's copies (newest group) may stay in flight
       cp_async_wait<1>();
@@ -596,7 +649,13 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
 #pragma unroll
-      for (int nt = 0; nt < W::NT; ++nt) bf[nt] = Ws[wbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+      for (int nt = 0; nt < W::NT; ++nt) {
+        bf[nt] = Ws[wbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+        if constexpr (FOLD) {   // even-degree warps: wv_i + wv_{G-i}; odd: wv_i - wv_{G-i}
+          const double m = Wm[wbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+          bf[nt] = warp < 2 ? bf[nt] + m : bf[nt] - m;
+        }
+      }
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -611,7 +670,8 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     for (int nt = 0; nt < W::NT; ++nt)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int deg = 32 * warp + 8 * mt + ar;
+        const int slot = 32 * warp + 8 * mt + ar;
+        const int deg = FOLD ? (slot < INV_DT / 2 ? 2 * slot : 2 * (slot - INV_DT / 2) + 1) : slot;
         const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
         if (bb < batch) dst[bb * INV_DT + deg] = acc[mt][nt][j];
       }
@@ -910,26 +970,33 @@ static int ws_debug() {
 
 int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
                        const double2* ck, const FwdItem* items, int64_t n_items, const double* c,
-                       int64_t ldc, int64_t ncoef, int64_t batch, int vt, double* part, cudaStream_t st) {
+                       int64_t ldc, int64_t ncoef, int64_t batch, int vt, bool fold, double* part,
+                       cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
   dim3 grid((unsigned)n_items, (unsigned)((batch + vt - 1) / vt));
+  if (fold && vt > 64) return fail(CJT_EINVAL, "folded contraction tiles hold at most 64 vectors");
   switch (vt) {
-#define CJT_FWD(V)                                                                               \
-  case V: {                                                                                      \
+#define CJT_FWD_F(V, F)                                                                          \
+  {                                                                                              \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
     const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + (R + 1) * V * (FWD_KS + 4) + 2 * REC_WIN_ROWS * FWD_KS);  \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V>,                                     \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V, F>,                                  \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_forward_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(rows, tab, ck_off, ck, items, c, ldc, \
-                                                           ncoef, batch, part, ws_debug());      \
-    break;                                                                                       \
+    k_rec_forward_ws<V, F><<<grid, WsCfg<V>::NTH, smem, st>>>(rows, tab, ck_off, ck, items, c,   \
+                                                              ldc, ncoef, batch, part, ws_debug()); \
   }
-    CJT_FWD(128) CJT_FWD(64) CJT_FWD(32) CJT_FWD(24) CJT_FWD(16)
+#define CJT_FWD(V)                                                                               \
+  case V:                                                                                        \
+    if (fold) CJT_FWD_F(V, true) else CJT_FWD_F(V, false)                                       \
+    break;
+    case 128: CJT_FWD_F(128, false) break;
+    CJT_FWD(64) CJT_FWD(32) CJT_FWD(24) CJT_FWD(16)
 #undef CJT_FWD
+#undef CJT_FWD_F
     default: return fail(CJT_EINVAL, "bad vector tile");
   }
   CJT_CUDA_TRY(cudaGetLastError());
@@ -938,10 +1005,13 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
 
 int launch_rec_forward_reduce(const int32_t* tile_slot0, const int32_t* tile_nslot, int64_t nrows,
                               const double* part, double* vals, int64_t ldv, int64_t batch,
-                              cudaStream_t st) {
+                              int64_t G, bool fold, cudaStream_t st) {
   const int T = 256;
   dim3 grid((unsigned)((nrows + T - 1) / T), (unsigned)batch);
-  k_rec_forward_reduce<<<grid, T, 0, st>>>(tile_slot0, tile_nslot, nrows, part, vals, ldv, batch);
+  if (fold)
+    k_rec_forward_reduce_fold<<<grid, T, 0, st>>>(tile_slot0, tile_nslot, nrows, part, vals, ldv, batch, G);
+  else
+    k_rec_forward_reduce<<<grid, T, 0, st>>>(tile_slot0, tile_nslot, nrows, part, vals, ldv, batch);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -959,27 +1029,34 @@ int launch_build_inv_gen(const RecRowsDev& rows, const int64_t* ck_off, const do
 
 int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, const InvItem* items,
                        int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
-                       int64_t batch, int vt, double* part, cudaStream_t st) {
+                       int64_t batch, int vt, bool fold, int64_t G, double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
+  if (fold && vt > 64) return fail(CJT_EINVAL, "folded contraction tiles hold at most 64 vectors");
   dim3 grid((unsigned)n_items, (unsigned)((batch + vt - 1) / vt));
   const GenState* g = (const GenState*)gen;
   switch (vt) {
-#define CJT_INV(V)                                                                               \
-  case V: {                                                                                      \
+#define CJT_INV_F(V, F)                                                                          \
+  {                                                                                              \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (R + 1) * V * (INV_RT + 4) + REC_WIN_ROWS * (INV_DT + 2 * (INV_DT / 32)));   \
+    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (F ? 2 : 1) * (R + 1) * V * (INV_RT + 4) + \
+                          REC_WIN_ROWS * (INV_DT + 2 * (INV_DT / 32)));                          \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V>,                                     \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V, F>,                                  \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_inverse_ws<V><<<grid, WsCfg<V>::NTH, smem, st>>>(tab, g, nrows, items, tile_ids, wv,   \
-                                                           ldw, batch, part, ws_debug());      \
-    break;                                                                                       \
+    k_rec_inverse_ws<V, F><<<grid, WsCfg<V>::NTH, smem, st>>>(tab, g, nrows, items, tile_ids, wv, \
+                                                              ldw, batch, part, ws_debug(), G);  \
   }
-    CJT_INV(128) CJT_INV(64) CJT_INV(32) CJT_INV(24) CJT_INV(16)
+#define CJT_INV(V)                                                                               \
+  case V:                                                                                        \
+    if (fold) CJT_INV_F(V, true) else CJT_INV_F(V, false)                                       \
+    break;
+    case 128: CJT_INV_F(128, false) break;
+    CJT_INV(64) CJT_INV(32) CJT_INV(24) CJT_INV(16)
 #undef CJT_INV
+#undef CJT_INV_F
     default: return fail(CJT_EINVAL, "bad vector tile");
   }
   CJT_CUDA_TRY(cudaGetLastError());

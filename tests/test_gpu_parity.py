@@ -80,3 +80,40 @@ def test_vector_tile_width_invariance(cuda, batch):
     scale = float(c[:8].abs().sum(dim=1).max())
     assert float((f[:8] - f1).abs().max()) <= 1e-15 * scale
     assert float((i[:8] - i1).abs().max()) <= 1e-15 * scale
+
+
+@pytest.mark.parametrize("ab,n", [((0.0, 0.0), 1023), ((0.5, 0.5), 4095), ((-0.45, -0.45), 2047),
+                                  ((0.25, 0.25), 8191)])
+def test_parity_folding_alpha_eq_beta(cuda, monkeypatch, ab, n):
+    """alpha = beta: the forward recurrence runs parity-folded (rows i and G-i
+    from one generated row, even / odd degrees contracted separately); it
+    agrees with the unfolded contraction and the oracle.  The opt-in folded
+    inverse ($CJT_FOLD_INVERSE=1) stays within the transform tolerance."""
+    import torch
+    a, b = ab
+    p = cj.JacobiParameters(a, b)
+    c = np.stack([O.seeded_vector(3, v, n) for v in range(20)])
+    x = torch.from_numpy(c).to(cuda)
+    scale = np.abs(c).sum(axis=1)
+
+    def run(direction, inp, env):
+        for k in ("CJT_FOLD", "CJT_FOLD_INVERSE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        tp = cj.plan(direction, p, n)
+        f = cj.forward_batched if direction == "forward" else cj.inverse_batched
+        out = f(tp, inp)
+        torch.cuda.synchronize()
+        return out
+
+    f_fold = run("forward", x, {})
+    f_flat = run("forward", x, {"CJT_FOLD": "0"})
+    d = (f_fold - f_flat).abs().max(dim=1).values.cpu().numpy()
+    assert np.all(d <= 1e-14 * scale)
+    for v in (0, 19):
+        assert O.parity(f_fold[v].cpu().numpy(), O.oracle_forward(a, b, c[v]), c[v]) <= TOL
+    i_fold = run("inverse", f_flat, {"CJT_FOLD_INVERSE": "1"})
+    fh = f_flat.cpu().numpy()
+    for v in (0, 19):
+        assert O.parity(i_fold[v].cpu().numpy(), O.oracle_inverse(a, b, fh[v]), fh[v]) <= TOL
