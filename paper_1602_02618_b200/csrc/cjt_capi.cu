@@ -378,6 +378,15 @@ int upload_ws(cjt_plan* P, T** dst, const std::vector<T>& v) {
   return CJT_OK;
 }
 
+// $CJT_FOLD_TWO_PASS=0 (experiments): folded forward plans stay warp-specialised
+bool fold_two_pass_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CJT_FOLD_TWO_PASS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int build_items(cjt_plan* P, int64_t batch) {
   const int64_t target = 8 * 148;  // CTAs worth of items to fill 148 SMs several times over
   P->two_pass = false;
@@ -392,7 +401,11 @@ int build_items(cjt_plan* P, int64_t batch) {
   // (inverse: the mirror rows' wv ring doubles the operand tiles, 16-vector
   // tiles keep two CTAs per SM)
   if (P->fold) P->vt = std::min(P->vt, P->direction == CJT_FORWARD ? 64 : 16);
-  const int64_t budget_blocks = (P->vt >= 128 && !P->fold) ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
+  // two-pass at 128-vector tiles; folded forward plans at 64-vector tiles
+  // (their GEMM holds two accumulator sets) once the batch spans several tiles
+  const bool tp = P->fold ? (P->direction == CJT_FORWARD && batch > 64 && fold_two_pass_enabled())
+                          : P->vt >= 128;
+  const int64_t budget_blocks = tp ? pgen_chunk_budget() / (32 * 128 * 8) : 0;
   const int64_t nbt = (batch + P->vt - 1) / P->vt;
   if (P->direction == CJT_FORWARD) {
     const std::vector<int64_t> tmax = tile_max_cut(P, FWD_ROWS);
@@ -679,10 +692,11 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       double* pw = nullptr;
       if (int rc = arena_get(P->device, st, P->chunk_bytes, &pw)) return rc;
       for (const auto& ch : P->chunks) {
-        if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj + ch.b0, ch.b1 - ch.b0, pw, st))
+        if (int rc = launch_pgen_fwd(P->rows, P->tab, P->ck_off, P->ck, P->blk_tj + ch.b0, ch.b1 - ch.b0, pw,
+                                     P->fold, st))
           return rc;
         if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, nullptr, in, N1, N1, batch, P->vt, false,
-                                     W.part, st)) return rc;
+                                     P->fold, W.part, st)) return rc;
         launches += 2;
       }
       launches -= 1;
@@ -718,7 +732,7 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       for (const auto& ch : P->chunks) {
         if (int rc = launch_pgen_inv(P->tab, P->inv_gen, P->d_gn0, ch.b0, ch.b1, pw, st)) return rc;
         if (int rc = launch_rec_gemm(ch.items, ch.n_items, pw, P->tile_ids, W.vals, G1, G1, batch, P->vt, true,
-                                     W.part, st)) return rc;
+                                     false, W.part, st)) return rc;
         launches += 2;
       }
       launches -= 1;

@@ -586,12 +586,13 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
                        int64_t n_items, const int32_t* tile_ids, const double* wv, int64_t ldw,
                        int64_t batch, int vt, bool fold, int64_t G, double* part, cudaStream_t st);
 int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
-                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st);
+                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, bool fold,
+                    cudaStream_t st);
 int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0, int64_t gbeg,
                     int64_t gend, double* P, cudaStream_t st);
 int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, const int32_t* ids,
                     const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, bool amk,
-                    double* part, cudaStream_t st);
+                    bool fold, double* part, cudaStream_t st);
 int launch_inverse_finish(const int32_t* dt_slot0, const int32_t* dt_nslot, int64_t ndeg,
                           const double* part, const double* blocks_acc, const double* scal,
                           double* out, int64_t ldo, int64_t batch, cudaStream_t st);

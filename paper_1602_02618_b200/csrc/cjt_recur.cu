@@ -795,7 +795,7 @@ __global__ void k_jacobi_values(RecTablesDev tab, int64_t n_max, const double* _
 __global__ void __launch_bounds__(128)
     k_pgen_fwd(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
                const double2* __restrict__ ck, const int2* __restrict__ blk_tj, int64_t nblk,
-               double* __restrict__ P) {
+               double* __restrict__ P, int fold) {
   const int tid = threadIdx.x;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int2 tj = blk_tj[blk];
@@ -815,8 +815,10 @@ __global__ void __launch_bounds__(128)
       }
     }
     const int nval = (int)max((int64_t)0, min((int64_t)FWD_KS + 1, cut - n0));
-    gen_chain_g<FWD_KS>(reg, reg == 0 ? x : xm, tab, n0, nval, s0, s1,
-                        [&](int k, double v) { out[k * FWD_ROWS] = v; });
+    // fold: parity-sorted degree slots (see k_rec_forward_ws)
+    gen_chain_g<FWD_KS>(reg, reg == 0 ? x : xm, tab, n0, nval, s0, s1, [&](int k, double v) {
+      out[(fold ? (k & 1) * (FWD_KS / 2) + (k >> 1) : k) * FWD_ROWS] = v;
+    });
   }
 }
 
@@ -866,7 +868,9 @@ struct GemmCfg {
 //   A_s[k][m] * x[b][xoff(s) + k],  A_s = P block (p_block0 + s) (32 x 128),
 // xoff(s) = x_off0 + 32 s (forward: contiguous degrees) or 32 * ids[ids_off + s]
 // (inverse: the item's row tiles).
-template <int VT, bool AMK>
+// FOLD (forward, alpha = beta): degree slots parity-sorted by k_pgen_fwd; two
+// accumulator sets (even / odd degrees), partials [slot][2][batch][128]
+template <int VT, bool AMK, bool FOLD = false>
 __global__ void __launch_bounds__(GemmCfg<VT, AMK>::NTH)
     k_rec_gemm(const GemmItem* __restrict__ items, const double* __restrict__ P,
                const int32_t* __restrict__ ids, const double* __restrict__ x, int64_t ldx,
@@ -897,15 +901,19 @@ __global__ void __launch_bounds__(GemmCfg<VT, AMK>::NTH)
       const int v = idx >> 5, k = idx & 31;
       const int64_t bb = b0 + v, kk = xoff + k;
       const bool ok = bb < batch && kk < xlen;
-      cp_async8(&Xs[buf][v][k], ok ? x + bb * ldx + kk : x, ok);
+      const int ks = FOLD ? (k & 1) * 16 + (k >> 1) : k;
+      cp_async8(&Xs[buf][v][ks], ok ? x + bb * ldx + kk : x, ok);
     }
   };
 
-  double acc[4][C::NT][2];
+  constexpr int NS = FOLD ? 2 : 1;
+  double acc[NS][4][C::NT][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int h = 0; h < NS; ++h)
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
 
   const int ns = it.nstages;
 #pragma unroll
@@ -928,24 +936,29 @@ __global__ void __launch_bounds__(GemmCfg<VT, AMK>::NTH)
         a[mt] = AMK ? As[buf][32 * warp + 8 * mt + ar][4 * kk + ak] : As[buf][4 * kk + ak][32 * warp + 8 * mt + ar];
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt) bf[nt] = Xs[buf][8 * (ntile0 + nt) + ar][4 * kk + ak];
+      const int h = (FOLD && kk >= 4) ? 1 : 0;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt]);
+        for (int nt = 0; nt < C::NT; ++nt)
+          dmma(acc[FOLD ? h : 0][mt][nt][0], acc[FOLD ? h : 0][mt][nt][1], a[mt], bf[nt]);
     }
   }
   cp_async_wait<0>();
-  double* dst = part + (int64_t)it.slot * batch * 128;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int h = 0; h < NS; ++h) {
+    double* dst = part + ((int64_t)it.slot * NS + h) * batch * 128;
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int m = 32 * warp + 8 * mt + ar;
-        const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
-        if (bb < batch) dst[bb * 128 + m] = acc[mt][nt][j];
-      }
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int m = 32 * warp + 8 * mt + ar;
+          const int64_t bb = b0 + 8 * (ntile0 + nt) + 2 * ak + j;
+          if (bb < batch) dst[bb * 128 + m] = acc[h][mt][nt][j];
+        }
+  }
 }
 
 }  // namespace
@@ -1065,10 +1078,11 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 
 
 int launch_pgen_fwd(const RecRowsDev& rows, const RecTablesDev& tab, const int64_t* ck_off,
-                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, cudaStream_t st) {
+                    const double2* ck, const int2* blk_tj, int64_t nblk, double* P, bool fold,
+                    cudaStream_t st) {
   if (nblk <= 0) return CJT_OK;
   const int64_t grid = std::min<int64_t>(nblk, 148 * 16);
-  k_pgen_fwd<<<(unsigned)grid, 128, 0, st>>>(rows, tab, ck_off, ck, blk_tj, nblk, P);
+  k_pgen_fwd<<<(unsigned)grid, 128, 0, st>>>(rows, tab, ck_off, ck, blk_tj, nblk, P, fold ? 1 : 0);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -1084,24 +1098,25 @@ int launch_pgen_inv(const RecTablesDev& tab, const void* gen, const int32_t* gn0
 
 int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, const int32_t* ids,
                     const double* x, int64_t ldx, int64_t xlen, int64_t batch, int vt, bool amk,
-                    double* part, cudaStream_t st) {
+                    bool fold, double* part, cudaStream_t st) {
   if (n_items <= 0 || batch <= 0) return CJT_OK;
   dim3 grid((unsigned)((batch + vt - 1) / vt), (unsigned)n_items);
-#define CJT_GEMM(V, M)                                                                           \
-  if (vt == V && amk == M) {                                                                     \
+#define CJT_GEMM(V, M, F)                                                                        \
+  if (vt == V && amk == M && fold == F) {                                                        \
     using Cf = GemmCfg<V, M>;                                                                    \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
-      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V, M>,                                        \
+      CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V, M, F>,                                     \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM)); \
       init = true;                                                                               \
     }                                                                                            \
-    k_rec_gemm<V, M><<<grid, Cf::NTH, Cf::SMEM, st>>>(items, P, ids, x, ldx, xlen, batch, part); \
+    k_rec_gemm<V, M, F><<<grid, Cf::NTH, Cf::SMEM, st>>>(items, P, ids, x, ldx, xlen, batch, part); \
     CJT_CUDA_TRY(cudaGetLastError());                                                            \
     return CJT_OK;                                                                               \
   }
-  CJT_GEMM(128, false) CJT_GEMM(64, false) CJT_GEMM(32, false) CJT_GEMM(16, false)
-  CJT_GEMM(128, true) CJT_GEMM(64, true) CJT_GEMM(32, true) CJT_GEMM(16, true)
+  CJT_GEMM(128, false, false) CJT_GEMM(64, false, false) CJT_GEMM(32, false, false) CJT_GEMM(16, false, false)
+  CJT_GEMM(128, true, false) CJT_GEMM(64, true, false) CJT_GEMM(32, true, false) CJT_GEMM(16, true, false)
+  CJT_GEMM(64, false, true)
 #undef CJT_GEMM
   return fail(CJT_EINVAL, "bad vector tile");
 }
