@@ -134,6 +134,19 @@ int cjt_execute_stage(cjt_plan* plan, const double* in, double* out, int64_t bat
 /* Measured fp64 FMA throughput of the current device (TFLOP/s, best of 5). */
 int cjt_probe_fp64_peak(double* tflops, void* stream);
 
+/* Standalone batched chirp-z products: the trigonometric transforms of
+ * trig.py (TrigPlanWorkspace.dct1 / dst1_bordered / chebyshev_synthesis /
+ * chebyshev_analysis, trig.py:35-63), each one cjt_chirpz_desc with M = 1
+ * (the Python layer builds pre / post / spectra).  Device pointers,
+ * in: [batch][ldi] (reads p0 .. p0+width), out: [batch][ldo] (writes q0 ..
+ * q0+count, overwritten or accumulated per desc.accumulate); stream ordered,
+ * per-stream workspaces (allocated on a stream's first use, outside capture). */
+typedef struct cjt_chirpz_plan cjt_chirpz_plan;
+int cjt_chirpz_create(const cjt_chirpz_desc* desc, cjt_chirpz_plan** out);
+int cjt_chirpz_execute(cjt_chirpz_plan* plan, const double* in, int64_t ldi, double* out,
+                       int64_t ldo, int64_t batch, void* stream);
+int cjt_chirpz_destroy(cjt_chirpz_plan* plan);
+
 /* Reference backend-plugin signatures, host arrays (see header comment). */
 int cjt_clenshaw_points(const double* A, const double* B, const double* C,
                         const double* rb_plus, const double* rb_minus,

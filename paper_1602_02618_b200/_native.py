@@ -90,11 +90,15 @@ def lib():
     L.cjt_clenshaw_points_dev.argtypes = [_p] * 7 + [_i64, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p]
     L.cjt_jacobi_values.argtypes = [_p] * 5 + [_i64, _i64, _p, _p, _i64, _p]
     L.cjt_clenshaw_smith_points.argtypes = [_p] * 6 + [_i64, _p, _p, _i64, _p]
+    L.cjt_chirpz_create.argtypes = [ctypes.POINTER(ChirpZDesc), ctypes.POINTER(_p)]
+    L.cjt_chirpz_execute.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p]
+    L.cjt_chirpz_destroy.argtypes = [_p]
     for name in ("cjt_device_count", "cjt_plan_create", "cjt_plan_destroy", "cjt_plan_reserve",
                  "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host", "cjt_clenshaw_points",
                  "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
                  "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak",
-                 "cjt_clenshaw_points_dev", "cjt_jacobi_values", "cjt_clenshaw_smith_points"):
+                 "cjt_clenshaw_points_dev", "cjt_jacobi_values", "cjt_clenshaw_smith_points",
+                 "cjt_chirpz_create", "cjt_chirpz_execute", "cjt_chirpz_destroy"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -105,7 +109,8 @@ EXPORTED_SYMBOLS = (
     "cjt_plan_reserve", "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host",
     "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
     "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak", "cjt_clenshaw_points_dev",
-    "cjt_jacobi_values", "cjt_clenshaw_smith_points",
+    "cjt_jacobi_values", "cjt_clenshaw_smith_points", "cjt_chirpz_create", "cjt_chirpz_execute",
+    "cjt_chirpz_destroy",
 )
 SHIFT_INC_BETA, SHIFT_DEC_BETA, SHIFT_INC_ALPHA, SHIFT_DEC_ALPHA = 0, 1, 2, 3
 STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7

@@ -124,6 +124,27 @@ struct cjt_plan {
   }
 };
 
+// Standalone batched chirp-z product (trig.py's DCT-I / DST-I / Chebyshev
+// synthesis and analysis): one ChirpZDev plus its per-stream workspaces.
+struct cjt_chirpz_plan {
+  std::unique_ptr<cjt_plan> owner;   // allocations, twiddle table
+  ChirpZDev cz{};
+  int64_t in_len = 0, out_len = 0;
+  struct Ws {
+    std::vector<void*> allocs;
+    int64_t batch = 0;
+    double2* scratch = nullptr;
+    double* part = nullptr;
+    double2* spec = nullptr;
+  };
+  std::map<cudaStream_t, Ws> ws;
+  std::mutex mu;
+  ~cjt_chirpz_plan() {
+    for (auto& kv : ws)
+      for (void* q : kv.second.allocs) cudaFree(q);
+  }
+};
+
 namespace {
 
 struct DeviceGuard {
@@ -1132,6 +1153,76 @@ int cjt_jacobi_values(const double* A, const double* B, const double* C, const d
   RecTablesDev tab{dA, dB, dC, rfp, rfm, nullptr, nullptr, (int64_t)tl};
   if (int rc = launch_jacobi_values(tab, n_max, dx, dxm, dmode, (double*)p, n_points, 0)) return rc;
   CJT_CUDA_TRY(cudaMemcpy(out, p, nout * 8, cudaMemcpyDeviceToHost));
+  return CJT_OK;
+}
+
+int cjt_chirpz_create(const cjt_chirpz_desc* d, cjt_chirpz_plan** out) {
+  if (!d || !out) return fail(CJT_EINVAL, "null argument");
+  *out = nullptr;
+  std::unique_ptr<cjt_chirpz_plan> C(new cjt_chirpz_plan());
+  C->owner.reset(new cjt_plan());
+  cjt_plan* P = C->owner.get();
+  CJT_CUDA_TRY(cudaGetDevice(&P->device));
+  std::vector<double2> tw(8192);
+  for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
+  if (int rc = upload(P->allocs, &P->tw8192, tw.data(), tw.size())) return rc;
+  if (int rc = build_chirpz(P, *d, &C->cz)) return rc;
+  C->in_len = d->p0 + d->width;
+  C->out_len = d->q0 + d->count;
+  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  *out = C.release();
+  return CJT_OK;
+}
+
+int cjt_chirpz_execute(cjt_chirpz_plan* C, const double* in, int64_t ldi, double* out, int64_t ldo,
+                       int64_t batch, void* stream) {
+  if (!C) return fail(CJT_EINVAL, "null plan");
+  if (batch < 0) return fail(CJT_EINVAL, "negative batch");
+  if (batch == 0) return CJT_OK;
+  if (!in || !out) return fail(CJT_EINVAL, "null buffer");
+  if (ldi < C->in_len || ldo < C->out_len) return fail(CJT_EINVAL, "leading dimension too small");
+  if (batch > 65535) return fail(CJT_EINVAL, "batch must be <= 65535 per call");
+  DeviceGuard g(C->owner->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  cjt_chirpz_plan::Ws* W = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(C->mu);
+    W = &C->ws[st];
+    if (W->batch < batch) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone)
+        return fail(CJT_EINVAL, "chirp-z workspace for this stream must exist before graph capture");
+      for (void* q : W->allocs) cudaFree(q);
+      *W = cjt_chirpz_plan::Ws{};
+      void* p;
+      const int64_t se = C->owner->scratch_elems_per_vec * batch;
+      if (se > 0) {
+        if (int rc = dalloc(W->allocs, &p, (size_t)se * 16)) return rc;
+        W->scratch = (double2*)p;
+      }
+      int64_t pe = 0, spe = 0;
+      chirpz_workspace(C->cz, batch, &pe, &spe);
+      if (pe > 0) {
+        if (int rc = dalloc(W->allocs, &p, (size_t)pe * 8)) return rc;
+        W->part = (double*)p;
+      }
+      if (spe > 0) {
+        if (int rc = dalloc(W->allocs, &p, (size_t)spe * 16)) return rc;
+        W->spec = (double2*)p;
+      }
+      W->batch = batch;
+    }
+  }
+  int launches = 0;
+  return launch_chirpz(C->cz, C->owner->tw8192, in, ldi, out, ldo, batch, W->scratch, W->part, W->spec, st,
+                       &launches);
+}
+
+int cjt_chirpz_destroy(cjt_chirpz_plan* C) {
+  if (!C) return CJT_OK;
+  cudaDeviceSynchronize();
+  delete C;
   return CJT_OK;
 }
 
