@@ -847,12 +847,13 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   if (int rc = upload_tables(A, src, tl, &P->tab)) return rc;
 
   // parity folding (alpha = beta): B_n = 0, rf- = -rf+, symmetric cuts,
-  // antisymmetric regions; only while the mirrored rows' x = -x_i stays
-  // within the transform tolerance of the reference's cos(theta_{G-i})
-  // (grids up to 2^16 points; a 1-ulp angle shift moves
-  // the alpha = beta = 1/2 inverse by 9e-13 at N = 65535)
+  // antisymmetric regions.  The forward is insensitive to the mirrored rows'
+  // x = -x_i vs the reference's cos(theta_{G-i}) (<= 2e-16 ||c||_1 measured,
+  // SURVEY.md 8(c)); the inverse is not (a 1-ulp angle shift moves the
+  // alpha = beta = 1/2 inverse by 9e-13 at N = 65535).
   {
-    bool sym = G <= 65534;
+    // (the inverse additionally stops at G <= 65534, see below)
+    bool sym = d->direction == CJT_FORWARD || G <= 65534;
     for (size_t n = 0; sym && n < tl; ++n)
       sym = d->B[n] == 0.0 && d->rf_minus[n] == -d->rf_plus[n];
     for (int64_t i = 0; sym && i < nr; ++i)

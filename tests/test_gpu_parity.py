@@ -117,3 +117,19 @@ def test_parity_folding_alpha_eq_beta(cuda, monkeypatch, ab, n):
     fh = f_flat.cpu().numpy()
     for v in (0, 19):
         assert O.parity(i_fold[v].cpu().numpy(), O.oracle_inverse(a, b, fh[v]), fh[v]) <= TOL
+
+
+def test_parity_folding_full_size_forward(cuda, monkeypatch):
+    """Folded forward at the largest ragged-config size, alpha = beta = 1/2,
+    N = 65535 (pure recurrence): equal to the unfolded contraction to 1e-14."""
+    import torch
+    p = cj.JacobiParameters(0.5, 0.5)
+    n = 65535
+    c = torch.from_numpy(np.stack([O.seeded_vector(5, v, n) for v in range(4)])).to(cuda)
+    monkeypatch.delenv("CJT_FOLD", raising=False)
+    f_fold = cj.forward_batched(cj.plan("forward", p, n), c)
+    monkeypatch.setenv("CJT_FOLD", "0")
+    f_flat = cj.forward_batched(cj.plan("forward", p, n), c)
+    torch.cuda.synchronize()
+    d = (f_fold - f_flat).abs().max(dim=1).values / c.abs().sum(dim=1)
+    assert float(d.max()) <= 1e-14
