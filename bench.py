@@ -35,6 +35,9 @@ sys.path.insert(0, str(ROOT / "oracle"))
 METRIC = "CJT coeffs/s (fp64 fwd+inv)"
 UNIT = "coeffs/s"
 NOMINAL_FP64_TFLOPS = 37.2
+BOUND_NOTE = ("fp64 pipe: the FFT stages run on DFMA/DADD, the contractions on DMMA (mma.sync f64; tcgen05 "
+              "has no f64 kind), which shares that pipe on B200; every stage moves <= 2.3 TB/s of HBM "
+              "(profiles/ncu_traffic.json), so neither 'hbm' nor the bf16 'tensor' peak applies")
 
 WORKLOADS = {
     1: dict(alpha=0.0, beta=0.0, n=1023, batch=1, env="1/(n+1)"),
@@ -454,7 +457,7 @@ def run_ours(args, wl):
             traffic = None if t_ is None else t_["bytes"]   # DRAM bytes of one stage execution (ncu)
         except (ValueError, OSError, KeyError, TypeError):
             traffic = None
-    roofline = {"bound": "fp64", "kernel": kern, "stage": dom, "achieved": achieved, "peak": peak,
+    roofline = {"bound": "fp64", "bound_note": BOUND_NOTE, "kernel": kern, "stage": dom, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
                 "traffic_note": "ncu dram__bytes_read+write of one execution of this stage (profiles/ncu_traffic.json)",
                 "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains)",
@@ -703,7 +706,7 @@ def run_ours5(args, wl):
             rec_flops += 2.0 * s_.rec_steps * rp.sizes[g] + 5.0 * s_.rec_steps
     rec_ms = stage_ms["fwd_rec"] + stage_ms["inv_rec"]
     achieved = rec_flops / (rec_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": "k_rec_gemm / k_rec_*_ws (K1+K2, all groups)", "stage": "fwd_rec+inv_rec",
+    roofline = {"bound": "fp64", "bound_note": BOUND_NOTE, "kernel": "k_rec_gemm / k_rec_*_ws (K1+K2, all groups)", "stage": "fwd_rec+inv_rec",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                 "traffic": None, "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains)",
                 "nominal_peak": NOMINAL_FP64_TFLOPS,
