@@ -83,7 +83,8 @@ def test_vector_tile_width_invariance(cuda, batch):
 
 
 @pytest.mark.parametrize("ab,n", [((0.0, 0.0), 1023), ((0.5, 0.5), 4095), ((-0.45, -0.45), 2047),
-                                  ((0.25, 0.25), 8191)])
+                                  ((0.25, 0.25), 8191), ((0.0, 0.0), 1), ((0.5, 0.5), 2),
+                                  ((-0.2, -0.2), 3)])
 def test_parity_folding_alpha_eq_beta(cuda, monkeypatch, ab, n):
     """alpha = beta: the forward recurrence runs parity-folded (rows i and G-i
     from one generated row, even / odd degrees contracted separately); it
