@@ -234,8 +234,10 @@ __global__ void k_build_inv_gen(RecRowsDev rows, const int64_t* __restrict__ ck_
   if (gi >= total * 128) return;
   const int64_t g = gi / 128;
   const int tid = (int)(gi % 128);
-  const int64_t i = (int64_t)ids[g] * INV_RT + (tid >> 2);
-  const int64_t nstart = gn0[g] + CK * (tid & 3);
+  // chunk-major: generator tid = (chunk tid / 32, row tid % 32), so each
+  // producer warp of K2 reads one degree window (broadcast table reads)
+  const int64_t i = (int64_t)ids[g] * INV_RT + (tid & 31);
+  const int64_t nstart = gn0[g] + CK * (tid >> 5);
   GenState st{0.0, 0.0, 0.0, 0};
   if (i < rows.nrows) {
     const int64_t cut = rows.cut[i];
@@ -548,18 +550,22 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
                      const double* __restrict__ wv, int64_t ldw, int64_t batch,
                      double* __restrict__ part, int dbg, int64_t G) {
   using W = WsCfg<VT>;
-  constexpr int PR = INV_DT + 4;    // P row stride; degree d stored at d + (d >> 5)
+  // P stored degree-major, [degree slot][row] with row stride RS: a producer
+  // warp (32 rows, one 32-degree chunk) stores 32 consecutive doubles per
+  // degree, and the consumers' A fragments (rows 4 kk + ak, degrees 8 mt + ar)
+  // hit bank pairs 4 ar + ak: conflict-free both ways
+  constexpr int RS = INV_RT + 4;
   constexpr int WS = INV_RT + 4;
   constexpr int SPAN = INV_DT;      // table window: degrees n0 .. n0 + 127
   // window row stride with two pad slots per 32 degrees: chunk gq starts at slot 34 gq -- 16-byte
   // aligned (vector table loads) and in bank pair 2 gq (conflict-free)
   constexpr int SPANP = SPAN + 2 * (SPAN / 32);
   extern __shared__ __align__(16) double smem_rec[];
-  double(*Ps)[INV_RT][PR] = reinterpret_cast<double(*)[INV_RT][PR]>(smem_rec);
-  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR);
+  double(*Ps)[INV_DT][RS] = reinterpret_cast<double(*)[INV_DT][RS]>(smem_rec);
+  double(*Ws)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_DT * RS);
   // FOLD: the mirror rows' wv tile, ring after Ws
-  double(*Wm)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_RT * PR + W::NCB * VT * WS);
-  double* Tw = smem_rec + W::NBUF * INV_RT * PR + (FOLD ? 2 : 1) * W::NCB * VT * WS;   // [REC_WIN_ROWS][SPAN]
+  double(*Wm)[VT][WS] = reinterpret_cast<double(*)[VT][WS]>(smem_rec + W::NBUF * INV_DT * RS + W::NCB * VT * WS);
+  double* Tw = smem_rec + W::NBUF * INV_DT * RS + (FOLD ? 2 : 1) * W::NCB * VT * WS;   // [REC_WIN_ROWS][SPAN]
   const InvItem it = items[blockIdx.x];
   const int64_t b0 = (int64_t)blockIdx.y * VT;
   const int tid = threadIdx.x;
@@ -567,7 +573,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   if (tid >= W::NC) {
     // ------------------------------ producer ------------------------------
     const int p = tid - W::NC;
-    const int grow = p >> 2, gq = p & 3;
+    const int grow = p & 31, gq = p >> 5;   // producer warp gq: degree chunk gq of all 32 rows
     for (int idx = p; idx < REC_WIN_ROWS * SPAN; idx += W::NP) {
       const int r = idx / SPAN, k = idx % SPAN;
       const int slot = r * SPANP + k + 2 * (k >> 5);
@@ -609,17 +615,12 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
       cp_async_commit();
       const int64_t cut = g.cutreg >> 2;
       const int reg = (int)(g.cutreg & 3) - 1;
-      double* dst = &Ps[buf][grow][CK * gq + gq];
       const int nval = (int)max((int64_t)0, min((int64_t)CK + 1, cut - nstart));
       // this chunk's window: degrees nl0 + k at slot nl0 + k + 2 gq (pads per 32)
       if (dbg != 1)
         gen_chain<CK, SPANP>(reg, g.xx, Tw + nl0 + 2 * gq, nval, g.s0, g.s1, [&](int k, double v) {
-          if constexpr (FOLD) {
-            const int dl = nl0 + k, ps = (dl & 1) * (INV_DT / 2) + (dl >> 1);
-            Ps[buf][grow][ps + (ps >> 5)] = v;
-          } else {
-            dst[k] = v;
-          }
+          const int dl = nl0 + k;
+          Ps[buf][FOLD ? (dl & 1) * (INV_DT / 2) + (dl >> 1) : dl][grow] = v;
         });
       // this stage's wv tile (committed one iteration ago) must have landed;
       // the next tile's copies (newest group) may stay in flight
@@ -633,7 +634,6 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
   const int lane = tid & 31, warp = (tid >> 5) & 3, wn = tid >> 7;
   const int ar = lane >> 2, ak = lane & 3;
   const int ntile0 = wn * W::NT;
-  const int dbase = 32 * warp + warp;   // padded column of this warp's first degree
   double acc[4][W::NT][2];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(WsCfg<VT>::NTH)
     for (int kk = 0; kk < INV_RT / 4; ++kk) {
       double a[4], bf[W::NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][4 * kk + ak][dbase + 8 * mt + ar];
+      for (int mt = 0; mt < 4; ++mt) a[mt] = Ps[buf][32 * warp + 8 * mt + ar][4 * kk + ak];
 #pragma unroll
       for (int nt = 0; nt < W::NT; ++nt) {
         bf[nt] = Ws[wbuf][8 * (ntile0 + nt) + ar][4 * kk + ak];
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(128)
   const int tid = threadIdx.x;
   const int q = tid >> 5, row = tid & 31;
   for (int64_t g = gbeg + blockIdx.x; g < gend; g += gridDim.x) {
-    GenState st = gen[g * 128 + row * 4 + q];
+    GenState st = gen[g * 128 + q * 32 + row];
     const int64_t cut = st.cutreg >> 2;
     const int reg = (int)(st.cutreg & 3) - 1;
     const int64_t nstart = (int64_t)gn0[g] + CK * q;
@@ -1051,7 +1051,7 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
 #define CJT_INV_F(V, F)                                                                          \
   {                                                                                              \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
-    const int smem = 8 * (R * INV_RT * (INV_DT + 4) + (F ? 2 : 1) * (R + 1) * V * (INV_RT + 4) + \
+    const int smem = 8 * (R * INV_DT * (INV_RT + 4) + (F ? 2 : 1) * (R + 1) * V * (INV_RT + 4) + \
                           REC_WIN_ROWS * (INV_DT + 2 * (INV_DT / 32)));                          \
     static bool init = false;                                                                    \
     if (!init) {                                                                                 \
