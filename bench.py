@@ -499,7 +499,10 @@ def run_ours(args, wl):
                "path": "paper_1602_02618_b200.pipeline((fwd_plan, inv_plan), pinned host in, pinned host out, "
                        "sync=False) per step: H2D, forward, inverse, D2H per chunk, chunks and steps "
                        "alternating over 2 streams, one synchronize after the K steps; host wall clock "
-                       "per step, max over ranks"}
+                       "per step, max over ranks",
+               "note": "streamed steps overlap on the two streams, so e2e can exceed the single-stream "
+                       "device value (which serialises steps); every step still copies its inputs in and "
+                       "its results out"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
