@@ -432,8 +432,9 @@ def run_ours(args, wl):
     torch.cuda.synchronize(dev)
     peak = ctypes_peak(L, st)
     fst, ist = fdp.stats(), idp.stats()
-    rec_flops = {"fwd_rec": 2.0 * fst.rec_steps * batch + 5.0 * fst.rec_steps,
-                 "inv_rec": 2.0 * ist.rec_steps * batch + 5.0 * ist.rec_steps}
+    # executed contraction work (parity-folded plans contract half the rows)
+    rec_flops = {"fwd_rec": 2.0 * fst.rec_steps_executed * batch + 5.0 * fst.rec_steps_executed,
+                 "inv_rec": 2.0 * ist.rec_steps_executed * batch + 5.0 * ist.rec_steps_executed}
     # nominal 5 L log2 L flop per complex FFT of length L executed (fft_points
     # counts L log2 L per FFT: one forward per input tile, one inverse per output tile, per term)
     fft_flops = {"fwd": 5.0 * fst.fft_points_per_vector * batch, "inv": 5.0 * ist.fft_points_per_vector * batch}
@@ -706,7 +707,7 @@ def run_ours5(args, wl):
     for g in range(len(rp.keys)):
         for k in range(2):
             s_ = rp.plans[g][k].device_plan(local).stats()
-            rec_flops += 2.0 * s_.rec_steps * rp.sizes[g] + 5.0 * s_.rec_steps
+            rec_flops += 2.0 * s_.rec_steps_executed * rp.sizes[g] + 5.0 * s_.rec_steps_executed
     rec_ms = stage_ms["fwd_rec"] + stage_ms["inv_rec"]
     achieved = rec_flops / (rec_ms * 1e-3) / 1e12
     roofline = {"bound": "fp64", "bound_note": BOUND_NOTE, "kernel": "k_rec_gemm / k_rec_*_ws (K1+K2, all groups)", "stage": "fwd_rec+inv_rec",

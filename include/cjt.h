@@ -105,6 +105,8 @@ typedef struct {
     int64_t reserved_batch;
     double rec_flops_per_vector;    /* 2 flop per (row, degree) contraction */
     double fft_points_per_vector;   /* sum over executed FFTs of length x log2(length) */
+    int64_t rec_steps_executed;     /* (row, degree) pairs the contractions execute: rec_steps,
+                                       or the rows i <= G/2 only for parity-folded plans */
 } cjt_plan_stats;
 
 int cjt_version(void);

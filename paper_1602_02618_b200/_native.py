@@ -51,6 +51,7 @@ class PlanStats(ctypes.Structure):
         ("launches_per_execute", _i64), ("rec_steps", _i64), ("checkpoint_bytes", _i64),
         ("workspace_bytes", _i64), ("reserved_batch", _i64),
         ("rec_flops_per_vector", ctypes.c_double), ("fft_points_per_vector", ctypes.c_double),
+        ("rec_steps_executed", _i64),
     ]
 
 

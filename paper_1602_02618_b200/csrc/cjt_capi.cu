@@ -930,7 +930,13 @@ int cjt_plan_stats_get(const cjt_plan* plan, cjt_plan_stats* s) {
   s->checkpoint_bytes = plan->ck_count * 16;
   s->workspace_bytes = plan->workspace_bytes;
   s->reserved_batch = plan->reserved;
-  s->rec_flops_per_vector = 2.0 * (double)plan->rec_steps;
+  int64_t executed = plan->rec_steps;
+  if (plan->fold) {
+    executed = 0;
+    for (int64_t i = 0; i < plan->nrows_fold; ++i) executed += plan->h_cut[i];
+  }
+  s->rec_steps_executed = executed;
+  s->rec_flops_per_vector = 2.0 * (double)executed;
   s->fft_points_per_vector = plan->fft_points;
   return CJT_OK;
 }

@@ -55,7 +55,7 @@ class RaggedPlan:
         """Relative cost of group g (recurrence steps and Bluestein points, per vector)."""
         fp, ip = self.plans[g]
         fs, is_ = fp.device_plan().stats(), ip.device_plan().stats()
-        return self.sizes[g] * sharding.plan_cost_model(fs.rec_steps, is_.rec_steps,
+        return self.sizes[g] * sharding.plan_cost_model(fs.rec_steps_executed, is_.rec_steps_executed,
                                                         fs.fft_points_per_vector,
                                                         is_.fft_points_per_vector)
 
