@@ -26,6 +26,14 @@
  *   cjt_host_angles      the libm cos / half-angle evaluation the reference
  *        kernel performs per point (_kernels_cy.pyx:27,58-64), exposed so
  *        plans carry bit-identical x and x -+ 1 values.
+ *   cjt_jacobi_shift     engine.increment_beta / decrement_beta /
+ *        increment_alpha / decrement_alpha (engine.py:239-288), batched.
+ *   cjt_clenshaw_points_dev / cjt_clenshaw_smith_points / cjt_jacobi_values
+ *        recurrences.evaluate_expansion (batched), clenshaw_smith[_reinsch],
+ *        jacobi_forward[_reinsch] (recurrences.py:74-171).
+ *   cjt_chirpz_create / _execute / _destroy   trig.TrigPlanWorkspace.dct1 /
+ *        dst1_bordered / chebyshev_synthesis / chebyshev_analysis
+ *        (trig.py:35-63), batched.
  */
 #ifndef CJT_B200_H
 #define CJT_B200_H
