@@ -1,15 +1,18 @@
 """Benchmark: forward + inverse CJT throughput (coefficients/s, fp64) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
 
 One step = forward then inverse transform of one batch of seeded synthetic
 coefficient vectors; value = coefficients pushed through
-fwd+inv per second over all ranks.  Default workload: BASELINE.json configs[1]
-(alpha=-0.25, beta=0.4, N=2^14-1, 64 vectors per GPU; weak scaling across
-GPUs).  Inputs are resident in HBM for `value`; `e2e` goes through the public
-batched API with pinned host arrays (H2D and D2H inside the timed region).
-`--impl reference` times the unmodified reference (oracle/_ref, Cython
-backend) on the host cores instead.
+fwd+inv per second over all ranks.  Default workload: the headline
+configuration the "1/2/4/8 B200" metric is quoted on, BASELINE.json
+configs[2] (alpha = beta = 1/2, N = 4095, a fixed batch of 8192 vectors split
+into contiguous slices over the GPUs: strong scaling).
+`--gpus N` outside torchrun re-launches itself as N ranks.  Inputs are
+resident in HBM for `value`; `e2e` goes through the public batched API with
+pinned host arrays (H2D and D2H inside the timed region).  `--impl reference`
+times the unmodified reference (oracle/_ref, Cython backend) on the host
+cores instead (rank 0 only).
 """
 
 from __future__ import annotations
@@ -53,8 +56,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=None, help="vectors per GPU (default: the config's)")
+    ap.add_argument("--config", type=int, default=3, choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None,
+                    help="global batch, split over the GPUs (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -163,11 +167,12 @@ def sample_size(arm, target_cpu_seconds):
     return int(math.ceil(n / arm.cores) * arm.cores)
 
 
-def config_json(wl, config, batch, world, scaling):
+def config_json(wl, config, total, world):
+    """The workload identity, identical in both arms (ours and --impl reference)."""
     return {"workload": f"config{config}: fwd+inv CJT alpha={wl['alpha']} beta={wl['beta']} "
-                        f"N={wl['n']} batch={batch}/GPU c_n=z_n*{wl['env']}",
-            "alpha": wl["alpha"], "beta": wl["beta"], "N": wl["n"], "global_batch": batch * world,
-            "batch_per_gpu": batch, "m_terms": 7, "parallelism": f"batch-sharded x{world}",
+                        f"N={wl['n']} batch={total} c_n=z_n*{wl['env']}",
+            "alpha": wl["alpha"], "beta": wl["beta"], "N": wl["n"], "global_batch": total,
+            "m_terms": 7, "parallelism": f"contiguous batch slices x{world} (SURVEY.md 8(e))",
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -186,8 +191,8 @@ def run_reference(args, wl):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
-        "config": config_json(wl, args.config, wl["batch"], 1, "weak"), "impl": "reference",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
+        "config": config_json(wl, args.config, args.batch or wl["batch"], world), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                          "sample": f"{nvec} vectors fwd+inv per step (bounded sample of config{args.config}), "
                                    f"multiprocessing over {arm.cores} host cores, plans untimed"},
@@ -198,38 +203,6 @@ def run_reference(args, wl):
 
 # ---------------------------------------------------------------------------
 # clocks
-
-
-def survey_flops(fhost, ihost, batch: int) -> float:
-    """Algorithmic flops of one forward + inverse of `batch` vectors by the
-    SURVEY.md 8(d) model F (the reference's own per-step constants and
-    layout; a build doing fewer real flops still uses this F):
-      B [6 S_f^int + 8 S_f^end + 2 (S_i^int + S_i^end)
-         + (2 M K_f + 1) 2.5 N log2 N + (2 M K_i + 1) 2.5 (2N) log2 (2N)]
-      + 5 S_i^int + 7 S_i^end      (diagonal scalings, < 2 %, omitted)."""
-    n = fhost.n
-    m = fhost.m_terms
-    fr, fc = fhost.regions, fhost.cuts.astype(np.float64)
-    ir, ic = ihost.regions, np.minimum(ihost.cuts, n + 1).astype(np.float64)
-    sf_int, sf_end = fc[fr == 0].sum(), fc[fr != 0].sum()
-    si_int, si_end = ic[ir == 0].sum(), ic[ir != 0].sum()
-    kf, ki = len(fhost.layout.blocks), len(ihost.layout.blocks)
-    fft = ((2 * m * kf + 1) * 2.5 * n * math.log2(n) if n > 1 else 0.0) \
-        + (2 * m * ki + 1) * 2.5 * (2 * n) * math.log2(2 * n)
-    per_vec = 6 * sf_int + 8 * sf_end + 2 * (si_int + si_end) + fft
-    return batch * per_vec + 5 * si_int + 7 * si_end
-
-
-def step_roofline(flop: float, peak_tflops: float, ms_per_step: float, coeffs: float) -> dict:
-    t_ms = flop / (peak_tflops * 1e12) * 1e3
-    t_hbm_ms = 32.0 * coeffs / 6.5546e12 * 1e3   # read c, write c per direction (SURVEY 8(d) bytes)
-    t_roof = max(t_ms, t_hbm_ms)
-    return {"model": "SURVEY.md 8(d) F: the reference's algorithmic fp64 flops per step",
-            "flop_per_step": float(flop), "t_fp64_ms": float(t_ms), "t_hbm_ms": float(t_hbm_ms),
-            "roofline_coeffs_per_s": float(coeffs / (t_roof * 1e-3)),
-            # capped at 1 (SURVEY 8(d)): the DMMA contraction does fewer real
-            # flops than the reference's per-vector Clenshaw chains
-            "frac": float(min(1.0, t_roof / ms_per_step)), "frac_uncapped": float(t_roof / ms_per_step)}
 
 
 class ClockSampler:
@@ -297,12 +270,134 @@ class ClockSampler:
 # GPU arm
 
 
+def stage_model(fhost, ihost, batch: int) -> dict:
+    """SURVEY.md 8(d) algorithmic work per stage of one forward + inverse of
+    `batch` vectors: flops with the reference's own per-step constants and
+    layout (a build doing fewer real flops still uses these), and the
+    compulsory HBM bytes of each stage (read its input vectors, write its
+    output vectors, f64):
+      fwd_rec    B (6 S_f^int + 8 S_f^end)                 bytes B 8 ((N+1) + (G_f+1))
+      fwd_blocks B 2 M K_f 2.5 N log2 N                    bytes B 8 ((N+1) + 2 (G_f+1))
+      fwd_edge   B 2.5 N log2 N                            bytes B 8 ((G_f+1) + (N+1))
+      inv_edge   B 2.5 (2N) log2 (2N)                      bytes B 8 ((N+1) + (G_i+1))
+      inv_blocks B 2 M K_i 2.5 (2N) log2 (2N)              bytes B 8 ((G_i+1) + (N+1))
+      inv_rec    B 2 (S_i^int + S_i^end) + 5 S_i^int + 7 S_i^end
+                                                           bytes B 8 ((G_i+1) + 2 (N+1))
+    with S_f = sum of forward row cuts per region, S_i = sum of inverse row
+    cuts capped at N+1 (degrees > N are discarded by the reference)."""
+    n, m = fhost.n, fhost.m_terms
+    fr, fc = fhost.regions, fhost.cuts.astype(np.float64)
+    ir, ic = ihost.regions, np.minimum(ihost.cuts, n + 1).astype(np.float64)
+    sf_int, sf_end = fc[fr == 0].sum(), fc[fr != 0].sum()
+    si_int, si_end = ic[ir == 0].sum(), ic[ir != 0].sum()
+    kf, ki = len(fhost.layout.blocks), len(ihost.layout.blocks)
+    nlog = n * math.log2(n) if n > 1 else 0.0
+    n2log = 2 * n * math.log2(2 * n)
+    gf1, gi1, n1 = fhost.grid_n + 1, ihost.grid_n + 1, n + 1
+    flops = {
+        "fwd_rec": batch * (6 * sf_int + 8 * sf_end),
+        "fwd_blocks": batch * 2 * m * kf * 2.5 * nlog,
+        "fwd_edge": batch * 2.5 * nlog,
+        "inv_edge": batch * 2.5 * n2log,
+        "inv_blocks": batch * 2 * m * ki * 2.5 * n2log,
+        "inv_rec": batch * 2 * (si_int + si_end) + 5 * si_int + 7 * si_end,
+    }
+    nbytes = {
+        "fwd_rec": batch * 8.0 * (n1 + gf1),
+        "fwd_blocks": batch * 8.0 * (n1 + 2 * gf1) if kf else 0.0,
+        "fwd_edge": batch * 8.0 * (gf1 + n1),
+        "inv_edge": batch * 8.0 * (n1 + gi1),
+        "inv_blocks": batch * 8.0 * (gi1 + n1) if ki else 0.0,
+        "inv_rec": batch * 8.0 * (gi1 + 2 * n1),
+    }
+    return {"flops": flops, "bytes": nbytes}
+
+
+def survey_flops(fhost, ihost, batch: int) -> float:
+    """SURVEY.md 8(d) F of one forward + inverse step (sum over the stages;
+    the diagonal scalings, < 2 %, are omitted)."""
+    return float(sum(stage_model(fhost, ihost, batch)["flops"].values()))
+
+
+def step_roofline(flop: float, peak_tflops: float, ms_per_step: float, coeffs: float) -> dict:
+    t_ms = flop / (peak_tflops * 1e12) * 1e3
+    t_hbm_ms = 32.0 * coeffs / 6.5546e12 * 1e3   # read c, write c per direction (SURVEY 8(d) bytes)
+    t_roof = max(t_ms, t_hbm_ms)
+    return {"model": "SURVEY.md 8(d) F: the reference's algorithmic fp64 flops per step",
+            "flop_per_step": float(flop), "t_fp64_ms": float(t_ms), "t_hbm_ms": float(t_hbm_ms),
+            "roofline_coeffs_per_s": float(coeffs / (t_roof * 1e-3)),
+            # capped at 1 (SURVEY 8(d)): the DMMA contraction does fewer real
+            # flops than the reference's per-vector Clenshaw chains
+            "frac": float(min(1.0, t_roof / ms_per_step)), "frac_uncapped": float(t_roof / ms_per_step)}
+
+
+def dominant_roofline(stages_ms: dict, model: dict, executed: dict, peak: float, config: int) -> dict:
+    """roofline object of the dominant stage (longest CUDA-event time):
+    achieved = its SURVEY 8(d) algorithmic flops / its time, frac = achieved /
+    measured fp64 peak (capped at 1, uncapped kept); the executed-flop rate and
+    pipe fraction are reported beside it, and ncu's DRAM bytes of one
+    execution of the stage over its compulsory bytes."""
+    dom = max(stages_ms, key=stages_ms.get)
+    t = stages_ms[dom] * 1e-3
+    alg = model["flops"][dom]
+    achieved = alg / t / 1e12
+    kern = {"fwd_rec": "k_rec_forward_ws / k_pgen_fwd + k_rec_gemm (K1)",
+            "inv_rec": "k_rec_inverse_ws / k_pgen_inv + k_rec_gemm (K2)"}.get(
+        dom, "k_chirpz_* (Bluestein chirp-z, K3/K4)")
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            t_ = json.loads(prof.read_text()).get(f"config{config}", {}).get(dom)
+            traffic = None if t_ is None else float(t_["bytes"])
+        except (ValueError, OSError, KeyError, TypeError):
+            traffic = None
+    ex = executed.get(dom)
+    ab = model["bytes"][dom]
+    return {
+        "bound": "fp64", "bound_note": BOUND_NOTE, "kernel": kern, "stage": dom,
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": min(1.0, achieved / peak) if peak else None,
+        "frac_uncapped": achieved / peak if peak else None,
+        "traffic": traffic,
+        "traffic_note": "ncu dram__bytes_read+write of one execution of this stage (profiles/ncu_traffic.json)",
+        "algorithmic_flop": alg, "algorithmic_bytes": ab,
+        "traffic_over_algorithmic_bytes": (traffic / ab) if (traffic and ab) else None,
+        "flops_model": "SURVEY.md 8(d) per-stage algorithmic flops (bench.stage_model)",
+        "executed": None if ex is None else {
+            "flop": ex, "tflops": ex / t / 1e12, "pipe_frac": ex / t / 1e12 / peak if peak else None,
+            "note": "flops the kernels actually execute (contraction 2 per row x degree x vector + "
+                    "generation; FFT 5 L log2 L per complex FFT executed)"},
+        "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains); nominal 37.2",
+        "nominal_peak": NOMINAL_FP64_TFLOPS,
+        "stage_ms": {k: round(v, 4) for k, v in stages_ms.items()},
+        "stage_share": {k: round(v / sum(stages_ms.values()), 4) for k, v in stages_ms.items()},
+    }
+
+
+def shard_batch(config: int, n: int, total: int, world: int, rank: int) -> tuple[int, int, np.ndarray]:
+    """This rank's contiguous slice [lo, hi) of the config's fixed seeded batch
+     and its input vectors."""
+    import cjt_oracle as O
+    from paper_1602_02618_b200 import sharding
+    lo, hi = sharding.contiguous_slice(total, world, rank)
+    if hi <= lo:
+        return lo, hi, np.zeros((0, n + 1))
+    return lo, hi, np.stack([O.seeded_vector(config, v, n) for v in range(lo, hi)])
+
+
+def roundtrip_stats(c, back):
+    """Per-vector round-trip error max|inv(fwd(c)) - c| / ||c||_1 (a (rows, 1) tensor)."""
+    return ((back - c).abs().amax(dim=1) / c.abs().sum(dim=1)).unsqueeze(1)
+
+
 def run_ours(args, wl):
     import torch
     import torch.distributed as dist
 
     import paper_1602_02618_b200 as cj
     from paper_1602_02618_b200 import _native as nat
+    from paper_1602_02618_b200 import sharding
     import cjt_oracle as O
 
     rank, local, world = dist_env()
@@ -310,13 +405,16 @@ def run_ours(args, wl):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    batch = args.batch or wl["batch"]
+    total = args.batch or wl["batch"]
     n1 = wl["n"] + 1
     p = cj.JacobiParameters(wl["alpha"], wl["beta"])
     fp = cj.plan("forward", p, wl["n"])
     ip = cj.plan("inverse", p, wl["n"])
-    # weak scaling: rank r owns vectors [r*batch, (r+1)*batch) of the seeded stream
-    c_host = np.stack([O.seeded_vector(args.config, rank * batch + v, wl["n"]) for v in range(batch)])
+    # strong scaling: the config's fixed batch, contiguous slices per rank
+    lo, hi, c_host = shard_batch(args.config, wl["n"], total, world, rank)
+    batch = hi - lo
+    if batch < 1:
+        raise SystemExit(f"rank {rank}: empty shard (batch {total} over {world} GPUs)")
     c_dev = torch.from_numpy(c_host).to(dev)
     cheb = torch.empty_like(c_dev)
     back = torch.empty_like(c_dev)
@@ -363,6 +461,13 @@ def run_ours(args, wl):
             dist.barrier()
         return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     # one step captured into a CUDA graph (stream-ordered, allocation-free
     # executes), replayed per timed step: launch overhead off the small configs
     graph = None
@@ -392,18 +497,19 @@ def run_ours(args, wl):
 
     with ClockSampler(local) as clk:
         step_ms = timed(run_step, args.steps)
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = world * batch * n1 / (ms_per_step * 1e-3)
+    ms_per_step = max_over_ranks(sum(step_ms)) / args.steps
+    value = total * n1 / (ms_per_step * 1e-3)
 
     if args.profile:
         if rank == 0:
             print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step}), flush=True)
         return
+
+    # coverage of the sharded batch (after timing): every rank's per-vector
+    # round-trip errors, reassembled in global vector order
+    rt = sharding.gather_rows(roundtrip_stats(c_dev, back), total, world, rank)
+    coverage = {"vectors": int(rt.shape[0]), "global_batch": total,
+                "max_roundtrip": float(rt.max()), "slice_rank0": [0, sharding.contiguous_slice(total, world, 0)[1]]}
 
     # correctness spot check of the timed output against the oracle (not timed)
     chk = None
@@ -414,7 +520,7 @@ def run_ours(args, wl):
             ref_i = O.oracle_inverse(wl["alpha"], wl["beta"], ref_f)
             chk = {"fwd": O.parity(cheb[v].cpu().numpy(), ref_f, c_host[v]),
                    "inv": O.parity(back[v].cpu().numpy(), ref_i, c_host[v]),
-                   "roundtrip": O.parity(back[v].cpu().numpy(), c_host[v], c_host[v])}
+                   "oracle_plans": O.plan_source()}
 
     # per-stage timing -> dominant kernel and its roofline
     L = nat.lib()
@@ -432,41 +538,16 @@ def run_ours(args, wl):
     torch.cuda.synchronize(dev)
     peak = ctypes_peak(L, st)
     fst, ist = fdp.stats(), idp.stats()
-    # executed contraction work (parity-folded plans contract half the rows)
-    rec_flops = {"fwd_rec": 2.0 * fst.rec_steps_executed * batch + 5.0 * fst.rec_steps_executed,
-                 "inv_rec": 2.0 * ist.rec_steps_executed * batch + 5.0 * ist.rec_steps_executed}
-    # nominal 5 L log2 L flop per complex FFT of length L executed (fft_points
-    # counts L log2 L per FFT: one forward per input tile, one inverse per output tile, per term)
-    fft_flops = {"fwd": 5.0 * fst.fft_points_per_vector * batch, "inv": 5.0 * ist.fft_points_per_vector * batch}
-    dom = max(stages, key=stages.get)
-    if dom.endswith("rec"):
-        flops = rec_flops[dom]
-        kern = "k_rec_forward (K1)" if dom.startswith("fwd") else "k_rec_inverse (K2)"
-        unit_note = "2 flop per (point, degree, vector) contraction + 5 flop per (point, degree) generation"
-    else:
-        d = dom.split("_")[0]
-        share = stages[dom] / (stages[f"{d}_blocks"] + stages[f"{d}_edge"])
-        flops = fft_flops[d] * share
-        kern = "k_chirpz_* (Bluestein chirp-z)"
-        unit_note = "5 L log2 L flop per complex FFT executed (per term: one forward FFT per input tile, one inverse per output tile)"
-    achieved = flops / (stages[dom] * 1e-3) / 1e12
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists():
-        try:
-            t_ = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
-            traffic = None if t_ is None else t_["bytes"]   # DRAM bytes of one stage execution (ncu)
-        except (ValueError, OSError, KeyError, TypeError):
-            traffic = None
-    roofline = {"bound": "fp64", "bound_note": BOUND_NOTE, "kernel": kern, "stage": dom, "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
-                "traffic_note": "ncu dram__bytes_read+write of one execution of this stage (profiles/ncu_traffic.json)",
-                "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains)",
-                "nominal_peak": NOMINAL_FP64_TFLOPS, "flops_model": unit_note,
-                "stage_ms": {k: round(v, 4) for k, v in stages.items()},
-                "stage_share": {k: round(v / sum(stages.values()), 4) for k, v in stages.items()}}
-
-    roofline["step"] = step_roofline(survey_flops(fp.host, ip.host, batch), peak, ms_per_step,
+    executed = {"fwd_rec": 2.0 * fst.rec_steps_executed * batch + 5.0 * fst.rec_steps_executed,
+                "inv_rec": 2.0 * ist.rec_steps_executed * batch + 5.0 * ist.rec_steps_executed}
+    for d, s_ in (("fwd", fst), ("inv", ist)):
+        both = stages[f"{d}_blocks"] + stages[f"{d}_edge"]
+        for sname in ("blocks", "edge"):
+            share = stages[f"{d}_{sname}"] / both if both > 0 else 0.0
+            executed[f"{d}_{sname}"] = 5.0 * s_.fft_points_per_vector * batch * share
+    model = stage_model(fp.host, ip.host, batch)
+    roofline = dominant_roofline(stages, model, executed, peak, args.config)
+    roofline["step"] = step_roofline(survey_flops(fp.host, ip.host, batch), peak, sum(step_ms) / args.steps,
                                      float(batch * n1))
 
     # e2e through the public API: pinned host input -> pipeline(forward, inverse)
@@ -475,7 +556,6 @@ def run_ours(args, wl):
     if not args.no_e2e:
         pin_in = torch.from_numpy(c_host).pin_memory()
         pin_outs = [torch.empty_like(pin_in).pin_memory() for _ in range(2)]
-        pin_out = pin_outs[0]
         chunk = max(batch // 4, min(batch, 64))
         # every step: H2D of its inputs, forward, inverse, D2H of its results;
         # steps are streamed (pipeline(sync=False) alternates 2 CUDA streams),
@@ -483,24 +563,22 @@ def run_ours(args, wl):
         for w_ in range(2):
             cj.pipeline((fp, ip), pin_in, pin_outs[w_], chunk=chunk, streams=2, device=local, sync=False)
         torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for k_ in range(args.steps):
             cj.pipeline((fp, ip), pin_in, pin_outs[k_ % 2], chunk=chunk, streams=2, device=local, sync=False)
         torch.cuda.synchronize(dev)
-        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
         pin_out = pin_outs[(args.steps - 1) % 2]
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
         nbytes = batch * n1 * 8
         ok = bool(np.array_equal(pin_out.numpy(), back.cpu().numpy())) if chunk == batch else None
-        e2e = {"value": world * batch * n1 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+        e2e = {"value": total * n1 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "chunk": chunk, "matches_device_path": ok,
                "path": "paper_1602_02618_b200.pipeline((fwd_plan, inv_plan), pinned host in, pinned host out, "
                        "sync=False) per step: H2D, forward, inverse, D2H per chunk, chunks and steps "
                        "alternating over 2 streams, one synchronize after the K steps; host wall clock "
-                       "per step, max over ranks",
+                       "per step, max over ranks (bytes are per rank)",
                "note": "streamed steps overlap on the two streams, so e2e can exceed the single-stream "
                        "device value (which serialises steps); every step still copies its inputs in and "
                        "its results out"}
@@ -518,11 +596,12 @@ def run_ours(args, wl):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md 8(d))",
-            "config": dict(config_json(wl, args.config, batch, world, "weak"), cuda_graph=graph is not None),
+            "config": config_json(wl, args.config, total, world),
+            "cuda_graph": graph is not None,
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roofline,
-            "cpu_baseline": cpu, "e2e": e2e, "parity_check_vector0": chk,
+            "cpu_baseline": cpu, "e2e": e2e, "parity_check_vector0": chk, "coverage": coverage,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -767,8 +846,23 @@ def run_ours5(args, wl):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     wl = WORKLOADS[args.config]
     if args.config == 5:
         (run_reference5 if args.impl == "reference" else run_ours5)(args, wl)

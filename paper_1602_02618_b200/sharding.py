@@ -46,3 +46,27 @@ def plan_cost_model(rec_steps_fwd: int, rec_steps_inv: int, fft_points_fwd: floa
     """Relative per-vector cost of forward+inverse from the device plan
     statistics (contraction steps and Bluestein points)."""
     return 2.0 * (rec_steps_fwd + rec_steps_inv) + 2.5 * (fft_points_fwd + fft_points_inv)
+
+
+def gather_rows(local, total: int, world: int, rank: int):
+    """All-gather per-rank row blocks [lo, hi) = contiguous_slice(total, world,
+    rank) of a (rows, ...) tensor into the full (total, ...) tensor, in global
+    row order, on every rank (torch.distributed; any backend).  The only
+    collective of the sharded path, used after timing stops."""
+    import torch
+    import torch.distributed as dist
+    lo, hi = contiguous_slice(total, world, rank)
+    if local.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} holds {local.shape[0]} rows, its slice is [{lo}, {hi})")
+    if world == 1:
+        return local
+    width = max(b - a for a, b in (contiguous_slice(total, world, r) for r in range(world)))
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: hi - lo] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    parts = []
+    for r in range(world):
+        a, b = contiguous_slice(total, world, r)
+        parts.append(bufs[r][: b - a])
+    return torch.cat(parts, dim=0)

@@ -82,3 +82,28 @@ def test_seeded_inputs():
     assert np.array_equal(c, z * (np.arange(101) + 1.0) ** -1.5)
     draws = O.config5_draws(32)
     assert len(draws) == 32 and all(n in {(1 << k) - 1 for k in range(8, 17)} for _, _, n in draws)
+
+
+def test_oracle_plans_come_from_the_reference():
+    """With oracle/_ref present the oracle takes every plan table from the
+    reference's own planner (engine.plan + _block_diagonals), so it shares no
+    code with the product; the product-planner fallback must agree bit for bit."""
+    if O.reference_package() is None:
+        pytest.skip("oracle/_ref (the built reference) is not present")
+    assert O.plan_source() == "reference"
+    g = load_golden("cfg2_small")
+    a, b = float(g["alpha"]), float(g["beta"])
+    O._plan.cache_clear()
+    f_ref, i_ref = O.oracle_forward(a, b, g["c"][0]), O.oracle_inverse(a, b, g["fwd"][0])
+    assert O._plan("forward", a, b, int(g["n"]), 7, O.DEFAULT_EPS).source == "reference"
+    real = O.reference_package
+    try:
+        O.reference_package = lambda: None
+        O._plan.cache_clear()
+        assert O.plan_source() == "product-planner"
+        f_pl, i_pl = O.oracle_forward(a, b, g["c"][0]), O.oracle_inverse(a, b, g["fwd"][0])
+        assert O._plan("forward", a, b, int(g["n"]), 7, O.DEFAULT_EPS).source == "product-planner"
+    finally:
+        O.reference_package = real
+        O._plan.cache_clear()
+    assert np.array_equal(f_ref, f_pl) and np.array_equal(i_ref, i_pl)

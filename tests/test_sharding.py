@@ -1,5 +1,7 @@
-"""Multi-GPU batch sharding: pure host logic plus a world_size-2 gloo run of the
-same per-rank path bench.py uses (shard, compute locally, max-reduce timing)."""
+"""Multi-GPU batch sharding: pure host logic, plus world_size-2 gloo runs of
+the collective helpers and of bench.py's per-rank path (contiguous slice of the
+fixed seeded batch, local forward+inverse with the CPU oracle standing in for
+the device, in-order reassembly, max-reduced timing)."""
 import os
 import socket
 
@@ -42,6 +44,52 @@ def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def _bench_rank(rank, world, port, q):
+    """bench.py's per-rank data path with the CPU oracle standing in for the
+    device: contiguous slice of the fixed seeded batch, local forward+inverse,
+    reassembly in global vector order (sharding.gather_rows), max-reduced time."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    import bench
+    import cjt_oracle as O
+    config, n, total = 3, 63, 7
+    lo, hi, c = bench.shard_batch(config, n, total, world, rank)
+    a = b = 0.5
+    cheb = np.stack([O.oracle_forward(a, b, v) for v in c])
+    back = np.stack([O.oracle_inverse(a, b, v) for v in cheb])
+    ct, bt = torch.from_numpy(c), torch.from_numpy(back)
+    full_c = sharding.gather_rows(ct, total, world, rank)
+    full_cheb = sharding.gather_rows(torch.from_numpy(cheb), total, world, rank)
+    stats = sharding.gather_rows(bench.roundtrip_stats(ct, bt), total, world, rank)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        q.put((lo, hi, full_c.numpy(), full_cheb.numpy(), stats.numpy(), t.item()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_bench_rank_logic():
+    import cjt_oracle as O
+    ctx = tmp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    lo, hi, full_c, full_cheb, stats, tmax = q.get()
+    assert (lo, hi) == (0, 4)          # rank 0 owns the first ceil(7/2) vectors
+    # disjoint, complete coverage of the seeded stream, reassembled in order
+    want = np.stack([O.seeded_vector(3, v, 63) for v in range(7)])
+    assert np.array_equal(full_c, want)
+    assert np.array_equal(full_cheb, np.stack([O.oracle_forward(0.5, 0.5, v) for v in want]))
+    assert stats.shape == (7, 1) and float(stats.max()) < 1e-12
+    assert tmax == 2.0
 
 
 def _worker(rank, world, port, q):
