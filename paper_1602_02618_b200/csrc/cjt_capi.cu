@@ -108,6 +108,14 @@ struct cjt_plan {
   };
   std::map<cudaStream_t, Workspace> ws;
   std::mutex ws_mu;
+  // serialises execute / reserve of one plan across host threads (the
+  // enqueue only; kernels of different streams still overlap), so growing
+  // the batch-dependent state never races a launch reading it
+  std::mutex exec_mu;
+  // set once an execution was recorded into a CUDA graph: from then on the
+  // batch-dependent buffers are frozen (a growth would free memory the graph
+  // still references), and a larger batch is an error
+  bool captured = false;
   int64_t workspace_bytes = 0;
   int64_t last_launches = 0;
   int vt = 64;
@@ -346,6 +354,7 @@ int64_t pgen_chunk_budget() {
 struct Arena {
   void* ptr = nullptr;
   int64_t bytes = 0;
+  bool captured = false;   // referenced by a CUDA graph: never freed or grown
 };
 std::map<std::pair<int, cudaStream_t>, Arena>& arenas() {
   static std::map<std::pair<int, cudaStream_t>, Arena> m;
@@ -358,11 +367,14 @@ std::mutex& arena_mutex() {
 int arena_get(int device, cudaStream_t st, int64_t need, double** out) {
   std::lock_guard<std::mutex> lk(arena_mutex());
   Arena& a = arenas()[{device, st}];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
   if (a.bytes < need) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone)
       return fail(CJT_EINVAL, "P workspace arena must be grown before graph capture (run once uncaptured)");
+    if (a.captured)
+      return fail(CJT_EINVAL, "P workspace arena of this stream is referenced by a captured CUDA graph and "
+                              "cannot grow; execute the largest plan on this stream before capturing");
     CJT_CUDA_TRY(cudaStreamSynchronize(st));
     if (a.ptr) cudaFree(a.ptr);
     a.ptr = nullptr;
@@ -374,6 +386,7 @@ int arena_get(int device, cudaStream_t st, int64_t need, double** out) {
     }
     a.bytes = need;
   }
+  if (cs != cudaStreamCaptureStatusNone) a.captured = true;
   *out = (double*)a.ptr;
   return CJT_OK;
 }
@@ -616,8 +629,13 @@ void free_workspace(cjt_plan* P) {
   P->workspace_bytes = 0;
 }
 
+// caller holds P->exec_mu
 int reserve(cjt_plan* P, int64_t batch) {
   if (batch <= P->reserved) return CJT_OK;
+  if (P->captured)
+    return fail(CJT_EINVAL, "plan is referenced by a captured CUDA graph (reserved batch " +
+                                std::to_string(P->reserved) + "); growing it to " + std::to_string(batch) +
+                                " would free buffers the graph uses: reserve the largest batch before capture");
   CJT_CUDA_TRY(cudaDeviceSynchronize());
   free_workspace(P);
   {
@@ -702,6 +720,11 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
 // synthesis chirp-z).  Partial masks are for timing individual kernels only.
 int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStream_t st,
             int stages = CJT_STAGE_ALL) {
+  {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) P->captured = true;
+  }
   cjt_plan::Workspace* Wp = nullptr;
   if (int rc = get_workspace(P, st, &Wp)) return rc;
   cjt_plan::Workspace& W = *Wp;
@@ -919,6 +942,7 @@ int cjt_plan_reserve(cjt_plan* plan, int64_t max_batch) {
   if (!plan) return fail(CJT_EINVAL, "null plan");
   if (max_batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
   DeviceGuard g(plan->device);
+  std::lock_guard<std::mutex> lk(plan->exec_mu);
   return reserve(plan, max_batch);
 }
 
@@ -941,19 +965,29 @@ int cjt_plan_stats_get(const cjt_plan* plan, cjt_plan_stats* s) {
   return CJT_OK;
 }
 
+// vectors per execution chunk: per-vector grid dimensions (y / z) stay <= 65535
+constexpr int64_t kMaxChunk = 65535;
+
 int cjt_execute(cjt_plan* plan, const double* in, double* out, int64_t batch, void* stream) {
   if (!plan || !in || !out) return fail(CJT_EINVAL, "null argument");
   if (batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
   DeviceGuard g(plan->device);
-  if (int rc = reserve(plan, batch)) return rc;
-  return execute(plan, in, out, batch, (cudaStream_t)stream);
+  std::lock_guard<std::mutex> lk(plan->exec_mu);
+  if (int rc = reserve(plan, std::min(batch, kMaxChunk))) return rc;
+  const int64_t n1 = plan->n + 1;
+  for (int64_t b0 = 0; b0 < batch; b0 += kMaxChunk) {
+    const int64_t nb = std::min(kMaxChunk, batch - b0);
+    if (int rc = execute(plan, in + b0 * n1, out + b0 * n1, nb, (cudaStream_t)stream)) return rc;
+  }
+  return CJT_OK;
 }
 
 int cjt_execute_stage(cjt_plan* plan, const double* in, double* out, int64_t batch, int32_t stages,
                       void* stream) {
   if (!plan || !in || !out) return fail(CJT_EINVAL, "null argument");
-  if (batch < 1 || batch > plan->reserved) return fail(CJT_EINVAL, "batch must be in [1, reserved]");
   DeviceGuard g(plan->device);
+  std::lock_guard<std::mutex> lk(plan->exec_mu);
+  if (batch < 1 || batch > plan->reserved) return fail(CJT_EINVAL, "batch must be in [1, reserved]");
   return execute(plan, in, out, batch, (cudaStream_t)stream, stages);
 }
 
@@ -994,14 +1028,20 @@ int cjt_execute_host(cjt_plan* plan, const double* in_host, double* out_host, in
   if (!plan || !in_host || !out_host) return fail(CJT_EINVAL, "null argument");
   if (batch < 1) return fail(CJT_EINVAL, "batch must be >= 1");
   DeviceGuard g(plan->device);
-  if (int rc = reserve(plan, batch)) return rc;
+  std::lock_guard<std::mutex> lk(plan->exec_mu);
+  const int64_t chunk = std::min(batch, kMaxChunk);
+  if (int rc = reserve(plan, chunk)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cjt_plan::Workspace* W = nullptr;
   if (int rc = get_workspace(plan, st, &W)) return rc;
-  const size_t bytes = (size_t)(batch * (plan->n + 1)) * 8;
-  CJT_CUDA_TRY(cudaMemcpyAsync(W->io_in, in_host, bytes, cudaMemcpyHostToDevice, st));
-  if (int rc = execute(plan, W->io_in, W->io_out, batch, st)) return rc;
-  CJT_CUDA_TRY(cudaMemcpyAsync(out_host, W->io_out, bytes, cudaMemcpyDeviceToHost, st));
+  const int64_t n1 = plan->n + 1;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int64_t nb = std::min(chunk, batch - b0);
+    const size_t bytes = (size_t)(nb * n1) * 8;
+    CJT_CUDA_TRY(cudaMemcpyAsync(W->io_in, in_host + b0 * n1, bytes, cudaMemcpyHostToDevice, st));
+    if (int rc = execute(plan, W->io_in, W->io_out, nb, st)) return rc;
+    CJT_CUDA_TRY(cudaMemcpyAsync(out_host + b0 * n1, W->io_out, bytes, cudaMemcpyDeviceToHost, st));
+  }
   CJT_CUDA_TRY(cudaStreamSynchronize(st));
   return CJT_OK;
 }

@@ -882,12 +882,12 @@ int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t l
               int64_t ldo, int64_t batch, double* part, double2* spec, cudaStream_t st, int* launches) {
   using Cfg = FusedCfg<LOGL>;
   static_assert(Cfg::NG == (LOGL >= 12 ? 1 : (1 << (12 - LOGL))), "fused_groups out of sync");
-  static bool init = false;
-  if (!init) {
+  static DeviceOnce once_;
+  if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(k_chirpz_fused<LOGL, false>, Cfg::SMEM)) return rc;
     if (int rc = set_smem(k_chirpz_fused<LOGL, true>, Cfg::SMEM)) return rc;
-    init = true;
-  }
+    return CJT_OK;
+  })) return rc_;
   const FusedSched sk = fused_sched(cz, batch);
   if (sk.streamk && batch > 65535) return fail(CJT_EINVAL, "chirp-z stream-K schedule out of range");
   if (cz.n_in > 1 && !spec) return fail(CJT_EINVAL, "chirp-z without spectrum workspace");
@@ -914,12 +914,12 @@ int run_cluster(const ChirpZDev& cz, const double2* tw, const double* x, int64_t
                 int64_t ldo, int64_t batch, cudaStream_t st) {
   using Cfg = ClusterCfg<LOGQ, P>;
   auto kern = k_chirpz_cluster<LOGQ, P>;
-  static bool init = false;
-  if (!init) {
+  static DeviceOnce once_;
+  if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(kern, Cfg::SMEM)) return rc;
     if (P > 8) CJT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    init = true;
-  }
+    return CJT_OK;
+  })) return rc_;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(P * batch));
   cfg.blockDim = dim3(Cfg::T);
@@ -940,11 +940,11 @@ template <int LOG1>
 int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_t ldx,
                  double2* buf, int64_t batch, cudaStream_t st) {
   using Cfg = ColCfg<LOG1>;
-  static bool init = false;
-  if (!init) {
+  static DeviceOnce once_;
+  if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(k_chirpz_cols_fwd<LOG1>, Cfg::SMEM)) return rc;
-    init = true;
-  }
+    return CJT_OK;
+  })) return rc_;
   const int64_t L2 = (int64_t)1 << cz.log2;
   if constexpr (LOG1 <= 5) {
     dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)(cz.n_in * cz.m_count));
@@ -961,13 +961,13 @@ int run_cols_fwd(const ChirpZDev& cz, const double2* tw, const double* x, int64_
 template <int LOG2>
 int run_rows(const ChirpZDev& cz, const double2* tw, double2* buf, int64_t batch, cudaStream_t st) {
   using Cfg = RowCfg<LOG2>;
-  static bool init = false;
-  if (!init) {
+  static DeviceOnce once_;
+  if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(k_chirpz_rows<LOG2, 0>, Cfg::SMEM)) return rc;
     if (int rc = set_smem(k_chirpz_rows<LOG2, 1>, Cfg::SMEM)) return rc;
     if (int rc = set_smem(k_chirpz_rows<LOG2, 2>, Cfg::SMEM)) return rc;
-    init = true;
-  }
+    return CJT_OK;
+  })) return rc_;
   const int64_t L1 = (int64_t)1 << cz.log1;
   dim3 grid((unsigned)(batch * cz.m_count), (unsigned)(L1 / Cfg::NR));
   auto kern = cz.n_in > 1 ? k_chirpz_rows<LOG2, 1> : cz.n_out > 1 ? k_chirpz_rows<LOG2, 2> : k_chirpz_rows<LOG2, 0>;
@@ -980,11 +980,11 @@ template <int LOG1>
 int run_cols_inv(const ChirpZDev& cz, const double2* tw, const double2* buf, double* out,
                  int64_t ldo, int64_t batch, cudaStream_t st) {
   using Cfg = ColCfg<LOG1>;
-  static bool init = false;
-  if (!init) {
+  static DeviceOnce once_;
+  if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(k_chirpz_cols_inv<LOG1>, Cfg::SMEM)) return rc;
-    init = true;
-  }
+    return CJT_OK;
+  })) return rc_;
   const int64_t L2 = (int64_t)1 << cz.log2;
   if constexpr (LOG1 <= 5) {
     dim3 grid((unsigned)batch, (unsigned)(L2 / COLR_T), (unsigned)cz.n_out);

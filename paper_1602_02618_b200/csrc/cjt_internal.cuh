@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -17,6 +19,29 @@
 #include "../../include/cjt.h"
 
 namespace cjt {
+
+// One-time per-DEVICE initialisation (cudaFuncSetAttribute and friends act on
+// the current device only): a process that drives several GPUs, or several
+// host threads racing to the first launch, runs `f` exactly once per device.
+struct DeviceOnce {
+  std::atomic<uint64_t> done{0};
+  std::mutex mu;
+  template <typename F>
+  int operator()(F&& f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = 0;
+    }
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.load(std::memory_order_relaxed) & bit) return 0;
+    const int rc = f();
+    if (rc == 0) done.fetch_or(bit, std::memory_order_release);
+    return rc;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // errors

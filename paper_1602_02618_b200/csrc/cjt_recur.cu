@@ -993,12 +993,12 @@ int launch_rec_forward(const RecRowsDev& rows, const RecTablesDev& tab, const in
   {                                                                                              \
     constexpr int R = WsCfg<V>::NBUF;                                                            \
     const int smem = 8 * (R * FWD_KS * (FWD_ROWS + 4) + (R + 1) * V * (FWD_KS + 4) + 2 * REC_WIN_ROWS * FWD_KS);  \
-    static bool init = false;                                                                    \
-    if (!init) {                                                                                 \
+    static DeviceOnce once_;                                                                    \
+    if (int rc_ = once_([&]() -> int {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_forward_ws<V, F>,                                  \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
-      init = true;                                                                               \
-    }                                                                                            \
+      return CJT_OK;                                                                               \
+    })) return rc_;                                                                                            \
     k_rec_forward_ws<V, F><<<grid, WsCfg<V>::NTH, smem, st>>>(rows, tab, ck_off, ck, items, c,   \
                                                               ldc, ncoef, batch, part, ws_debug()); \
   }
@@ -1053,12 +1053,12 @@ int launch_rec_inverse(const RecTablesDev& tab, const void* gen, int64_t nrows, 
     constexpr int R = WsCfg<V>::NBUF;                                                            \
     const int smem = 8 * (R * INV_DT * (INV_RT + 4) + (F ? 2 : 1) * (R + 1) * V * (INV_RT + 4) + \
                           REC_WIN_ROWS * (INV_DT + 2 * (INV_DT / 32)));                          \
-    static bool init = false;                                                                    \
-    if (!init) {                                                                                 \
+    static DeviceOnce once_;                                                                    \
+    if (int rc_ = once_([&]() -> int {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_inverse_ws<V, F>,                                  \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
-      init = true;                                                                               \
-    }                                                                                            \
+      return CJT_OK;                                                                               \
+    })) return rc_;                                                                                            \
     k_rec_inverse_ws<V, F><<<grid, WsCfg<V>::NTH, smem, st>>>(tab, g, nrows, items, tile_ids, wv, \
                                                               ldw, batch, part, ws_debug(), G);  \
   }
@@ -1104,12 +1104,12 @@ int launch_rec_gemm(const GemmItem* items, int64_t n_items, const double* P, con
 #define CJT_GEMM(V, M, F)                                                                        \
   if (vt == V && amk == M && fold == F) {                                                        \
     using Cf = GemmCfg<V, M>;                                                                    \
-    static bool init = false;                                                                    \
-    if (!init) {                                                                                 \
+    static DeviceOnce once_;                                                                    \
+    if (int rc_ = once_([&]() -> int {                                                                                 \
       CJT_CUDA_TRY(cudaFuncSetAttribute(k_rec_gemm<V, M, F>,                                     \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM)); \
-      init = true;                                                                               \
-    }                                                                                            \
+      return CJT_OK;                                                                               \
+    })) return rc_;                                                                                            \
     k_rec_gemm<V, M, F><<<grid, Cf::NTH, Cf::SMEM, st>>>(items, P, ids, x, ldx, xlen, batch, part); \
     CJT_CUDA_TRY(cudaGetLastError());                                                            \
     return CJT_OK;                                                                               \

@@ -259,6 +259,21 @@ def inverse(tp: TransformPlan, c: CoefficientVector) -> CoefficientVector:
     return jacobi(tp.p, _run_host(tp, c.data))
 
 
+def empty_on_stream(like, stream=None):
+    """torch.empty_like(like) for use by kernels on `stream` (a torch stream or
+    a raw cudaStream_t handle): when that is not the current stream, the block
+    is recorded on it, so the caching allocator cannot hand it out again while
+    work queued there may still touch it."""
+    import torch
+    out = torch.empty_like(like)
+    if stream is not None:
+        s = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(
+            int(stream), device=like.device)
+        if s.cuda_stream != torch.cuda.current_stream(like.device).cuda_stream:
+            out.record_stream(s)
+    return out
+
+
 def _execute_batched(tp: TransformPlan, data, out=None, check_finite: bool = True, stream=None):
     n1 = tp.n + 1
     if hasattr(data, "data_ptr"):  # torch tensor
@@ -277,7 +292,7 @@ def _execute_batched(tp: TransformPlan, data, out=None, check_finite: bool = Tru
             raise ValueError("coefficient data must be finite")
         dev = data.device.index
         if out is None:
-            out = torch.empty_like(data)
+            out = empty_on_stream(data, stream)
         elif out.shape != data.shape or out.dtype != torch.float64 or not out.is_contiguous():
             raise ValueError("out must be a contiguous float64 tensor shaped like the input")
         dp = tp.device_plan(dev)

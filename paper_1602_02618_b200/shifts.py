@@ -66,7 +66,7 @@ def shift_batched(op: str, p: JacobiParameters, x, out=None, stream=None):
     target = _shifted(p, da, db)
     x = _cuda_2d(x)
     if out is None:
-        out = torch.empty_like(x)
+        out = engine.empty_on_stream(x, stream)
     elif out.shape != x.shape or not out.is_contiguous() or out.dtype != torch.float64:
         raise ValueError("out must be a contiguous float64 tensor shaped like x")
     st = _raw_stream(stream, x.device)
@@ -132,7 +132,8 @@ def _apply_ops(ops, p: JacobiParameters, x, stream=None):
     import torch
     if not ops:
         return x, p
-    bufs = [torch.empty_like(x), torch.empty_like(x)]
+    # temporaries recorded on `stream` (kernels run there, not on the current stream)
+    bufs = [engine.empty_on_stream(x, stream), engine.empty_on_stream(x, stream)]
     cur = x
     for k, op in enumerate(ops):
         cur, p = shift_batched(op, p, cur, out=bufs[k % 2], stream=stream)
