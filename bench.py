@@ -313,6 +313,25 @@ def stage_model(fhost, ihost, batch: int) -> dict:
     return {"flops": flops, "bytes": nbytes}
 
 
+def remap_half_exact(model: dict, executed: dict, fhost, ihost, batch: int) -> None:
+    """alpha = beta = 1/2 plans run the exact expansion: the forward's U -> T
+    kernel (timed as fwd_rec) replaces the reference's recurrence AND its
+    analysis DCT, the inverse's one chirp-z product (timed as inv_blocks)
+    replaces its transposed recurrence.  The SURVEY 8(d) algorithmic work of
+    the replaced reference stages is credited to the stages that now do it."""
+    f, b = model["flops"], model["bytes"]
+    n1 = fhost.n + 1
+    model["half_exact"] = fhost.half_k is not None or ihost.half_k is not None
+    if fhost.half_k is not None:
+        f["fwd_rec"], f["fwd_edge"] = f["fwd_rec"] + f["fwd_edge"], 0.0
+        b["fwd_rec"], b["fwd_edge"] = batch * 8.0 * 2 * n1, 0.0
+        executed["fwd_rec"] = None
+    if ihost.half_k is not None:
+        f["inv_blocks"], f["inv_rec"] = f["inv_blocks"] + f["inv_rec"], 0.0
+        b["inv_blocks"], b["inv_rec"] = batch * 8.0 * ((ihost.grid_n + 1) + n1), 0.0
+        executed["inv_rec"] = None
+
+
 def survey_flops(fhost, ihost, batch: int) -> float:
     """SURVEY.md 8(d) F of one forward + inverse step (sum over the stages;
     the diagonal scalings, < 2 %, are omitted)."""
@@ -344,6 +363,8 @@ def dominant_roofline(stages_ms: dict, model: dict, executed: dict, peak: float,
     kern = {"fwd_rec": "k_rec_forward_ws / k_pgen_fwd + k_rec_gemm (K1)",
             "inv_rec": "k_rec_inverse_ws / k_pgen_inv + k_rec_gemm (K2)"}.get(
         dom, "k_chirpz_* (Bluestein chirp-z, K3/K4)")
+    if model.get("half_exact") and dom == "fwd_rec":
+        kern = "k_half_forward (alpha = beta = 1/2 exact U -> T conversion)"
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
@@ -546,6 +567,7 @@ def run_ours(args, wl):
             share = stages[f"{d}_{sname}"] / both if both > 0 else 0.0
             executed[f"{d}_{sname}"] = 5.0 * s_.fft_points_per_vector * batch * share
     model = stage_model(fp.host, ip.host, batch)
+    remap_half_exact(model, executed, fp.host, ip.host, batch)
     roofline = dominant_roofline(stages, model, executed, peak, args.config)
     roofline["step"] = step_roofline(survey_flops(fp.host, ip.host, batch), peak, sum(step_ms) / args.steps,
                                      float(batch * n1))

@@ -54,7 +54,7 @@ extern "C" {
 #define CJT_INVERSE 1
 
 /* One batched chirp-z product with fused diagonals (see planner.py ChirpZ):
- *   out[b, q0+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
+ *   out[b, q0-out_shift+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
  *   z_{b,m}[s] = sum_t exp(i pi (p0+t)(q0+s)/G) pre[m, t] x[b, p0+t].
  * Complex arrays are interleaved (re, im) float64. */
 typedef struct {
@@ -73,6 +73,7 @@ typedef struct {
     const int64_t* tiles_in;   /* [n_tiles_in][2] */
     const int64_t* tiles_out;  /* [n_tiles_out][2] */
     const double* kernel_hat;  /* [n_tiles_out][n_tiles_in][length] complex, 1/length folded in */
+    int64_t out_shift;         /* results for q land at out[q - out_shift] (0: at out[q]) */
 } cjt_chirpz_desc;
 
 typedef struct {
@@ -101,6 +102,11 @@ typedef struct {
     cjt_chirpz_desc edge;
     /* inverse: 1/A_n for n = 0..N (NULL for forward) */
     const double* scalings;
+    /* forward, alpha = beta = 1/2 only (else NULL): k_n = P_n(1) / (n+1),
+     * n = 0..N, so P_n = k_n U_n; the forward then is the exact
+     * U -> T conversion (cheb_j = e_j sum_{n >= j, n = j mod 2} k_n c_n) and
+     * needs no recurrence rows, blocks or edge (edge.length may be 0) */
+    const double* half_k;
 } cjt_plan_desc;
 
 typedef struct cjt_plan cjt_plan;
@@ -171,6 +177,15 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
                              const int64_t* cuts, const int8_t* regions,
                              double* out, int64_t n_out, int64_t n_points,
                              int64_t table_len);
+
+/* alpha = beta = 1/2 exact-expansion tables (planner.half_exact_tables):
+ * k[m] = P_m(1)/(m+1), m = 0..n; for every row p of the inverse grid G the
+ * angle phi_p of the point the reference's recurrence evaluates (interior:
+ * acos(x_p); near +-1: from the half-angle x-+1 value xm_p), computed in
+ * binary128, as inv_sin[p] = 1/sin(phi_p) and delta_over_sin[p] =
+ * (phi_p - pi p/G)/sin(phi_p) (endpoint rows p = 0, G: 0).  Host only. */
+int cjt_host_half_exact(const double* x, const double* xm, const int8_t* regions, int64_t G, int64_t n,
+                        double* k, double* inv_sin, double* delta_over_sin);
 
 int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n,
                     double* x, double* xm);

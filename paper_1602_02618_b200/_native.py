@@ -29,7 +29,7 @@ class ChirpZDesc(ctypes.Structure):
         ("m_count", _i32), ("accumulate", _i32),
         ("pre", _p), ("post", _p),
         ("n_tiles_in", _i32), ("n_tiles_out", _i32), ("tiles_in", _p), ("tiles_out", _p),
-        ("kernel_hat", _p),
+        ("kernel_hat", _p), ("out_shift", _i64),
     ]
 
 
@@ -42,7 +42,7 @@ class PlanDesc(ctypes.Structure):
         ("rf_plus", _p), ("rf_minus", _p), ("rf_plus_inv", _p), ("rf_minus_inv", _p),
         ("n_blocks", _i32), ("blocks", ctypes.POINTER(ChirpZDesc)),
         ("edge", ChirpZDesc),
-        ("scalings", _p),
+        ("scalings", _p), ("half_k", _p),
     ]
 
 
@@ -86,6 +86,7 @@ def lib():
     L.cjt_clenshaw_points.argtypes = [_p] * 8 + [_i64, _p, _p, _p, _p, _i64]
     L.cjt_transpose_accumulate.argtypes = [_p] * 12 + [_i64, _i64, _i64]
     L.cjt_host_angles.argtypes = [_p, _p, _i64, _p, _p]
+    L.cjt_host_half_exact.argtypes = [_p, _p, _p, _i64, _i64, _p, _p, _p]
     L.cjt_host_moments.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, _i64, _p]
     L.cjt_jacobi_shift.argtypes = [_i32, ctypes.c_double, ctypes.c_double, _p, _p, _i64, _i64, _p]
     L.cjt_clenshaw_points_dev.argtypes = [_p] * 7 + [_i64, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i64, _p]
@@ -96,7 +97,7 @@ def lib():
     L.cjt_chirpz_destroy.argtypes = [_p]
     for name in ("cjt_device_count", "cjt_plan_create", "cjt_plan_destroy", "cjt_plan_reserve",
                  "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host", "cjt_clenshaw_points",
-                 "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
+                 "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments", "cjt_host_half_exact",
                  "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak",
                  "cjt_clenshaw_points_dev", "cjt_jacobi_values", "cjt_clenshaw_smith_points",
                  "cjt_chirpz_create", "cjt_chirpz_execute", "cjt_chirpz_destroy"):
@@ -111,7 +112,7 @@ EXPORTED_SYMBOLS = (
     "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
     "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak", "cjt_clenshaw_points_dev",
     "cjt_jacobi_values", "cjt_clenshaw_smith_points", "cjt_chirpz_create", "cjt_chirpz_execute",
-    "cjt_chirpz_destroy",
+    "cjt_chirpz_destroy", "cjt_host_half_exact",
 )
 SHIFT_INC_BETA, SHIFT_DEC_BETA, SHIFT_INC_ALPHA, SHIFT_DEC_ALPHA = 0, 1, 2, 3
 STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7

@@ -72,6 +72,11 @@ struct cjt_plan {
   // i < nrows_fold only, split into even and odd degrees (half the work)
   bool fold = false;
   int64_t nrows_fold = 0;
+  // alpha = beta = 1/2 exact expansion (cjt_plan_desc.half_k): forward = the
+  // U -> T conversion kernel; inverse = synthesis + one chirp-z written
+  // straight to the output (no recurrence rows)
+  bool half_exact = false;
+  double* half_k = nullptr;
   int64_t rec_rows() const { return fold ? nrows_fold : nrows; }
   InvItem* iitems = nullptr;
   int64_t n_iitems = 0;
@@ -232,6 +237,7 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   cz.p0 = d.p0;
   cz.width = d.width;
   cz.q0 = d.q0;
+  cz.qout = d.q0 - d.out_shift;
   cz.count = d.count;
   cz.length = d.length;
   cz.m_count = d.m_count;
@@ -240,6 +246,7 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (lg < 4 || lg > 26) return fail(CJT_EINVAL, "chirp-z length must be a power of two in [16, 2^26]");
   if (d.width < 1 || d.count < 1 || d.m_count < 1 || d.n_tiles_in < 1 || d.n_tiles_out < 1)
     return fail(CJT_EINVAL, "inconsistent chirp-z descriptor");
+  if (cz.qout < 0) return fail(CJT_EINVAL, "chirp-z out_shift exceeds q0");
   const bool tiled = d.n_tiles_in > 1 || d.n_tiles_out > 1;
   if (tiled && lg > 13 && d.n_tiles_in > 1 && d.n_tiles_out > 1)
     return fail(CJT_EINVAL, "tiled multi-pass chirp-z needs n_tiles_in == 1 or n_tiles_out == 1");
@@ -339,6 +346,12 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   P->fft_points += (double)d.m_count * ffts * (double)d.length * lg;
   *out = cz;
   return CJT_OK;
+}
+
+bool rec_any(const cjt_plan* P) {
+  for (int64_t c : P->h_cut)
+    if (c > 0) return true;
+  return false;
 }
 
 // P chunk size of the two-pass contraction (bytes of generated P per chunk):
@@ -670,10 +683,12 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
   if (int rc = dalloc(W.allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
   W.part = (double*)p;
   bytes += part_elems * batch * 8;
-  if (int rc = dalloc(W.allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
-  W.vals = (double*)p;
-  bytes += G1 * batch * 8;
-  if (P->direction == CJT_INVERSE && !P->blocks.empty()) {
+  if (!(P->half_exact && P->direction == CJT_FORWARD)) {   // the exact forward needs no grid values
+    if (int rc = dalloc(W.allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
+    W.vals = (double*)p;
+    bytes += G1 * batch * 8;
+  }
+  if (P->direction == CJT_INVERSE && !P->blocks.empty() && !P->half_exact) {
     if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
     W.yacc = (double*)p;
     bytes += N1 * batch * 8;
@@ -731,7 +746,20 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
   int launches = 0;
   const int64_t N1 = P->n + 1, G1 = P->G + 1;
   const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
-  if (P->direction == CJT_FORWARD) {
+  if (P->half_exact && P->direction == CJT_FORWARD) {
+    if (rec) {
+      if (int rc = launch_half_forward(in, N1, out, N1, P->half_k, N1, batch, st)) return rc;
+      launches += 1;
+    }
+  } else if (P->half_exact) {
+    if (edge)
+      if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, W.spec, st, &launches))
+        return rc;
+    if (blk)
+      for (const ChirpZDev& cz : P->blocks)
+        if (int rc = launch_chirpz(cz, P->tw8192, W.vals, G1, out, N1, batch, W.scratch, W.czpart, W.spec, st, &launches))
+          return rc;
+  } else if (P->direction == CJT_FORWARD) {
     if (rec && P->two_pass) {
       double* pw = nullptr;
       if (int rc = arena_get(P->device, st, P->chunk_bytes, &pw)) return rc;
@@ -915,13 +943,25 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
   if (int rc = upload(A, &P->tw8192, tw.data(), tw.size())) return rc;
 
+  if (d->half_k) {
+    if (d->direction == CJT_INVERSE && (d->n_blocks != 1 || d->blocks[0].accumulate || rec_any(P.get())))
+      return fail(CJT_EINVAL, "exact-expansion inverse plans take one non-accumulating block and no recurrence rows");
+    if (d->direction == CJT_FORWARD && (d->n_blocks != 0 || rec_any(P.get())))
+      return fail(CJT_EINVAL, "exact-expansion forward plans take no blocks and no recurrence rows");
+    P->half_exact = true;
+    if (int rc = upload(A, &P->half_k, d->half_k, (size_t)(d->n + 1))) return rc;
+  }
   for (int k = 0; k < d->n_blocks; ++k) {
     ChirpZDev cz{};
     if (int rc = build_chirpz(P.get(), d->blocks[k], &cz)) return rc;
     P->blocks.push_back(cz);
   }
-  if (int rc = build_chirpz(P.get(), d->edge, &P->edge)) return rc;
-  P->has_edge = true;
+  if (d->edge.length > 0) {
+    if (int rc = build_chirpz(P.get(), d->edge, &P->edge)) return rc;
+    P->has_edge = true;
+  } else if (!(P->half_exact && d->direction == CJT_FORWARD)) {
+    return fail(CJT_EINVAL, "plan requires an edge (analysis / synthesis) chirp-z");
+  }
   if (d->direction == CJT_INVERSE) {
     if (!d->scalings) return fail(CJT_EINVAL, "inverse plan requires scalings");
     if (int rc = upload(A, &P->scal, d->scalings, (size_t)(d->n + 1))) return rc;
@@ -1215,7 +1255,7 @@ int cjt_chirpz_create(const cjt_chirpz_desc* d, cjt_chirpz_plan** out) {
   if (int rc = upload(P->allocs, &P->tw8192, tw.data(), tw.size())) return rc;
   if (int rc = build_chirpz(P, *d, &C->cz)) return rc;
   C->in_len = d->p0 + d->width;
-  C->out_len = d->q0 + d->count;
+  C->out_len = d->q0 - d->out_shift + d->count;
   CJT_CUDA_TRY(cudaDeviceSynchronize());
   *out = C.release();
   return CJT_OK;

@@ -217,7 +217,7 @@ __device__ __forceinline__ void fused_direct(const ChirpZDev& cz, const TW& tw, 
   for (int m = 0; m < cz.m_count; ++m) fused_unit<LOGL, MULTI>(cz, tw, s, t, valid, xb, j, m, 0, cz.n_in, specb, sink);
   __syncthreads();
   if (!valid) return;
-  double* ob = out + b * ldo + cz.q0 + so;
+  double* ob = out + b * ldo + cz.qout + so;
 #pragma unroll
   for (int i = 0; i < Cfg::EPT; ++i) {
     const int e = t + i * TPG;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256) k_chirpz_combine_sk(ChirpZDev cz, const d
   const int64_t ka = gj - sk.start(ca) / cz.n_in / cz.m_count;
   double v = pe[(ca * sk.S + ka) * stride];
   for (int64_t c = ca + 1; c <= cb; ++c) v += pe[c * sk.S * stride];
-  double* o = out + b * ldo + cz.q0 + so + e;
+  double* o = out + b * ldo + cz.qout + so + e;
   *o = cz.accumulate ? *o + v : v;
 }
 
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
       }
     }
   }
-  double* ob = out + b * ldo + cz.q0;
+  double* ob = out + b * ldo + cz.qout;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int n2 = t + i * T;
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
 #pragma unroll
     for (int r = 0; r < L1; ++r) acc[r] += fma(pq[r].x, v[r].x, -pq[r].y * v[r].y);
   }
-  double* ob = out + b * ldo + cz.q0 + so;
+  double* ob = out + b * ldo + cz.qout + so;
 #pragma unroll
   for (int r = 0; r < L1; ++r) {
     const int64_t q = r * L2 + n2;
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
     }
     __syncthreads();
   }
-  double* ob = out + b * ldo + cz.q0 + so;
+  double* ob = out + b * ldo + cz.qout + so;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int idx = threadIdx.x + i * T;

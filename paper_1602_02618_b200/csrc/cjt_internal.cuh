@@ -511,6 +511,7 @@ __device__ __forceinline__ void fft2_sub(double2* s, int n2, const TW& tw, const
 
 struct ChirpZDev {
   int64_t p0, width, q0, count, length;
+  int64_t qout;                  // output index of q = q0 (q0 - out_shift)
   int32_t m_count, accumulate;
   int32_t log2len, log1, log2;   // multipass split L = L1 * L2 (log1 + log2 = log2len)
   const double2* pre;       // [m][width]
@@ -581,6 +582,10 @@ inline int pick_vt(int64_t batch) {
 // scratch: multi-pass buffer (batch x m x L complex); part: m-split partial
 // sums (m x batch x count doubles), used when too few CTAs would run; spec:
 // per-CTA spectrum sums of input-tiled fused chirp-z (chirpz_spec_elems).
+// alpha = beta = 1/2 forward (exact U -> T conversion), cjt_half.cu
+int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, const double* k,
+                        int64_t n1, int64_t batch, cudaStream_t st);
+
 int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, int64_t ldx,
                   double* out, int64_t ldo, int64_t batch, double2* scratch, double* part,
                   double2* spec, cudaStream_t st, int* launches);

@@ -82,7 +82,7 @@ class _DevicePlan:
         thetas = np.ascontiguousarray(hp.thetas, dtype=np.float64)
         nat.check(L.cjt_host_angles(thetas.ctypes.data, regions.ctypes.data, g1,
                                     x.ctypes.data, xm.ctypes.data), "cjt_host_angles")
-        cuts = hp.cuts if hp.direction == "forward" else hp.rec_cuts
+        cuts = hp.device_cuts
 
         def cz_desc(cz: pl.ChirpZ) -> nat.ChirpZDesc:
             d = nat.ChirpZDesc()
@@ -96,6 +96,7 @@ class _DevicePlan:
             d.tiles_in = arr(cz.tiles_in, np.int64)
             d.tiles_out = arr(cz.tiles_out, np.int64)
             d.kernel_hat = arr(cz.kernel_hat, np.complex128)
+            d.out_shift = cz.out_shift
             return d
 
         desc = nat.PlanDesc()
@@ -117,8 +118,11 @@ class _DevicePlan:
             blocks[k] = cz_desc(cz)
         desc.n_blocks = len(hp.blocks)
         desc.blocks = blocks
-        desc.edge = cz_desc(hp.analysis if hp.direction == "forward" else hp.synthesis)
+        edge = hp.analysis if hp.direction == "forward" else hp.synthesis
+        if edge is not None:
+            desc.edge = cz_desc(edge)
         desc.scalings = arr(hp.scalings) if hp.scalings is not None else None
+        desc.half_k = arr(hp.half_k) if hp.half_k is not None else None
         handle = ctypes.c_void_p()
         nat.check(L.cjt_plan_create(ctypes.byref(desc), ctypes.byref(handle)), "cjt_plan_create")
         self.handle = handle

@@ -543,6 +543,7 @@ class ChirpZ:
     accumulate: bool
     tiles_in: np.ndarray = None   # (n_in, 2) int64: (offset, width) relative to p0
     tiles_out: np.ndarray = None  # (n_out, 2) int64: (offset, count) relative to q0
+    out_shift: int = 0            # results for q are written to out[q - out_shift]
 
     @property
     def m_count(self) -> int:
@@ -624,7 +625,7 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
 
 def chirpz(g: int, p0: int, width: int, q0: int, count: int,
            pre_scale: np.ndarray, post_scale: np.ndarray, accumulate: bool,
-           tiled: bool = True) -> ChirpZ:
+           tiled: bool = True, out_shift: int = 0) -> ChirpZ:
     """Build the Bluestein layout of sum_p x_p e^{i pi p q/G}.
     pre_scale/post_scale: (M, width)/(M, count) real or complex diagonals."""
     pidx = np.arange(p0, p0 + width, dtype=np.int64)
@@ -644,7 +645,7 @@ def chirpz(g: int, p0: int, width: int, q0: int, count: int,
     return ChirpZ(g, p0, width, q0, count, length,
                   np.ascontiguousarray(pre, dtype=np.complex128),
                   np.ascontiguousarray(post, dtype=np.complex128),
-                  khat, accumulate, tin, tout)
+                  khat, accumulate, tin, tout, out_shift)
 
 
 # ---------------------------------------------------------------------------
@@ -670,6 +671,74 @@ class HostPlan:
     synthesis: ChirpZ | None = None  # inverse: Chebyshev coefficients -> weighted values
     weights: np.ndarray | None = None
     scalings: np.ndarray | None = None
+    # alpha = beta = 1/2 exact expansion (half_exact_enabled): k_n = P_n(1)/(n+1)
+    half_k: np.ndarray | None = None
+    exec_cuts: np.ndarray | None = None   # recurrence rows the device runs (None: cuts / rec_cuts)
+
+    @property
+    def device_cuts(self) -> np.ndarray:
+        if self.exec_cuts is not None:
+            return self.exec_cuts
+        return self.cuts if self.direction == "forward" else self.rec_cuts
+
+
+def host_angles(thetas: np.ndarray, regions: np.ndarray):
+    """x = cos(theta) and the half-angle x -+ 1 values with the host libm, as
+    the reference kernel computes them per point (_kernels_cy.pyx:27, 58-64)."""
+    from . import _native as nat
+    th = np.ascontiguousarray(thetas, dtype=np.float64)
+    reg = np.ascontiguousarray(regions, dtype=np.int8)
+    x, xm = np.empty(len(th)), np.empty(len(th))
+    nat.check(nat.lib().cjt_host_angles(th.ctypes.data, reg.ctypes.data, len(th), x.ctypes.data,
+                                        xm.ctypes.data), "cjt_host_angles")
+    return x, xm
+
+
+def half_exact_enabled(p: JacobiParameters) -> bool:
+    """alpha = beta = 1/2 runs the exact (terminating) Hahn expansion instead
+    of the reference's all-recurrence layout ($CJT_HALF_EXACT=0 disables)."""
+    import os
+    return p.alpha == 0.5 and p.beta == 0.5 and os.environ.get("CJT_HALF_EXACT", "1") != "0"
+
+
+def half_exact_tables(thetas: np.ndarray, regions: np.ndarray, g: int, n: int):
+    """(k, inv_sin, delta_over_sin): k_m = P_m(1)/(m+1) (m <= n), and per grid
+    row p the angle phi_p of the point the reference's recurrence evaluates
+    (libm x_p / half-angle xm_p) as 1/sin(phi_p) and (phi_p - pi p/G)/sin(phi_p),
+    in binary128 (csrc/cjt_host.cpp)."""
+    from . import _native as nat
+    x, xm = host_angles(thetas, regions)
+    reg = np.ascontiguousarray(regions, dtype=np.int8)
+    k, inv_sin, dos = np.empty(n + 1), np.empty(g + 1), np.empty(g + 1)
+    nat.check(nat.lib().cjt_host_half_exact(x.ctypes.data, xm.ctypes.data, reg.ctypes.data, g, n,
+                                            k.ctypes.data, inv_sin.ctypes.data, dos.ctypes.data),
+              "cjt_host_half_exact")
+    return k, inv_sin, dos
+
+
+def half_exact_inverse(g: int, n: int, k: np.ndarray, inv_sin: np.ndarray, dos: np.ndarray,
+                       scalings: np.ndarray) -> ChirpZ:
+    """The inverse's whole contraction for alpha = beta = 1/2 as ONE chirp-z
+    product over the weighted grid values wv (engine.py:220-227 with
+    P_m(cos phi) = k_m sin((m+1) phi)/sin phi evaluated at the reference's
+    points phi_p = pi p/G + delta_p, to first order in (m+1) delta_p):
+
+      out[m] = k_m / A_m [ sum_p wv_p / sin(phi_p) sin(pi p q/G)
+                           + q sum_p wv_p delta_p / sin(phi_p) cos(pi p q/G) ],  q = m + 1
+
+    plus the endpoint rows' exact limits P_m(+-1) = k_m (m+1) (+-1)^m.  Term 0
+    (cosine, Re z) carries delta/sin and the endpoints, term 1 (sine, Im z)
+    1/sin; outputs q = 1..N+1 land at out[q - 1]."""
+    pre = np.zeros((2, g + 1))
+    pre[0] = dos
+    pre[0, 0], pre[0, g] = 1.0, -1.0
+    pre[1] = inv_sin
+    q = np.arange(1, n + 2, dtype=np.float64)
+    ks = k * scalings
+    post = np.empty((2, n + 1), dtype=np.complex128)
+    post[0] = ks * q
+    post[1] = -1j * ks
+    return chirpz(g, 0, g + 1, 1, n + 1, pre, post, accumulate=False, out_shift=1)
 
 
 _POOL = None
@@ -682,6 +751,26 @@ def _pool():
         import os
         _POOL = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
     return _POOL
+
+
+def _build_half_exact(hp: HostPlan) -> HostPlan:
+    """alpha = beta = 1/2: the reference's layout (no blocks, every row in the
+    recurrence region) is kept in hp.layout / hp.cuts for the SURVEY 8(d)
+    accounting; the device runs the exact expansion instead (no recurrence
+    rows): forward = U -> T conversion with k_n, inverse = synthesis + one
+    chirp-z (half_exact_inverse)."""
+    g, n = hp.grid_n, hp.n
+    k, inv_sin, dos = half_exact_tables(hp.thetas, hp.regions, g, n)
+    hp.half_k = k
+    hp.exec_cuts = np.zeros(g + 1, dtype=np.int64)
+    if hp.direction == "inverse":
+        mu = moments(hp.p, g)
+        w = cc_weights(hp.p, g, mu)
+        hp.weights = w
+        hp.synthesis = chirpz(g, 0, n + 1, 0, g + 1, np.ones((1, n + 1)), w[None, :], accumulate=False)
+        hp.scalings = 1.0 / orthonormality(hp.p, n)
+        hp.blocks = [half_exact_inverse(g, n, k, inv_sin, dos, hp.scalings)]
+    return hp
 
 
 def build(direction: str, p: JacobiParameters, n: int,
@@ -704,6 +793,8 @@ def build(direction: str, p: JacobiParameters, n: int,
     regions.flags.writeable = False
     hp = HostPlan(direction, p, n, m_terms, eps, g, th, regions, cuts, layout, tables,
                   np.minimum(cuts, n + 1))
+    if half_exact_enabled(p) and not layout.blocks:
+        return _build_half_exact(hp)
 
     if layout.blocks:
         # engine.py:133-141: u, v with endpoint rows zeroed; C_{n,m} columns

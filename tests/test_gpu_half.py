@@ -1,0 +1,81 @@
+"""GPU: the alpha = beta = 1/2 exact-expansion path (planner.half_exact_*,
+csrc/cjt_half.cu, csrc/cjt_host.cpp) against the reference's outputs and
+against the recurrence layout the reference itself runs ($CJT_HALF_EXACT=0).
+
+Tolerance (north_star): 1e-12 * ||c||_1 per vector; the measured margin is
+reported by the full-size tests (tests/test_gpu_fullsize.py)."""
+import numpy as np
+import pytest
+
+import cjt_oracle as O
+import paper_1602_02618_b200 as cj
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _run(p, n, c, monkeypatch, exact: bool):
+    import torch
+    monkeypatch.setenv("CJT_HALF_EXACT", "1" if exact else "0")
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    assert (fp.host.half_k is not None) == exact
+    x = torch.from_numpy(c).cuda()
+    f = cj.forward_batched(fp, x)
+    i = cj.inverse_batched(ip, f)
+    return f.cpu().numpy(), i.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["cfg3_full", "cfg5_e"])
+def test_half_exact_vs_reference_goldens(cuda, name, monkeypatch):
+    import torch
+    g = load_golden(name)
+    n = int(g["n"])
+    p = cj.JacobiParameters(0.5, 0.5)
+    monkeypatch.setenv("CJT_HALF_EXACT", "1")
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    f = cj.forward_batched(fp, torch.from_numpy(g["c"]).to(cuda)).cpu().numpy()
+    i = cj.inverse_batched(ip, torch.from_numpy(g["fwd"]).to(cuda)).cpu().numpy()
+    for v in range(g["c"].shape[0]):
+        assert O.parity(f[v], g["fwd"][v], g["c"][v]) <= 1e-15
+        assert O.parity(i[v], g["inv"][v], g["fwd"][v]) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 17, 255, 1000, 2047, 8191])
+def test_half_exact_vs_recurrence_layout(cuda, n, monkeypatch):
+    """Same inputs through both device paths (the recurrence layout is the
+    reference's own algorithm, parity-pinned elsewhere), and the oracle."""
+    p = cj.JacobiParameters(0.5, 0.5)
+    batch = 3 if n < 4000 else 2
+    c = np.stack([O.seeded_vector(5, v, n) for v in range(batch)])
+    f1, i1 = _run(p, n, c, monkeypatch, exact=True)
+    f0, i0 = _run(p, n, c, monkeypatch, exact=False)
+    l1c = np.abs(c).sum(axis=1)
+    l1f = np.abs(f0).sum(axis=1)
+    assert np.all(np.max(np.abs(f1 - f0), axis=1) <= 1e-14 * l1c)
+    assert np.all(np.max(np.abs(i1 - i0), axis=1) <= TOL * l1f)
+    for v in (0, batch - 1):
+        rf = O.oracle_forward(0.5, 0.5, c[v])
+        assert O.parity(f1[v], rf, c[v]) <= 1e-14
+        assert O.parity(i1[v], O.oracle_inverse(0.5, 0.5, f1[v]), f1[v]) <= TOL
+
+
+def test_half_exact_large_batch_and_host_api(cuda, monkeypatch):
+    """Many vectors (multi-tile scan, stream-K chirp-z) and the single-vector
+    host API (engine.forward / inverse) on the exact path."""
+    import torch
+    monkeypatch.setenv("CJT_HALF_EXACT", "1")
+    p = cj.JacobiParameters(0.5, 0.5)
+    n = 4095
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    c = np.stack([O.seeded_vector(3, v, n) for v in range(300)])
+    f = cj.forward_batched(fp, torch.from_numpy(c).to(cuda))
+    i = cj.inverse_batched(ip, f).cpu().numpy()
+    f = f.cpu().numpy()
+    for v in (0, 137, 299):
+        assert O.parity(f[v], O.oracle_forward(0.5, 0.5, c[v]), c[v]) <= 1e-14
+        assert O.parity(i[v], c[v], c[v]) <= 1e-12                 # round trip
+    one = cj.forward(fp, cj.jacobi(p, c[137]))
+    assert np.array_equal(one.data, f[137])
+    back = cj.inverse(ip, cj.chebyshev(f[137]))
+    assert np.max(np.abs(back.data - i[137])) <= 1e-15 * np.abs(f[137]).sum()

@@ -73,7 +73,7 @@ def test_growth_after_graph_capture_is_an_error(cuda):
     ref = y.clone()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
-        cj.forward_batched(fp, x, out=y)
+        cj.forward_batched(fp, x, out=y, check_finite=False)   # no host sync while capturing
     y.zero_()
     g.replay()
     torch.cuda.synchronize()

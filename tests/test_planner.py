@@ -155,10 +155,11 @@ def run_chirpz(cz, x, out):
                 a[:tn] = x[cz.p0 + to: cz.p0 + to + tn] * cz.pre[m, to:to + tn]
                 y = np.fft.ifft(np.fft.fft(a) * cz.kernel_hat[j, i]) * cz.length
                 acc[so:so + sc] += (cz.post[m, so:so + sc] * y[:sc]).real
+    q = cz.q0 - cz.out_shift
     if cz.accumulate:
-        out[cz.q0:cz.q0 + cz.count] += acc
+        out[q:q + cz.count] += acc
     else:
-        out[cz.q0:cz.q0 + cz.count] = acc
+        out[q:q + cz.count] = acc
 
 
 @pytest.mark.parametrize("tiled", [False, True])
@@ -210,17 +211,41 @@ def _gen_p(hp, nmax):
     return out
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2_small", "cfg5_a", "cfg5_e"])
-def test_device_decomposition_matches_reference(name):
+def half_forward_host(k, c):
+    """Host emulation of k_half_forward: cheb_j = e_j sum_{n >= j, n = j mod 2} k_n c_n."""
+    u = np.asarray(k, dtype=np.longdouble) * np.asarray(c, dtype=np.longdouble)
+    out = np.zeros(len(c), dtype=np.longdouble)
+    for par in (0, 1):
+        out[par::2] = np.cumsum(u[par::2][::-1])[::-1]
+    out[1:] *= 2
+    return out.astype(float)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_small", "cfg5_a", "cfg5_e", "cfg3_full"])
+def test_device_decomposition_matches_reference(name, monkeypatch):
     """The exact decomposition the kernels execute (generated-P contraction over
-    the recurrence region + tiled chirp-z blocks + chirp-z analysis/synthesis),
-    emulated on the host, reproduces the reference's outputs."""
+    the recurrence region + tiled chirp-z blocks + chirp-z analysis/synthesis;
+    for alpha = beta = 1/2 the exact-expansion path), emulated on the host,
+    reproduces the reference's outputs."""
     from conftest import load_golden
     import cjt_oracle as O
     g = load_golden(name)
     a, b, n = float(g["alpha"]), float(g["beta"]), int(g["n"])
     p = P.JacobiParameters(a, b)
     c, ref_f, ref_i = g["c"][0], g["fwd"][0], g["inv"][0]
+    if P.half_exact_enabled(p):
+        hf, hi = P.build("forward", p, n), P.build("inverse", p, n)
+        assert hf.half_k is not None and not hf.blocks and hf.analysis is None
+        assert O.parity(half_forward_host(hf.half_k, c), ref_f, c) <= 1e-15
+        wv = np.zeros(hi.grid_n + 1)
+        run_chirpz(hi.synthesis, ref_f, wv)
+        got_i = np.zeros(n + 1)
+        (cz,) = hi.blocks
+        run_chirpz(cz, wv, got_i)
+        assert O.parity(got_i, ref_i, ref_f) <= 1e-13
+        if name != "cfg5_e":
+            return
+        monkeypatch.setenv("CJT_HALF_EXACT", "0")   # and the recurrence layout below
     hf = P.build("forward", p, n)
     pm = _gen_p(hf, n + 1)
     vals = ((pm * (np.arange(n + 1)[:, None] < hf.cuts[None, :])) * c[:, None]).sum(0)
