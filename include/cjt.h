@@ -23,6 +23,11 @@
  *   cjt_transpose_accumulate   backend plugin `transpose_accumulate`
  *        (_kernels_cy.pyx:201-237, _kernels_np.py:60-97), same 12 arrays,
  *        host pointers, accumulates into out.
+ *   cjt_kernel_plan_create / _execute / _destroy   the same two plugin
+ *        kernels with their per-plan device state kept across calls
+ *        (backend.py caches one per reference plan).
+ *   cjt_host_half_exact  alpha = beta = 1/2 exact-expansion tables
+ *        (k_n, the reference's evaluation angles), host binary128.
  *   cjt_host_angles      the libm cos / half-angle evaluation the reference
  *        kernel performs per point (_kernels_cy.pyx:27,58-64), exposed so
  *        plans carry bit-identical x and x -+ 1 values.
@@ -177,6 +182,29 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C,
                              const int64_t* cuts, const int8_t* regions,
                              double* out, int64_t n_out, int64_t n_points,
                              int64_t table_len);
+
+/* Reusable device state of one backend-plugin call site (the reference
+ * engine passes the same plan arrays on every call, engine.py:177-183,
+ * 220-225): tables, libm angles and row layout are uploaded once by
+ * cjt_kernel_plan_create; each cjt_kernel_plan_execute moves one vector.
+ *   CJT_KERNEL_CLENSHAW   clenshaw_points: r_* = rb+-, 1/rb+-; n_len = number
+ *                         of coefficients; execute(in = coeffs, out = values
+ *                         at the n_points rows, overwritten)
+ *   CJT_KERNEL_TRANSPOSE  transpose_accumulate: r_* = rf+-, 1/rf+-; n_len =
+ *                         length of out; execute(in = wv at the rows, out +=)
+ * cjt_clenshaw_points / cjt_transpose_accumulate are create + execute +
+ * destroy in one call.  Thread-safe (one call at a time per plan). */
+#define CJT_KERNEL_CLENSHAW 0
+#define CJT_KERNEL_TRANSPOSE 1
+typedef struct cjt_kernel_plan cjt_kernel_plan;
+int cjt_kernel_plan_create(int32_t kind, const double* A, const double* B, const double* C,
+                           const double* r_plus, const double* r_minus,
+                           const double* r_plus_inv, const double* r_minus_inv,
+                           int64_t table_len, const double* thetas, const int64_t* cuts,
+                           const int8_t* regions, int64_t n_points, int64_t n_len,
+                           cjt_kernel_plan** out);
+int cjt_kernel_plan_execute(cjt_kernel_plan* plan, const double* in, double* out);
+int cjt_kernel_plan_destroy(cjt_kernel_plan* plan);
 
 /* alpha = beta = 1/2 exact-expansion tables (planner.half_exact_tables):
  * k[m] = P_m(1)/(m+1), m = 0..n; for every row p of the inverse grid G the

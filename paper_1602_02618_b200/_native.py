@@ -95,12 +95,16 @@ def lib():
     L.cjt_chirpz_create.argtypes = [ctypes.POINTER(ChirpZDesc), ctypes.POINTER(_p)]
     L.cjt_chirpz_execute.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p]
     L.cjt_chirpz_destroy.argtypes = [_p]
+    L.cjt_kernel_plan_create.argtypes = [_i32] + [_p] * 7 + [_i64, _p, _p, _p, _i64, _i64, ctypes.POINTER(_p)]
+    L.cjt_kernel_plan_execute.argtypes = [_p, _p, _p]
+    L.cjt_kernel_plan_destroy.argtypes = [_p]
     for name in ("cjt_device_count", "cjt_plan_create", "cjt_plan_destroy", "cjt_plan_reserve",
                  "cjt_plan_stats_get", "cjt_execute", "cjt_execute_host", "cjt_clenshaw_points",
                  "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments", "cjt_host_half_exact",
                  "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak",
                  "cjt_clenshaw_points_dev", "cjt_jacobi_values", "cjt_clenshaw_smith_points",
-                 "cjt_chirpz_create", "cjt_chirpz_execute", "cjt_chirpz_destroy"):
+                 "cjt_chirpz_create", "cjt_chirpz_execute", "cjt_chirpz_destroy",
+                 "cjt_kernel_plan_create", "cjt_kernel_plan_execute", "cjt_kernel_plan_destroy"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -112,8 +116,10 @@ EXPORTED_SYMBOLS = (
     "cjt_clenshaw_points", "cjt_transpose_accumulate", "cjt_host_angles", "cjt_host_moments",
     "cjt_jacobi_shift", "cjt_execute_stage", "cjt_probe_fp64_peak", "cjt_clenshaw_points_dev",
     "cjt_jacobi_values", "cjt_clenshaw_smith_points", "cjt_chirpz_create", "cjt_chirpz_execute",
-    "cjt_chirpz_destroy", "cjt_host_half_exact",
+    "cjt_chirpz_destroy", "cjt_host_half_exact", "cjt_kernel_plan_create", "cjt_kernel_plan_execute",
+    "cjt_kernel_plan_destroy",
 )
+CJT_KERNEL_CLENSHAW, CJT_KERNEL_TRANSPOSE = 0, 1
 SHIFT_INC_BETA, SHIFT_DEC_BETA, SHIFT_INC_ALPHA, SHIFT_DEC_ALPHA = 0, 1, 2, 3
 STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7
 
@@ -127,6 +133,17 @@ def check(rc: int, what: str = "cjt"):
     if rc == CJT_ENOMEM:
         raise MemoryError(f"{what}: {msg}")
     raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def current_device() -> int:
+    """The calling thread's current CUDA device (0 without torch / CUDA)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except ImportError:
+        pass
+    return 0
 
 
 def device_count() -> int:

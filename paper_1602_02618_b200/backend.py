@@ -17,6 +17,10 @@ reference installation can run its own engine with the B200 recurrence by
 
 from __future__ import annotations
 
+import collections
+import ctypes
+import hashlib
+import threading
 import types
 
 import numpy as np
@@ -28,26 +32,86 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+class _KernelPlan:
+    """One cjt_kernel_plan (device tables + rows of one plugin call site)."""
+
+    def __init__(self, kind, tables, thetas, cuts, regions, n_len):
+        tabs = [_f64(t) for t in tables]
+        thetas = _f64(thetas)
+        cuts = np.ascontiguousarray(cuts, dtype=np.int64)
+        regions = np.ascontiguousarray(regions, dtype=np.int8)
+        npts = len(thetas)
+        if not (len(cuts) == len(regions) == npts):
+            raise ValueError("thetas, cuts and regions must have equal length")
+        tl = min(len(t) for t in tabs)
+        if kind == nat.CJT_KERNEL_CLENSHAW and npts and int(cuts.max()) + 1 > min(len(t) for t in tabs[:3]):
+            raise ValueError("recurrence tables are shorter than the largest cut + 1")
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().cjt_kernel_plan_create(
+            kind, *[t.ctypes.data for t in tabs], tl, thetas.ctypes.data, cuts.ctypes.data,
+            regions.ctypes.data, npts, int(n_len), ctypes.byref(h)), "cjt_kernel_plan_create")
+        self.handle = h
+        self.n_points = npts
+        self.n_len = int(n_len)
+
+    def execute(self, x, out):
+        nat.check(nat.lib().cjt_kernel_plan_execute(self.handle, x.ctypes.data, out.ctypes.data),
+                  "cjt_kernel_plan_execute")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and nat._lib is not None:
+            try:
+                nat._lib.cjt_kernel_plan_destroy(h)
+            except Exception:
+                pass
+
+
+# Plugin call sites -> device state.  The reference engine passes the same
+# read-only plan arrays (tables, angles, cuts, regions; engine.py:118-119,
+# kernels.py:362-363) on every forward / inverse, so the key is their identity
+# (the cache holds references, so identities cannot be recycled while cached);
+# a writeable array also contributes a digest of its contents.
+_KCACHE: "collections.OrderedDict" = collections.OrderedDict()
+_KCACHE_MAX = 16
+_KLOCK = threading.Lock()
+
+
+def _ident(a):
+    a_ = np.asarray(a)
+    key = (id(a), a_.shape, a_.dtype.str)
+    if a_.flags.writeable:
+        key += (hashlib.blake2b(np.ascontiguousarray(a_).tobytes(), digest_size=16).digest(),)
+    return key
+
+
+def _kernel_plan(kind, tables, thetas, cuts, regions, n_len) -> _KernelPlan:
+    args = (*tables, thetas, cuts, regions)
+    key = (kind, int(n_len), nat.current_device(), tuple(_ident(a) for a in args))
+    with _KLOCK:
+        hit = _KCACHE.get(key)
+        if hit is not None:
+            _KCACHE.move_to_end(key)
+            return hit[0]
+    kp = _KernelPlan(kind, tables, thetas, cuts, regions, n_len)
+    with _KLOCK:
+        _KCACHE[key] = (kp, args)
+        while len(_KCACHE) > _KCACHE_MAX:
+            _KCACHE.popitem(last=False)
+    return kp
+
+
 def clenshaw_points(A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv,
                     coeffs, thetas, cuts, regions, out):
     """out[i] = sum_{n < cuts[i]} coeffs[n] P_n(cos thetas[i]) on the GPU."""
     if out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError("out must be a C-contiguous float64 array")
-    A, B, C = _f64(A), _f64(B), _f64(C)
-    rbp, rbm, rbpi, rbmi = _f64(rb_plus), _f64(rb_minus), _f64(rb_plus_inv), _f64(rb_minus_inv)
-    coeffs, thetas = _f64(coeffs), _f64(thetas)
-    cuts = np.ascontiguousarray(cuts, dtype=np.int64)
-    regions = np.ascontiguousarray(regions, dtype=np.int8)
-    npts = len(thetas)
-    if not (len(cuts) == len(regions) == len(out) == npts):
+    if not (len(thetas) == len(out)):
         raise ValueError("thetas, cuts, regions and out must have equal length")
-    if npts and int(cuts.max()) + 1 > min(len(A), len(B), len(C)):
-        raise ValueError("recurrence tables are shorter than the largest cut + 1")
-    nat.check(nat.lib().cjt_clenshaw_points(
-        A.ctypes.data, B.ctypes.data, C.ctypes.data, rbp.ctypes.data, rbm.ctypes.data,
-        rbpi.ctypes.data, rbmi.ctypes.data, coeffs.ctypes.data, len(coeffs),
-        thetas.ctypes.data, cuts.ctypes.data, regions.ctypes.data, out.ctypes.data, npts),
-        "cjt_clenshaw_points")
+    coeffs = _f64(coeffs)
+    kp = _kernel_plan(nat.CJT_KERNEL_CLENSHAW, (A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv),
+                      thetas, cuts, regions, len(coeffs))
+    kp.execute(coeffs, out)
     return None
 
 
@@ -56,20 +120,12 @@ def transpose_accumulate(A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv,
     """out[n] += sum_i wv[i] P_n(cos thetas[i]) over i with n < cuts[i] on the GPU."""
     if out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError("out must be a C-contiguous float64 array")
-    A, B, C = _f64(A), _f64(B), _f64(C)
-    rfp, rfm, rfpi, rfmi = _f64(rf_plus), _f64(rf_minus), _f64(rf_plus_inv), _f64(rf_minus_inv)
-    wv, thetas = _f64(wv), _f64(thetas)
-    cuts = np.ascontiguousarray(cuts, dtype=np.int64)
-    regions = np.ascontiguousarray(regions, dtype=np.int8)
-    npts = len(thetas)
-    if not (len(cuts) == len(regions) == len(wv) == npts):
+    wv = _f64(wv)
+    if len(wv) != len(thetas):
         raise ValueError("thetas, cuts, regions and wv must have equal length")
-    tl = min(len(A), len(B), len(C), len(rfp), len(rfm), len(rfpi), len(rfmi))
-    nat.check(nat.lib().cjt_transpose_accumulate(
-        A.ctypes.data, B.ctypes.data, C.ctypes.data, rfp.ctypes.data, rfm.ctypes.data,
-        rfpi.ctypes.data, rfmi.ctypes.data, wv.ctypes.data, thetas.ctypes.data,
-        cuts.ctypes.data, regions.ctypes.data, out.ctypes.data, len(out), npts, tl),
-        "cjt_transpose_accumulate")
+    kp = _kernel_plan(nat.CJT_KERNEL_TRANSPOSE, (A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv),
+                      thetas, cuts, regions, len(out))
+    kp.execute(wv, out)
     return None
 
 

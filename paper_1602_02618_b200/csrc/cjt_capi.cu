@@ -1132,44 +1132,213 @@ int cjt_host_angles(const double* thetas, const int8_t* regions, int64_t n, doub
   return CJT_OK;
 }
 
-static int clenshaw_host(const double* A, const double* B, const double* C, const double* rb_plus,
-                         const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
-                         const double* coeffs, int64_t n_coeffs, const double* thetas,
-                         const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points,
-                         int divide) {
-  if (n_points < 0 || n_coeffs < 0) return fail(CJT_EINVAL, "negative size");
-  if (n_points == 0) return CJT_OK;
+}  // extern "C"
+
+// Device state of one backend-plugin call site (cjt_kernel_plan_*): the
+// reference engine passes the same plan arrays on every forward / inverse
+// (engine.py:177-183, 220-225), so tables, angles and the row layout are
+// uploaded once and each call moves only its vector in and out.
+struct cjt_kernel_plan {
+  int kind = 0;                  // CJT_KERNEL_CLENSHAW / CJT_KERNEL_TRANSPOSE
+  int device = 0;
+  bool divide = false;           // clenshaw_smith (scalar API): divide by rb
+  int64_t n_points = 0, n_len = 0, n_res = 0;
+  std::vector<void*> allocs;
+  RecTablesDev tab{};
+  const double *rbp = nullptr, *rbm = nullptr, *rbpi = nullptr, *rbmi = nullptr;
+  const double *x = nullptr, *xm = nullptr;
+  const int8_t* reg = nullptr;
+  const int64_t* cut = nullptr;
+  double* d_in = nullptr;
+  double* d_out = nullptr;
+  std::unique_ptr<cjt_plan> P;   // transpose: single-vector inverse contraction plan
+  double* d_ones = nullptr;
+  std::vector<double> h_res;
+  std::mutex mu;
+  ~cjt_kernel_plan() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    for (void* q : allocs) cudaFree(q);
+    P.reset();
+    cudaSetDevice(cur);
+  }
+};
+
+namespace {
+
+int kernel_plan_create(int32_t kind, const double* A, const double* B, const double* C, const double* r_plus,
+                       const double* r_minus, const double* r_plus_inv, const double* r_minus_inv,
+                       int64_t table_len, const double* thetas, const int64_t* cuts, const int8_t* regions,
+                       int64_t n_points, int64_t n_len, bool divide, cjt_kernel_plan** out) {
+  if (!out) return fail(CJT_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_points < 0 || n_len < 0 || table_len < 0) return fail(CJT_EINVAL, "negative size");
+  if (kind != CJT_KERNEL_CLENSHAW && kind != CJT_KERNEL_TRANSPOSE) return fail(CJT_EINVAL, "bad kernel kind");
+  if (n_points > 0 && (!A || !B || !C || !r_plus || !r_minus || !r_plus_inv || !r_minus_inv || !thetas ||
+                       !cuts || !regions))
+    return fail(CJT_EINVAL, "null argument");
   int64_t maxcut = 0;
-  for (int64_t i = 0; i < n_points; ++i) maxcut = std::max(maxcut, cuts[i]);
-  if (maxcut > n_coeffs) return fail(CJT_EINVAL, "cut exceeds the coefficient count");
-  const size_t tl = (size_t)maxcut + 1;  // C[n+1] is read up to n = maxcut-1
+  for (int64_t i = 0; i < n_points; ++i) {
+    if (cuts[i] < 0) return fail(CJT_EINVAL, "negative cut");
+    maxcut = std::max(maxcut, cuts[i]);
+  }
+  if (maxcut > n_len)
+    return fail(CJT_EINVAL, kind == CJT_KERNEL_CLENSHAW ? "cut exceeds the coefficient count"
+                                                        : "cut exceeds the output length");
+  std::unique_ptr<cjt_kernel_plan> K(new cjt_kernel_plan());
+  CJT_CUDA_TRY(cudaGetDevice(&K->device));
+  K->kind = kind;
+  K->divide = divide;
+  K->n_points = n_points;
+  K->n_len = n_len;
+  if (n_points == 0) {
+    *out = K.release();
+    return CJT_OK;
+  }
   std::vector<double> x((size_t)n_points), xm((size_t)n_points);
   cjt_host_angles(thetas, regions, n_points, x.data(), xm.data());
-  std::vector<void*> tmp;
-  struct Free {
-    std::vector<void*>* v;
-    ~Free() { for (void* p : *v) cudaFree(p); }
-  } fr{&tmp};
-  double *dA, *dB, *dC, *rbp, *rbm, *rbpi, *rbmi, *dc, *dx, *dxm, *dout;
+  if (kind == CJT_KERNEL_CLENSHAW) {
+    // C[n+1] is read up to n = maxcut - 1
+    if (table_len < maxcut + 1) return fail(CJT_EINVAL, "recurrence tables are shorter than the largest cut + 1");
+    const size_t tl = (size_t)maxcut + 1;
+    double *dA, *dB, *dC, *rbp, *rbm, *rbpi, *rbmi, *dx, *dxm;
+    int8_t* dreg;
+    int64_t* dcut;
+    const double* srcs[7] = {A, B, C, r_plus, r_minus, r_plus_inv, r_minus_inv};
+    double** dsts[7] = {&dA, &dB, &dC, &rbp, &rbm, &rbpi, &rbmi};
+    for (int k = 0; k < 7; ++k)
+      if (int rc = upload(K->allocs, dsts[k], srcs[k], tl)) return rc;
+    if (int rc = upload(K->allocs, &dx, x.data(), x.size())) return rc;
+    if (int rc = upload(K->allocs, &dxm, xm.data(), xm.size())) return rc;
+    if (int rc = upload(K->allocs, &dreg, regions, (size_t)n_points)) return rc;
+    if (int rc = upload(K->allocs, &dcut, cuts, (size_t)n_points)) return rc;
+    void* p;
+    if (int rc = dalloc(K->allocs, &p, (size_t)std::max<int64_t>(n_len, 1) * 8)) return rc;
+    K->d_in = (double*)p;
+    if (int rc = dalloc(K->allocs, &p, (size_t)n_points * 8)) return rc;
+    K->d_out = (double*)p;
+    K->tab = RecTablesDev{dA, dB, dC, nullptr, nullptr, nullptr, nullptr, (int64_t)tl};
+    K->rbp = rbp, K->rbm = rbm, K->rbpi = rbpi, K->rbmi = rbmi;
+    K->x = dx, K->xm = dxm, K->reg = dreg, K->cut = dcut;
+    CJT_CUDA_TRY(cudaDeviceSynchronize());
+    *out = K.release();
+    return CJT_OK;
+  }
+  if (table_len < maxcut) return fail(CJT_EINVAL, "tables shorter than the largest cut");
+  // transpose: a single-vector inverse contraction plan over the caller's
+  // rows, degrees 0..maxcut-1
+  K->P.reset(new cjt_plan());
+  cjt_plan* P = K->P.get();
+  P->device = K->device;
+  P->direction = CJT_INVERSE;
+  P->n = std::max<int64_t>(maxcut, 1) - 1;
+  P->G = n_points - 1;
+  P->nrows = n_points;
+  P->h_cut.assign(cuts, cuts + n_points);
+  auto& Al = P->allocs;
+  double *dx, *dxm;
   int8_t* dreg;
   int64_t* dcut;
-  const double* srcs[7] = {A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv};
-  double** dsts[7] = {&dA, &dB, &dC, &rbp, &rbm, &rbpi, &rbmi};
-  for (int k = 0; k < 7; ++k)
-    if (int rc = upload(tmp, dsts[k], srcs[k], tl)) return rc;
-  if (int rc = upload(tmp, &dc, coeffs, (size_t)std::max<int64_t>(n_coeffs, 1))) return rc;
-  if (int rc = upload(tmp, &dx, x.data(), x.size())) return rc;
-  if (int rc = upload(tmp, &dxm, xm.data(), xm.size())) return rc;
-  if (int rc = upload(tmp, &dreg, regions, (size_t)n_points)) return rc;
-  if (int rc = upload(tmp, &dcut, cuts, (size_t)n_points)) return rc;
+  if (int rc = upload(Al, &dx, x.data(), x.size())) return rc;
+  if (int rc = upload(Al, &dxm, xm.data(), xm.size())) return rc;
+  if (int rc = upload(Al, &dreg, regions, (size_t)n_points)) return rc;
+  if (int rc = upload(Al, &dcut, cuts, (size_t)n_points)) return rc;
+  P->rows = RecRowsDev{dx, dxm, dreg, dcut, n_points};
+  const size_t tl = (size_t)std::max<int64_t>(maxcut, 1);
+  const double* src[7] = {A, B, C, r_plus, r_minus, r_plus_inv, r_minus_inv};
+  if (int rc = upload_tables(Al, src, tl, &P->tab)) return rc;
+  std::vector<int64_t> off((size_t)n_points);
+  int64_t tot = 0;
+  for (int64_t i = 0; i < n_points; ++i) {
+    off[i] = tot;
+    tot += (cuts[i] >= 1) ? (cuts[i] - 1) / CK : 0;
+  }
+  if (int rc = upload(Al, &P->ck_off, off.data(), off.size())) return rc;
   void* p;
-  if (int rc = dalloc(tmp, &p, (size_t)n_points * 8)) return rc;
-  dout = (double*)p;
-  RecTablesDev tab{dA, dB, dC, nullptr, nullptr, nullptr, nullptr, (int64_t)tl};
-  if (int rc = launch_clenshaw_points(tab, rbp, rbm, rbpi, rbmi, dc, 0, dx, dxm, dreg, dcut, dout, 0,
-                                     n_points, 1, divide != 0, 0))
+  if (int rc = dalloc(Al, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
+  P->ck = (double2*)p;
+  if (tot > 0)
+    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, 0)) return rc;
+  if (int rc = reserve(P, 1)) return rc;
+  K->n_res = P->n + 1;
+  std::vector<double> ones((size_t)K->n_res, 1.0);
+  if (int rc = upload(Al, &K->d_ones, ones.data(), ones.size())) return rc;
+  if (int rc = dalloc(Al, &p, (size_t)n_points * 8)) return rc;
+  K->d_in = (double*)p;
+  if (int rc = dalloc(Al, &p, (size_t)K->n_res * 8)) return rc;
+  K->d_out = (double*)p;
+  K->h_res.resize((size_t)K->n_res);
+  cjt_plan::Workspace* W = nullptr;
+  if (int rc = get_workspace(P, 0, &W)) return rc;
+  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  *out = K.release();
+  return CJT_OK;
+}
+
+int kernel_plan_execute(cjt_kernel_plan* K, const double* in, double* out) {
+  if (!K) return fail(CJT_EINVAL, "null plan");
+  if (K->n_points == 0) return CJT_OK;
+  if (!in || !out) return fail(CJT_EINVAL, "null buffer");
+  DeviceGuard g(K->device);
+  std::lock_guard<std::mutex> lk(K->mu);
+  if (K->kind == CJT_KERNEL_CLENSHAW) {
+    if (K->n_len > 0) CJT_CUDA_TRY(cudaMemcpy(K->d_in, in, (size_t)K->n_len * 8, cudaMemcpyHostToDevice));
+    if (int rc = launch_clenshaw_points(K->tab, K->rbp, K->rbm, K->rbpi, K->rbmi, K->d_in, 0, K->x, K->xm,
+                                        K->reg, K->cut, K->d_out, 0, K->n_points, 1, K->divide, 0))
+      return rc;
+    CJT_CUDA_TRY(cudaMemcpy(out, K->d_out, (size_t)K->n_points * 8, cudaMemcpyDeviceToHost));
+    return CJT_OK;
+  }
+  cjt_plan* P = K->P.get();
+  std::lock_guard<std::mutex> lp(P->exec_mu);
+  cjt_plan::Workspace* W = nullptr;
+  if (int rc = get_workspace(P, 0, &W)) return rc;
+  CJT_CUDA_TRY(cudaMemcpy(K->d_in, in, (size_t)K->n_points * 8, cudaMemcpyHostToDevice));
+  if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids, K->d_in,
+                                  K->n_points, 1, P->vt, false, P->G, W->part, 0))
     return rc;
-  CJT_CUDA_TRY(cudaMemcpy(out, dout, (size_t)n_points * 8, cudaMemcpyDeviceToHost));
+  if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, K->n_res, W->part, nullptr, K->d_ones, K->d_out,
+                                     K->n_res, 1, 0))
+    return rc;
+  CJT_CUDA_TRY(cudaMemcpy(K->h_res.data(), K->d_out, (size_t)K->n_res * 8, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < K->n_res && k < K->n_len; ++k) out[k] += K->h_res[(size_t)k];
+  return CJT_OK;
+}
+
+int kernel_once(int32_t kind, const double* A, const double* B, const double* C, const double* rp,
+                const double* rm, const double* rpi, const double* rmi, int64_t table_len, const double* thetas,
+                const int64_t* cuts, const int8_t* regions, int64_t n_points, int64_t n_len, bool divide,
+                const double* in, double* out) {
+  cjt_kernel_plan* K = nullptr;
+  if (int rc = kernel_plan_create(kind, A, B, C, rp, rm, rpi, rmi, table_len, thetas, cuts, regions, n_points,
+                                  n_len, divide, &K))
+    return rc;
+  std::unique_ptr<cjt_kernel_plan> hold(K);
+  return kernel_plan_execute(K, in, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cjt_kernel_plan_create(int32_t kind, const double* A, const double* B, const double* C,
+                           const double* r_plus, const double* r_minus, const double* r_plus_inv,
+                           const double* r_minus_inv, int64_t table_len, const double* thetas,
+                           const int64_t* cuts, const int8_t* regions, int64_t n_points, int64_t n_len,
+                           cjt_kernel_plan** out) {
+  return kernel_plan_create(kind, A, B, C, r_plus, r_minus, r_plus_inv, r_minus_inv, table_len, thetas, cuts,
+                            regions, n_points, n_len, false, out);
+}
+
+int cjt_kernel_plan_execute(cjt_kernel_plan* plan, const double* in, double* out) {
+  return kernel_plan_execute(plan, in, out);
+}
+
+int cjt_kernel_plan_destroy(cjt_kernel_plan* plan) {
+  if (!plan) return CJT_OK;
+  cudaDeviceSynchronize();
+  delete plan;
   return CJT_OK;
 }
 
@@ -1177,8 +1346,11 @@ int cjt_clenshaw_points(const double* A, const double* B, const double* C, const
                         const double* rb_minus, const double* rb_plus_inv, const double* rb_minus_inv,
                         const double* coeffs, int64_t n_coeffs, const double* thetas,
                         const int64_t* cuts, const int8_t* regions, double* out, int64_t n_points) {
-  return clenshaw_host(A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv, coeffs, n_coeffs, thetas,
-                       cuts, regions, out, n_points, 0);
+  if (n_points < 0 || n_coeffs < 0) return fail(CJT_EINVAL, "negative size");
+  int64_t maxcut = 0;
+  for (int64_t i = 0; i < n_points; ++i) maxcut = std::max(maxcut, cuts[i]);
+  return kernel_once(CJT_KERNEL_CLENSHAW, A, B, C, rb_plus, rb_minus, rb_plus_inv, rb_minus_inv, maxcut + 1,
+                     thetas, cuts, regions, n_points, n_coeffs, false, coeffs, out);
 }
 
 int cjt_clenshaw_smith_points(const double* A, const double* B, const double* C, const double* rb_plus,
@@ -1189,8 +1361,8 @@ int cjt_clenshaw_smith_points(const double* A, const double* B, const double* C,
     if (modes[i] < -1 || modes[i] > 1) return fail(CJT_EINVAL, "mode must be -1, 0 or +1");
   std::vector<int64_t> cuts((size_t)n_points, n_coeffs);
   // the reciprocal tables are unused by the dividing variant
-  return clenshaw_host(A, B, C, rb_plus, rb_minus, rb_plus, rb_minus, coeffs, n_coeffs, thetas,
-                       cuts.data(), modes, out, n_points, 1);
+  return kernel_once(CJT_KERNEL_CLENSHAW, A, B, C, rb_plus, rb_minus, rb_plus, rb_minus, n_coeffs + 1, thetas,
+                     cuts.data(), modes, n_points, n_coeffs, true, coeffs, out);
 }
 
 int cjt_clenshaw_points_dev(const double* A, const double* B, const double* C, const double* rb_plus,
@@ -1318,63 +1490,8 @@ int cjt_transpose_accumulate(const double* A, const double* B, const double* C, 
                              const double* rf_minus_inv, const double* wv, const double* thetas,
                              const int64_t* cuts, const int8_t* regions, double* out, int64_t n_out,
                              int64_t n_points, int64_t table_len) {
-  if (n_points < 0 || n_out < 0) return fail(CJT_EINVAL, "negative size");
-  if (n_points == 0) return CJT_OK;
-  int64_t maxcut = 0;
-  for (int64_t i = 0; i < n_points; ++i) maxcut = std::max(maxcut, cuts[i]);
-  if (maxcut > n_out) return fail(CJT_EINVAL, "cut exceeds the output length");
-  if (table_len < maxcut) return fail(CJT_EINVAL, "tables shorter than the largest cut");
-  // a single-vector plan over the caller's rows: degrees 0..maxcut-1
-  std::unique_ptr<cjt_plan> P(new cjt_plan());
-  CJT_CUDA_TRY(cudaGetDevice(&P->device));
-  P->direction = CJT_INVERSE;
-  P->n = std::max<int64_t>(maxcut, 1) - 1;
-  P->G = n_points - 1;
-  P->nrows = n_points;
-  P->h_cut.assign(cuts, cuts + n_points);
-  std::vector<double> x((size_t)n_points), xm((size_t)n_points);
-  cjt_host_angles(thetas, regions, n_points, x.data(), xm.data());
-  auto& Al = P->allocs;
-  double *dx, *dxm;
-  int8_t* dreg;
-  int64_t* dcut;
-  if (int rc = upload(Al, &dx, x.data(), x.size())) return rc;
-  if (int rc = upload(Al, &dxm, xm.data(), xm.size())) return rc;
-  if (int rc = upload(Al, &dreg, regions, (size_t)n_points)) return rc;
-  if (int rc = upload(Al, &dcut, cuts, (size_t)n_points)) return rc;
-  P->rows = RecRowsDev{dx, dxm, dreg, dcut, n_points};
-  const size_t tl = (size_t)std::max<int64_t>(maxcut, 1);
-  const double* src[7] = {A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv};
-  if (int rc = upload_tables(Al, src, tl, &P->tab)) return rc;
-  std::vector<int64_t> off((size_t)n_points);
-  int64_t tot = 0;
-  for (int64_t i = 0; i < n_points; ++i) {
-    off[i] = tot;
-    tot += (cuts[i] >= 1) ? (cuts[i] - 1) / CK : 0;
-  }
-  if (int rc = upload(Al, &P->ck_off, off.data(), off.size())) return rc;
-  void* p;
-  if (int rc = dalloc(Al, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
-  P->ck = (double2*)p;
-  if (tot > 0)
-    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, 0)) return rc;
-  if (int rc = reserve(P.get(), 1)) return rc;
-  std::vector<double> ones((size_t)(P->n + 1), 1.0);
-  double *dscal, *dwv, *dres;
-  if (int rc = upload(Al, &dscal, ones.data(), ones.size())) return rc;
-  if (int rc = upload(Al, &dwv, wv, (size_t)n_points)) return rc;
-  if (int rc = dalloc(Al, &p, ones.size() * 8)) return rc;
-  dres = (double*)p;
-  cjt_plan::Workspace* W = nullptr;
-  if (int rc = get_workspace(P.get(), 0, &W)) return rc;
-  if (int rc = launch_rec_inverse(P->tab, P->inv_gen, P->nrows, P->iitems, P->n_iitems, P->tile_ids,
-                                  dwv, n_points, 1, P->vt, false, P->G, W->part, 0)) return rc;
-  if (int rc = launch_inverse_finish(P->dt_slot0, P->dt_nslot, P->n + 1, W->part, nullptr, dscal, dres,
-                                     P->n + 1, 1, 0)) return rc;
-  std::vector<double> res(ones.size());
-  CJT_CUDA_TRY(cudaMemcpy(res.data(), dres, res.size() * 8, cudaMemcpyDeviceToHost));
-  for (int64_t k = 0; k <= P->n && k < n_out; ++k) out[k] += res[k];
-  return CJT_OK;
+  return kernel_once(CJT_KERNEL_TRANSPOSE, A, B, C, rf_plus, rf_minus, rf_plus_inv, rf_minus_inv, table_len,
+                     thetas, cuts, regions, n_points, n_out, false, wv, out);
 }
 
 }  // extern "C"
