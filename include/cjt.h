@@ -79,7 +79,20 @@ typedef struct {
     const int64_t* tiles_out;  /* [n_tiles_out][2] */
     const double* kernel_hat;  /* [n_tiles_out][n_tiles_in][length] complex, 1/length folded in */
     int64_t out_shift;         /* results for q land at out[q - out_shift] (0: at out[q]) */
+    /* device-side planning (device_tables = 1): pre / post are the bare
+     * diagonals (no chirp), kernel_hat is ignored, and the library builds the
+     * chirps, the folded tables and every tile's spectrum on the GPU for the
+     * grid parameter grid_g.  A diagonal of kind CJT_DIAG_MODULATION is not
+     * passed at all: it is u_m - i v_m (asymptotics.py:36-75) of the plan's
+     * grid rows pre_row0 + t / post_row0 + s (plan create only). */
+    int32_t device_tables;
+    int32_t pre_kind, post_kind;   /* CJT_DIAG_ARRAY or CJT_DIAG_MODULATION */
+    int64_t grid_g;
+    int64_t pre_row0, post_row0;
 } cjt_chirpz_desc;
+
+#define CJT_DIAG_ARRAY 0
+#define CJT_DIAG_MODULATION 1
 
 typedef struct {
     int32_t direction;      /* CJT_FORWARD or CJT_INVERSE */
@@ -112,6 +125,10 @@ typedef struct {
      * U -> T conversion (cheb_j = e_j sum_{n >= j, n = j mod 2} k_n c_n) and
      * needs no recurrence rows, blocks or edge (edge.length may be 0) */
     const double* half_k;
+    /* grid angles theta_i (i = 0..G) and (alpha, beta): needed when a block
+     * diagonal is of kind CJT_DIAG_MODULATION (else may be NULL / unused) */
+    const double* thetas;
+    double alpha, beta;
 } cjt_plan_desc;
 
 typedef struct cjt_plan cjt_plan;

@@ -30,6 +30,8 @@ class ChirpZDesc(ctypes.Structure):
         ("pre", _p), ("post", _p),
         ("n_tiles_in", _i32), ("n_tiles_out", _i32), ("tiles_in", _p), ("tiles_out", _p),
         ("kernel_hat", _p), ("out_shift", _i64),
+        ("device_tables", _i32), ("pre_kind", _i32), ("post_kind", _i32),
+        ("grid_g", _i64), ("pre_row0", _i64), ("post_row0", _i64),
     ]
 
 
@@ -43,6 +45,7 @@ class PlanDesc(ctypes.Structure):
         ("n_blocks", _i32), ("blocks", ctypes.POINTER(ChirpZDesc)),
         ("edge", ChirpZDesc),
         ("scalings", _p), ("half_k", _p),
+        ("thetas", _p), ("alpha", ctypes.c_double), ("beta", ctypes.c_double),
     ]
 
 
@@ -120,6 +123,7 @@ EXPORTED_SYMBOLS = (
     "cjt_kernel_plan_destroy",
 )
 CJT_KERNEL_CLENSHAW, CJT_KERNEL_TRANSPOSE = 0, 1
+CJT_DIAG_ARRAY, CJT_DIAG_MODULATION = 0, 1
 SHIFT_INC_BETA, SHIFT_DEC_BETA, SHIFT_INC_ALPHA, SHIFT_DEC_ALPHA = 0, 1, 2, 3
 STAGE_REC, STAGE_BLOCKS, STAGE_EDGE, STAGE_ALL = 1, 2, 4, 7
 

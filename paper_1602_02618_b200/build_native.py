@@ -13,7 +13,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 OUT = HERE / "_lib" / "libcjt_b200.so"
-SOURCES = ["cjt_capi.cu", "cjt_chirpz.cu", "cjt_recur.cu", "cjt_shift.cu", "cjt_half.cu", "cjt_host.cpp"]
+SOURCES = ["cjt_capi.cu", "cjt_chirpz.cu", "cjt_recur.cu", "cjt_shift.cu", "cjt_half.cu", "cjt_host.cpp", "cjt_plan_dev.cu"]
 HEADERS = ["cjt_internal.cuh"]
 
 NVCC_FLAGS = [
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = True, out: Path | None = None) ->
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(target),
-           *map(str, objs), "-lquadmath"]
+           *map(str, objs), "-lquadmath", "-lcufft", "-lpthread"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

@@ -77,6 +77,8 @@ struct cjt_plan {
   // straight to the output (no recurrence rows)
   bool half_exact = false;
   double* half_k = nullptr;
+  // grid angles and (alpha, beta) on the device: modulation diagonals built here
+  PlanGrid grid{};
   int64_t rec_rows() const { return fold ? nrows_fold : nrows; }
   InvItem* iitems = nullptr;
   int64_t n_iitems = 0;
@@ -273,36 +275,7 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   if (int rc = upload(P->allocs, const_cast<int64_t**>(&cz.tout), d.tiles_out, (size_t)2 * d.n_tiles_out)) return rc;
   cz.log2len = lg;
   const size_t nm = (size_t)d.m_count;
-  if (int rc = upload(P->allocs, const_cast<double2**>(&cz.pre),
-                      reinterpret_cast<const double2*>(d.pre), nm * d.width)) return rc;
-  if (int rc = upload(P->allocs, const_cast<double2**>(&cz.post),
-                      reinterpret_cast<const double2*>(d.post), nm * d.count)) return rc;
-  const double2* kh = reinterpret_cast<const double2*>(d.kernel_hat);
   const bool cluster = lg >= 14 && lg <= 17 && !tiled && cluster_enabled();
-  if (lg <= 13 || cluster) {
-    // cluster / short fused tiles read the spectra in natural order; the
-    // two-level FFT (fft2_used) in the permuted order k1 S + k2 <- k1 + 16 k2
-    const size_t nk = (size_t)d.length * d.n_tiles_in * d.n_tiles_out;
-    if (lg <= 13 && fft2_used(lg)) {
-      const int64_t L = d.length, S = L / 16;
-      std::vector<double2> perm(nk);
-      for (size_t tile = 0; tile < nk / (size_t)L; ++tile)
-        for (int64_t k1 = 0; k1 < 16; ++k1)
-          for (int64_t k2 = 0; k2 < S; ++k2)
-            perm[tile * L + (size_t)(k1 * S + k2)] = kh[tile * L + (size_t)(k1 + 16 * k2)];
-      if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), nk)) return rc;
-    } else {
-      if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), kh, nk)) return rc;
-    }
-  }
-  if (lg >= 14) {
-    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
-    std::vector<double2> hi((size_t)nhi), lo(4096);
-    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
-    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
-  }
   if (lg >= 14 && !cluster) {
     // on-chip rows (two-level FFT) and short columns: wide,
     // coalesced column tiles (E / L1 columns) in passes 1 and 3
@@ -318,22 +291,43 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     // points: 4096-point rows at 2 CTAs/SM win for 2^16 .. 2^19 too, config-4/5
     // A/B with CJT_MP_L2MAX: 58.9 -> 57.8 ms, 159.4 -> 155.5 ms)
     const int l2 = std::min({l2max, lg - 4, lg >= 16 ? 12 : 13});
-    const int l1 = lg - l2;
-    cz.log1 = l1;
+    cz.log1 = lg - l2;
     cz.log2 = l2;
-    const int64_t L1 = int64_t(1) << l1, L2 = int64_t(1) << l2;
-    const int64_t ntile = (int64_t)d.n_tiles_in * d.n_tiles_out;
-    std::vector<double2> perm((size_t)(d.length * ntile));
-    const bool f2 = fft2_used(l2);
-    const int64_t S2 = L2 / 16;
-    for (int64_t tile = 0; tile < ntile; ++tile)
-      for (int64_t k1 = 0; k1 < L1; ++k1)
-        for (int64_t k2 = 0; k2 < L2; ++k2) {
-          // row k1, row spectrum index k2 (natural) or its two-level position
-          const int64_t pos = f2 ? (k2 % 16) * S2 + k2 / 16 : k2;
-          perm[(size_t)(tile * d.length + k1 * L2 + pos)] = kh[tile * d.length + k1 + L1 * k2];
-        }
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.khat), perm.data(), perm.size())) return rc;
+  }
+  // spectrum layout of the executing kernels: natural (cluster, short fused
+  // tiles), two-level on-chip order (fused tiles >= 512), multi-pass rows
+  // [k1][k2] with the rows' own order
+  const int mode = cluster ? 0 : lg <= 13 ? (fft2_used(lg) ? 1 : 0) : (fft2_used(cz.log2) ? 3 : 2);
+  const int ntile = d.n_tiles_in * d.n_tiles_out;
+  if (d.device_tables) {
+    // device-side planning: chirps, folded diagonals, spectra (cjt_plan_dev.cu)
+    const int64_t G = d.grid_g;
+    if (G < 1) return fail(CJT_EINVAL, "device-built chirp-z tables need grid_g >= 1");
+    if (int rc = build_device_diag(DevDiag{d.pre_kind, reinterpret_cast<const double2*>(d.pre), d.pre_row0},
+                                   d.width, d.m_count, d.p0, G, P->grid, P->allocs, &cz.pre))
+      return rc;
+    if (int rc = build_device_diag(DevDiag{d.post_kind, reinterpret_cast<const double2*>(d.post), d.post_row0},
+                                   d.count, d.m_count, d.q0, G, P->grid, P->allocs, &cz.post))
+      return rc;
+    if (int rc = build_device_spectra(cz, cz.tin, cz.tout, G, mode, P->allocs, &cz.khat)) return rc;
+  } else {
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.pre),
+                        reinterpret_cast<const double2*>(d.pre), nm * d.width)) return rc;
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.post),
+                        reinterpret_cast<const double2*>(d.post), nm * d.count)) return rc;
+    if (int rc = permute_spectra(reinterpret_cast<const double2*>(d.kernel_hat), d.length, ntile, mode, cz.log1,
+                                 cz.log2, P->allocs, &cz.khat))
+      return rc;
+  }
+  if (lg >= 14) {
+    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
+    std::vector<double2> hi((size_t)nhi), lo(4096);
+    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
+    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
+    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
+  }
+  if (lg >= 14 && !cluster) {
     // one slot per input or output tile per (vector, term)
     P->scratch_elems_per_vec = std::max<int64_t>(
         P->scratch_elems_per_vec, d.length * d.m_count * std::max(d.n_tiles_in, d.n_tiles_out));
@@ -943,6 +937,22 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
   if (int rc = upload(A, &P->tw8192, tw.data(), tw.size())) return rc;
 
+  if (d->thetas) {
+    double* th = nullptr;
+    if (int rc = upload(A, &th, d->thetas, (size_t)nr)) return rc;
+    // pair weights of the modulation sums (asymptotics.py:22-33)
+    std::vector<double> wa((size_t)std::max(1, d->m_terms)), wb(wa.size());
+    for (int which = 0; which < 2; ++which) {
+      std::vector<double>& w = which ? wb : wa;
+      const double gam = which ? d->beta : d->alpha;
+      w[0] = 1.0;
+      for (size_t l = 1; l < w.size(); ++l) w[l] = w[l - 1] * (0.5 + gam + (double)l - 1) * (0.5 - gam + (double)l - 1) / (double)l;
+    }
+    double *dwa = nullptr, *dwb = nullptr;
+    if (int rc = upload(A, &dwa, wa.data(), wa.size())) return rc;
+    if (int rc = upload(A, &dwb, wb.data(), wb.size())) return rc;
+    P->grid = PlanGrid{th, dwa, dwb, d->alpha, d->beta};
+  }
   if (d->half_k) {
     if (d->direction == CJT_INVERSE && (d->n_blocks != 1 || d->blocks[0].accumulate || rec_any(P.get())))
       return fail(CJT_EINVAL, "exact-expansion inverse plans take one non-accumulating block and no recurrence rows");

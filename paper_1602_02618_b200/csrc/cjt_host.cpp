@@ -18,6 +18,10 @@
 #include <quadmath.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <thread>
+#include <vector>
+
 #include "../../include/cjt.h"
 
 namespace {
@@ -43,17 +47,30 @@ extern "C" int cjt_host_half_exact(const double* x, const double* xm, const int8
     if (m > 0) p1 = p1 * ((__float128)m + kHalf) / (__float128)m;
     k[m] = (double)(p1 / (__float128)(m + 1));
   }
-  for (int64_t p = 0; p <= G; ++p) {
-    if (p == 0 || p == G) {
-      inv_sin[p] = 0.0;
-      delta_over_sin[p] = 0.0;
-      continue;
+  auto rows = [&](int64_t p0, int64_t p1) {
+    for (int64_t p = p0; p < p1; ++p) {
+      if (p == 0 || p == G) {
+        inv_sin[p] = 0.0;
+        delta_over_sin[p] = 0.0;
+        continue;
+      }
+      const __float128 phi = effective_angle(x[p], xm[p], regions[p]);
+      const __float128 ideal = kPi * (__float128)p / (__float128)G;
+      const __float128 s = sinq(phi);
+      inv_sin[p] = (double)(kOne / s);
+      delta_over_sin[p] = (double)((phi - ideal) / s);
     }
-    const __float128 phi = effective_angle(x[p], xm[p], regions[p]);
-    const __float128 ideal = kPi * (__float128)p / (__float128)G;
-    const __float128 s = sinq(phi);
-    inv_sin[p] = (double)(kOne / s);
-    delta_over_sin[p] = (double)((phi - ideal) / s);
+  };
+  // binary128 is software arithmetic (~1 us per row): large grids on threads
+  const int64_t nrow = G + 1;
+  const int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                        std::max<int64_t>(1, nrow / 8192));
+  if (nt <= 1) {
+    rows(0, nrow);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(rows, nrow * t / nt, nrow * (t + 1) / nt);
+    for (auto& t : th) t.join();
   }
   return CJT_OK;
 }

@@ -582,6 +582,29 @@ inline int pick_vt(int64_t batch) {
 // scratch: multi-pass buffer (batch x m x L complex); part: m-split partial
 // sums (m x batch x count doubles), used when too few CTAs would run; spec:
 // per-CTA spectrum sums of input-tiled fused chirp-z (chirpz_spec_elems).
+// device-side planning of chirp-z products, cjt_plan_dev.cu
+struct DevDiag {
+  int kind;               // CJT_DIAG_ARRAY: host table; CJT_DIAG_MODULATION: u_m - i v_m of grid rows
+  const double2* host;    // [m][len] (array kind)
+  int64_t row0;           // modulation kind: grid row of index 0
+};
+struct PlanGrid {         // what the modulation kind needs (device pointers)
+  const double* thetas = nullptr;
+  const double* wa = nullptr;
+  const double* wb = nullptr;
+  double alpha = 0.0, beta = 0.0;
+};
+// diag[m][t] (from the host or the modulation functions) times chirp(base + t)
+int build_device_diag(const DevDiag& dd, int64_t len, int m_count, int64_t base, int64_t G, const PlanGrid& grid,
+                      std::vector<void*>& allocs, const double2** out);
+// every tile's kernel spectrum, 1/L folded in, in the execution layout `mode`
+// (0 natural, 1 two-level on-chip, 2 multi-pass rows, 3 multi-pass two-level rows)
+int build_device_spectra(const ChirpZDev& cz, const int64_t* tin_dev, const int64_t* tout_dev, int64_t G,
+                         int mode, std::vector<void*>& allocs, const double2** out);
+// host natural-order spectra -> device, permuted into layout `mode`
+int permute_spectra(const double2* natural_host, int64_t L, int ntile, int mode, int log1, int log2,
+                    std::vector<void*>& allocs, const double2** out);
+
 // alpha = beta = 1/2 forward (exact U -> T conversion), cjt_half.cu
 int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, const double* k,
                         int64_t n1, int64_t batch, cudaStream_t st);

@@ -89,14 +89,25 @@ class _DevicePlan:
             d.p0, d.width, d.q0, d.count, d.length = cz.p0, cz.width, cz.q0, cz.count, cz.length
             d.m_count = cz.m_count
             d.accumulate = 1 if cz.accumulate else 0
-            d.pre = arr(cz.pre, np.complex128)
-            d.post = arr(cz.post, np.complex128)
             d.n_tiles_in = len(cz.tiles_in)
             d.n_tiles_out = len(cz.tiles_out)
             d.tiles_in = arr(cz.tiles_in, np.int64)
             d.tiles_out = arr(cz.tiles_out, np.int64)
-            d.kernel_hat = arr(cz.kernel_hat, np.complex128)
             d.out_shift = cz.out_shift
+            if cz.device_tables:
+                # bare diagonals; chirps, modulation and spectra built on the device
+                d.device_tables = 1
+                d.grid_g = cz.g
+                for which, diag in (("pre", cz.pre_diag), ("post", cz.post_diag)):
+                    if isinstance(diag, pl.Modulation):
+                        setattr(d, which + "_kind", nat.CJT_DIAG_MODULATION)
+                        setattr(d, which + "_row0", diag.row0)
+                    else:
+                        setattr(d, which, arr(np.atleast_2d(diag), np.complex128))
+            else:
+                d.pre = arr(cz.pre, np.complex128)
+                d.post = arr(cz.post, np.complex128)
+                d.kernel_hat = arr(cz.kernel_hat, np.complex128)
             return d
 
         desc = nat.PlanDesc()
@@ -123,6 +134,8 @@ class _DevicePlan:
             desc.edge = cz_desc(edge)
         desc.scalings = arr(hp.scalings) if hp.scalings is not None else None
         desc.half_k = arr(hp.half_k) if hp.half_k is not None else None
+        desc.thetas = arr(thetas)
+        desc.alpha, desc.beta = hp.p.alpha, hp.p.beta
         handle = ctypes.c_void_p()
         nat.check(L.cjt_plan_create(ctypes.byref(desc), ctypes.byref(handle)), "cjt_plan_create")
         self.handle = handle

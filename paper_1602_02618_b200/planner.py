@@ -116,10 +116,18 @@ def stirling_series(z):
     z = np.asarray(z, dtype=float)
     if np.any(z < 9.0):
         raise ValueError("Stirling series requires z >= 9")
-    terms = _STIRLING_TERMS[np.searchsorted(_STIRLING_CUTS, z, side="right") - 1]
+    idx = np.searchsorted(_STIRLING_CUTS, z, side="right") - 1
     res = np.empty_like(z)
-    for k in np.unique(terms):
-        pick = terms == k
+    if z.ndim == 1 and z.size > 1 and np.all(z[1:] >= z[:-1]):
+        # ascending arguments (the planner's degree ranges): contiguous runs of
+        # equal term counts, no masks
+        bounds = np.flatnonzero(np.diff(idx)) + 1
+        runs = zip(np.concatenate([[0], bounds]), np.concatenate([bounds, [z.size]]))
+        groups = [(int(_STIRLING_TERMS[idx[a]]), slice(int(a), int(b))) for a, b in runs]
+    else:
+        terms = _STIRLING_TERMS[idx]
+        groups = [(int(k), terms == k) for k in np.unique(terms)]
+    for k, pick in groups:
         zz = z[pick]
         horner = np.zeros_like(zz)
         for j in range(k - 1, 0, -1):
@@ -519,35 +527,86 @@ def _next_pow2(v: int) -> int:
     return 1 << max(4, int(v - 1).bit_length())
 
 
-@dataclass
+class Modulation:
+    """A diagonal of u_m - i v_m (asymptotics.py:36-75, endpoint rows zeroed as
+    engine.py:138-139) over grid rows row0 .. row0 + len - 1; built on the
+    device by the library (cjt_plan_dev.cu) or on the host on demand."""
+
+    def __init__(self, p: "JacobiParameters", m_count: int, thetas: np.ndarray, row0: int, length: int):
+        self.p, self.m_count, self.thetas, self.row0, self.length = p, m_count, thetas, row0, length
+
+    def host(self) -> np.ndarray:
+        g = len(self.thetas) - 1
+        rows = np.arange(self.row0, self.row0 + self.length)
+        u, v = modulation(self.p, self.m_count, self.thetas[rows])
+        edge = (rows == 0) | (rows == g)
+        u[:, edge] = 0.0
+        v[:, edge] = 0.0
+        return u - 1j * v
+
+
 class ChirpZ:
     """One batched chirp-z product with fused diagonal scalings:
 
-        out[b, q0+s] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
+        out[b, q0+s-out_shift] (+)= sum_m Re(post[m, s] * z_{b,m}[s]),
         z_{b,m}[s] = sum_t exp(i pi (p0+t)(q0+s)/G) pre[m, t] x[b, p0+t].
 
     The index rectangle (input t < width) x (output s < count) may be tiled:
     tile (j, i) covers inputs tiles_in[i] and outputs tiles_out[j] and is one
     Bluestein convolution of length `length` with spectrum kernel_hat[j, i].
-    """
 
-    g: int
-    p0: int
-    width: int
-    q0: int
-    count: int
-    length: int
-    pre: np.ndarray      # (M, width) complex128: scaling * chirp(p)
-    post: np.ndarray     # (M, count) complex128: scaling * chirp(q)
-    kernel_hat: np.ndarray  # (n_out, n_in, length) complex128, 1/length folded in
-    accumulate: bool
-    tiles_in: np.ndarray = None   # (n_in, 2) int64: (offset, width) relative to p0
-    tiles_out: np.ndarray = None  # (n_out, 2) int64: (offset, count) relative to q0
-    out_shift: int = 0            # results for q are written to out[q - out_shift]
+    `pre_diag` / `post_diag` are the bare diagonals (arrays, or Modulation);
+    with device_tables the library builds the chirps, folded tables and
+    spectra on the GPU.  `pre`, `post` and `kernel_hat`
+    are the host-built equivalents, computed on first access (tests, the
+    standalone trigonometric transforms, $CJT_DEVICE_PLAN=0)."""
+
+    def __init__(self, g, p0, width, q0, count, length, pre_diag, post_diag, accumulate,
+                 tiles_in, tiles_out, out_shift=0, device_tables=True):
+        self.g, self.p0, self.width, self.q0, self.count, self.length = g, p0, width, q0, count, length
+        self.pre_diag, self.post_diag = pre_diag, post_diag
+        self.accumulate = accumulate
+        self.tiles_in, self.tiles_out = tiles_in, tiles_out
+        self.out_shift = out_shift
+        self.device_tables = device_tables
+        self._pre = self._post = self._khat = None
 
     @property
     def m_count(self) -> int:
-        return self.pre.shape[0]
+        d = self.pre_diag
+        return d.m_count if isinstance(d, Modulation) else np.atleast_2d(d).shape[0]
+
+    @staticmethod
+    def _diag(d) -> np.ndarray:
+        return d.host() if isinstance(d, Modulation) else np.atleast_2d(d)
+
+    @property
+    def pre(self) -> np.ndarray:
+        if self._pre is None:
+            pidx = np.arange(self.p0, self.p0 + self.width, dtype=np.int64)
+            self._pre = np.ascontiguousarray(self._diag(self.pre_diag) * chirp(pidx, self.g)[None, :],
+                                             dtype=np.complex128)
+        return self._pre
+
+    @property
+    def post(self) -> np.ndarray:
+        if self._post is None:
+            qidx = np.arange(self.q0, self.q0 + self.count, dtype=np.int64)
+            self._post = np.ascontiguousarray(self._diag(self.post_diag) * chirp(qidx, self.g)[None, :],
+                                              dtype=np.complex128)
+        return self._post
+
+    @property
+    def kernel_hat(self) -> np.ndarray:
+        """(n_out, n_in, length) complex spectra, 1/length folded in."""
+        if self._khat is None:
+            khat = np.empty((len(self.tiles_out), len(self.tiles_in), self.length), dtype=np.complex128)
+            for j, (so, sc) in enumerate(self.tiles_out):
+                for i, (to, tw) in enumerate(self.tiles_in):
+                    khat[j, i] = _spectrum(self.g, self.p0 + int(to), int(tw), self.q0 + int(so), int(sc),
+                                           self.length)
+            self._khat = khat
+        return self._khat
 
 
 FUSED_MAX = 8192        # largest Bluestein length kept entirely in one CTA's shared memory
@@ -591,6 +650,7 @@ def _split(n: int, parts: int) -> np.ndarray:
 KHAT_MAX_POINTS = 1 << 24    # tile spectra stored per chirp-z (x 16 B)
 
 
+@functools.lru_cache(maxsize=4096)
 def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     """Choose (length, n_in, n_out) for a width x count chirp-z: one untiled
     power-of-two Bluestein, or a grid of on-chip tiles, by measured cost."""
@@ -623,29 +683,26 @@ def tile_layout(width: int, count: int, fused_max: int = FUSED_MAX):
     return best[1:]
 
 
+def device_planning() -> bool:
+    """Chirp-z tables and spectra are built on the device unless $CJT_DEVICE_PLAN=0."""
+    import os
+    return os.environ.get("CJT_DEVICE_PLAN", "1") != "0"
+
+
 def chirpz(g: int, p0: int, width: int, q0: int, count: int,
-           pre_scale: np.ndarray, post_scale: np.ndarray, accumulate: bool,
-           tiled: bool = True, out_shift: int = 0) -> ChirpZ:
-    """Build the Bluestein layout of sum_p x_p e^{i pi p q/G}.
-    pre_scale/post_scale: (M, width)/(M, count) real or complex diagonals."""
-    pidx = np.arange(p0, p0 + width, dtype=np.int64)
-    qidx = np.arange(q0, q0 + count, dtype=np.int64)
-    pre = np.atleast_2d(pre_scale) * chirp(pidx, g)[None, :]
-    post = np.atleast_2d(post_scale) * chirp(qidx, g)[None, :]
+           pre_scale, post_scale, accumulate: bool,
+           tiled: bool = True, out_shift: int = 0, device_tables: bool | None = None) -> ChirpZ:
+    """Lay out sum_p x_p e^{i pi p q/G} over [p0, p0+width) x [q0, q0+count)
+    as a (tiled) Bluestein product.  pre_scale/post_scale: (M, width)/(M,
+    count) real or complex diagonals, or Modulation."""
     if tiled:
         length, n_in, n_out = tile_layout(width, count)
     else:
         length, n_in, n_out = _next_pow2(width + count - 1), 1, 1
-    tin = _split(width, n_in)
-    tout = _split(count, n_out)
-    khat = np.empty((n_out, n_in, length), dtype=np.complex128)
-    for j, (so, sc) in enumerate(tout):
-        for i, (to, tw) in enumerate(tin):
-            khat[j, i] = _spectrum(g, p0 + int(to), int(tw), q0 + int(so), int(sc), length)
-    return ChirpZ(g, p0, width, q0, count, length,
-                  np.ascontiguousarray(pre, dtype=np.complex128),
-                  np.ascontiguousarray(post, dtype=np.complex128),
-                  khat, accumulate, tin, tout, out_shift)
+    if device_tables is None:
+        device_tables = device_planning()
+    return ChirpZ(g, p0, width, q0, count, length, pre_scale, post_scale, accumulate,
+                  _split(width, n_in), _split(count, n_out), out_shift, device_tables)
 
 
 # ---------------------------------------------------------------------------
@@ -741,18 +798,6 @@ def half_exact_inverse(g: int, n: int, k: np.ndarray, inv_sin: np.ndarray, dos: 
     return chirpz(g, 0, g + 1, 1, n + 1, pre, post, accumulate=False, out_shift=1)
 
 
-_POOL = None
-
-
-def _pool():
-    global _POOL
-    if _POOL is None:
-        import concurrent.futures as cf
-        import os
-        _POOL = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
-    return _POOL
-
-
 def _build_half_exact(hp: HostPlan) -> HostPlan:
     """alpha = beta = 1/2: the reference's layout (no blocks, every row in the
     recurrence region) is kept in hp.layout / hp.cuts for the SURVEY 8(d)
@@ -797,29 +842,28 @@ def build(direction: str, p: JacobiParameters, n: int,
         return _build_half_exact(hp)
 
     if layout.blocks:
-        # engine.py:133-141: u, v with endpoint rows zeroed; C_{n,m} columns
-        u, v = modulation(p, m_terms, th)
-        u[:, 0] = u[:, -1] = 0.0
-        v[:, 0] = v[:, -1] = 0.0
-        ccols = cnm_table(p, g, m_terms)
-        w_uv = u - 1j * v
+        # engine.py:133-141: u - i v over each block's rows (Modulation; built
+        # on the device), C_{n,m} columns of its strip
+        # only degrees <= N are used (inverse strips are clipped to N); the
+        # table's values do not depend on its length once it reaches the
+        # Stirling switch degree
+        ccols = cnm_table(p, min(g, max(n, _cnm_switch(p.alpha, p.beta))), m_terms)
         jobs = []
         for (lo, hi), blk in zip(layout.column_strips(), layout.blocks):
-            rows = slice(blk.i1, blk.i2 + 1)
+            nrow = blk.i2 - blk.i1 + 1
+            w_uv = Modulation(p, m_terms, th, blk.i1, nrow)
             if direction == "forward":
                 # values[rows] += u_m DCT(C_m c)[rows] + v_m DST(C_m c)[rows]
-                jobs.append((g, lo, hi - lo + 1, blk.i1, blk.i2 - blk.i1 + 1,
-                             ccols[lo:hi + 1, :].T, w_uv[:, rows], True))
+                jobs.append((g, lo, hi - lo + 1, blk.i1, nrow,
+                             np.ascontiguousarray(ccols[lo:hi + 1, :].T), w_uv, True))
             else:
                 # out[strip] += C_m (DCT(u_m wv) + DST(v_m wv)); degrees > N dropped
                 top = min(hi, n)
                 if lo > top:
                     continue
-                jobs.append((g, blk.i1, blk.i2 - blk.i1 + 1, lo, top - lo + 1,
-                             w_uv[:, rows], ccols[lo:top + 1, :].T, True))
-        # blocks are independent: their chirp / spectrum tables are built
-        # concurrently (NumPy releases the GIL in the large array kernels)
-        hp.blocks = list(_pool().map(lambda a: chirpz(*a), jobs))
+                jobs.append((g, blk.i1, nrow, lo, top - lo + 1,
+                             w_uv, np.ascontiguousarray(ccols[lo:top + 1, :].T), True))
+        hp.blocks = [chirpz(*a) for a in jobs]
 
     if direction == "forward":
         # chebyshev_analysis (trig.py:53-63): scipy DCT-I of 0.5 v, i.e. the

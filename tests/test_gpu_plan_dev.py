@@ -1,0 +1,69 @@
+"""GPU: device-side planning (csrc/cjt_plan_dev.cu):
+chirp-z tables, modulation functions and Bluestein spectra built on the GPU
+give the same transforms as host-built tables ($CJT_DEVICE_PLAN=0), across
+every spectrum layout (fused short / two-level tiles, multi-pass rows with
+and without the two-level row FFT, tiled products) and stay within the
+north_star tolerance of the oracle."""
+import time
+
+import numpy as np
+import pytest
+
+import cjt_oracle as O
+import paper_1602_02618_b200 as cj
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(p, n, monkeypatch, device):
+    monkeypatch.setenv("CJT_DEVICE_PLAN", "1" if device else "0")
+    fp, ip = cj.plan("forward", p, n), cj.plan("inverse", p, n)
+    assert all(cz.device_tables == device for cz in fp.host.blocks + ip.host.blocks)
+    return fp, ip
+
+
+@pytest.mark.parametrize("ab,n", [((0.0, 0.0), 1023), ((-0.25, 0.4), 16383), ((0.25, -0.45), 4095),
+                                  ((-0.45, -0.2), 65535), ((0.3, -0.45), 2**18 - 1)])
+def test_device_planned_equals_host_planned(cuda, ab, n, monkeypatch):
+    import torch
+    p = cj.JacobiParameters(*ab)
+    c = np.stack([O.seeded_vector(5, v, n) for v in range(2)])
+    x = torch.from_numpy(c).to(cuda)
+    res = {}
+    for device in (True, False):
+        fp, ip = _pair(p, n, monkeypatch, device)
+        f = cj.forward_batched(fp, x)
+        i = cj.inverse_batched(ip, f)
+        res[device] = (f.cpu().numpy(), i.cpu().numpy())
+    l1 = np.abs(c).sum(axis=1)
+    df = np.max(np.abs(res[True][0] - res[False][0]), axis=1) / l1
+    di = np.max(np.abs(res[True][1] - res[False][1]), axis=1) / np.abs(res[False][0]).sum(axis=1)
+    assert np.all(df <= 1e-14) and np.all(di <= 1e-13), (df, di)
+    if n <= 16383:
+        for v in range(2):
+            rf = O.oracle_forward(*ab, c[v])
+            assert O.parity(res[True][0][v], rf, c[v]) <= 1e-12
+            assert O.parity(res[True][1][v], O.oracle_inverse(*ab, res[True][0][v]), res[True][0][v]) <= 1e-12
+
+
+def test_plan_time_config4_and_config5(cuda):
+    """Done-criterion of SURVEY 8(f) item 1: a config-4 inverse plan
+    (host + device) well under a second, config 5's 225 plan pairs too (the
+    timings are printed; the bounds leave room for a slow host)."""
+    import torch
+    from paper_1602_02618_b200.ragged import RaggedPlan
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ip = cj.plan("inverse", cj.JacobiParameters(0.3, -0.45), 2**20 - 1)
+    ip.device_plan(0)
+    torch.cuda.synchronize()
+    t4 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rp = RaggedPlan(O.config5_draws(4096))
+    for fp_, ip_ in rp.plans:
+        fp_.device_plan(0)
+        ip_.device_plan(0)
+    torch.cuda.synchronize()
+    t5 = time.perf_counter() - t0
+    print(f"config-4 inverse plan {t4:.2f} s; config-5 225 plan pairs {t5:.2f} s")
+    assert t4 < 2.0 and t5 < 3.0
