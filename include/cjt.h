@@ -129,6 +129,11 @@ typedef struct {
      * diagonal is of kind CJT_DIAG_MODULATION (else may be NULL / unused) */
     const double* thetas;
     double alpha, beta;
+    /* inverse exact-expansion plans only: 1 = run as the exact conversion plus
+     * a bf16 tensor-core correction (blocks[0] is then the CORRECTION chirp-z;
+     * the library applies edge + blocks[0] to the identity once to build the
+     * (N+1) x (N+1) correction matrix) */
+    int32_t half_gemm;
 } cjt_plan_desc;
 
 typedef struct cjt_plan cjt_plan;

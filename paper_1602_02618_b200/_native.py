@@ -46,6 +46,7 @@ class PlanDesc(ctypes.Structure):
         ("edge", ChirpZDesc),
         ("scalings", _p), ("half_k", _p),
         ("thetas", _p), ("alpha", ctypes.c_double), ("beta", ctypes.c_double),
+        ("half_gemm", _i32),
     ]
 
 

@@ -77,6 +77,10 @@ struct cjt_plan {
   // straight to the output (no recurrence rows)
   bool half_exact = false;
   double* half_k = nullptr;
+  // inverse, moderate N: exact conversion + bf16 tensor-core correction with
+  // the per-plan matrix X = M^T (cjt_half.cu), built from edge + blocks[0]
+  bool half_gemm = false;
+  void* gemm_X = nullptr;
   // grid angles and (alpha, beta) on the device: modulation diagonals built here
   PlanGrid grid{};
   int64_t rec_rows() const { return fold ? nrows_fold : nrows; }
@@ -112,6 +116,8 @@ struct cjt_plan {
     double2* spec = nullptr;   // tiled chirp-z spectrum sums
     double* io_in = nullptr;
     double* io_out = nullptr;
+    void* tbf = nullptr;       // half_gemm: bf16 copy of the input [B][N+1]
+    float* corr = nullptr;     // half_gemm: fp32 correction [B][N+1]
   };
   std::map<cudaStream_t, Workspace> ws;
   std::mutex ws_mu;
@@ -672,6 +678,20 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
   const int64_t G1 = P->G + 1, N1 = P->n + 1;
   void* p;
   int64_t bytes = 0;
+  if (P->half_gemm) {
+    if (int rc = half_gemm_prepare(st)) return rc;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 2)) return rc;
+    W.tbf = p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 4)) return rc;
+    W.corr = (float*)p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+    W.io_in = (double*)p;
+    if (int rc = dalloc(W.allocs, &p, (size_t)(N1 * batch) * 8)) return rc;
+    W.io_out = (double*)p;
+    W.batch = batch;
+    P->workspace_bytes = std::max<int64_t>(P->workspace_bytes, N1 * batch * 22);
+    return CJT_OK;
+  }
   const int64_t part_elems = (P->direction == CJT_FORWARD) ? P->n_fslots * FWD_ROWS * (P->fold ? 2 : 1)
                                                             : P->n_islots * INV_DT;
   if (int rc = dalloc(W.allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
@@ -745,6 +765,11 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
       if (int rc = launch_half_forward(in, N1, out, N1, P->half_k, N1, batch, st)) return rc;
       launches += 1;
     }
+  } else if (P->half_gemm) {
+    if (blk) {
+      if (int rc = half_gemm_inverse(in, out, N1, batch, P->gemm_X, W.tbf, W.corr, P->half_k, st)) return rc;
+      launches += 3;
+    }
   } else if (P->half_exact) {
     if (edge)
       if (int rc = launch_chirpz(P->edge, P->tw8192, in, N1, W.vals, G1, batch, W.scratch, W.czpart, W.spec, st, &launches))
@@ -813,6 +838,61 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
     }
   }
   if (stages == CJT_STAGE_ALL) P->last_launches = launches;
+  return CJT_OK;
+}
+
+// X = M^T of a half_gemm plan: M e_b for the unit vectors e_b, in chunks,
+// through the plan's synthesis (edge) and correction (blocks[0]) chirp-z
+// products, rounded to bf16 (row b of X = column b of M).
+int build_half_gemm_matrix(cjt_plan* P) {
+  const int64_t n1 = P->n + 1, G1 = P->G + 1;
+  const int64_t chunk = std::min<int64_t>(n1, 512);
+  std::vector<void*> tmp;
+  struct Free {
+    std::vector<void*>* v;
+    ~Free() { for (void* q : *v) cudaFree(q); }
+  } fr{&tmp};
+  void* p;
+  if (int rc = dalloc(P->allocs, &p, (size_t)(n1 * n1) * 2)) return rc;
+  P->gemm_X = p;
+  double *ein, *eout, *vals, *part = nullptr;
+  double2 *scratch = nullptr, *spec = nullptr;
+  if (int rc = dalloc(tmp, &p, (size_t)(chunk * n1) * 8)) return rc;
+  ein = (double*)p;
+  if (int rc = dalloc(tmp, &p, (size_t)(chunk * n1) * 8)) return rc;
+  eout = (double*)p;
+  if (int rc = dalloc(tmp, &p, (size_t)(chunk * G1) * 8)) return rc;
+  vals = (double*)p;
+  if (P->scratch_elems_per_vec > 0) {
+    if (int rc = dalloc(tmp, &p, (size_t)(P->scratch_elems_per_vec * chunk) * 16)) return rc;
+    scratch = (double2*)p;
+  }
+  int64_t pe = 0, se = 0;
+  for (const ChirpZDev* cz : {&P->edge, &P->blocks[0]}) {
+    int64_t a, b;
+    chirpz_workspace(*cz, chunk, &a, &b);
+    pe = std::max(pe, a);
+    se = std::max(se, b);
+  }
+  if (pe > 0) {
+    if (int rc = dalloc(tmp, &p, (size_t)pe * 8)) return rc;
+    part = (double*)p;
+  }
+  if (se > 0) {
+    if (int rc = dalloc(tmp, &p, (size_t)se * 16)) return rc;
+    spec = (double2*)p;
+  }
+  int launches = 0;
+  for (int64_t b0 = 0; b0 < n1; b0 += chunk) {
+    const int64_t nb = std::min(chunk, n1 - b0);
+    if (int rc = launch_identity(ein, n1, b0, nb, 0)) return rc;
+    if (int rc = launch_chirpz(P->edge, P->tw8192, ein, n1, vals, G1, nb, scratch, part, spec, 0, &launches))
+      return rc;
+    if (int rc = launch_chirpz(P->blocks[0], P->tw8192, vals, G1, eout, n1, nb, scratch, part, spec, 0, &launches))
+      return rc;
+    if (int rc = launch_to_bf16(eout, n1, (char*)P->gemm_X + (size_t)(b0 * n1) * 2, n1, n1, nb, 0)) return rc;
+  }
+  CJT_CUDA_TRY(cudaDeviceSynchronize());
   return CJT_OK;
 }
 
@@ -971,6 +1051,12 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     P->has_edge = true;
   } else if (!(P->half_exact && d->direction == CJT_FORWARD)) {
     return fail(CJT_EINVAL, "plan requires an edge (analysis / synthesis) chirp-z");
+  }
+  if (d->half_gemm) {
+    if (!P->half_exact || d->direction != CJT_INVERSE || !P->has_edge)
+      return fail(CJT_EINVAL, "half_gemm needs an exact-expansion inverse plan");
+    if (int rc = build_half_gemm_matrix(P.get())) return rc;
+    P->half_gemm = true;
   }
   if (d->direction == CJT_INVERSE) {
     if (!d->scalings) return fail(CJT_EINVAL, "inverse plan requires scalings");

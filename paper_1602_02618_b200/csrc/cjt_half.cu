@@ -17,6 +17,12 @@
 // exchange) adds the higher part, and the carry moves to the next tile; the
 // result is rounded once.
 
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+
+#include <map>
+#include <mutex>
+
 #include "cjt_internal.cuh"
 
 namespace cjt {
@@ -143,7 +149,121 @@ __global__ void __launch_bounds__(kThreads) k_half_forward(const double* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// alpha = beta = 1/2 inverse, small / moderate N (half_gemm plans):
+//   out = E t + M t,
+// E t the exact Chebyshev -> Jacobi conversion (T_0 = U_0, T_j = (U_j -
+// U_{j-2}) / 2, c_m = u_m / k_m: two coefficients per output), and M the
+// (N+1) x (N+1) first-order correction that moves the evaluation to the
+// reference's points (cjt_host.cpp), built once per plan by running the
+// synthesis + correction chirp-z products on the identity.  |M t| is ~1e-12
+// ||t||_1 (the reference's own deviation from the exact transform at
+// N = 4095), so M and t in bf16 with fp32 accumulation are ~1e3 x more
+// accurate than needed: the contraction runs on the tensor cores (cuBLAS
+// GemmEx; 2 (N+1)^2 flop per vector).
+
+__global__ void k_to_bf16(const double* __restrict__ in, int64_t ldi, __nv_bfloat16* __restrict__ out,
+                          int64_t ldo, int64_t n1, int64_t rows) {
+  const int64_t total = n1 * rows;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n1, c = e % n1;
+    out[r * ldo + c] = __double2bfloat16(in[r * ldi + c]);
+  }
+}
+
+__global__ void k_identity(double* buf, int64_t n1, int64_t b0, int64_t nb) {
+  const int64_t total = n1 * nb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n1, c = e % n1;
+    buf[e] = (c == b0 + r) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_half_inv_finish(const double* __restrict__ t, int64_t ldt, const float* __restrict__ corr,
+                                  int64_t ldc, const double* __restrict__ kt, double* __restrict__ out,
+                                  int64_t ldo, int64_t n1, int64_t batch) {
+  const int64_t total = n1 * batch;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / n1, m = e % n1;
+    const double* tb = t + b * ldt;
+    const double hi = m + 2 < n1 ? tb[m + 2] : 0.0;
+    const double u = (m == 0 ? tb[0] - 0.5 * hi : 0.5 * (tb[m] - hi));
+    out[b * ldo + m] = u / kt[m] + (double)corr[b * ldc + m];
+  }
+}
+
+inline unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32); }
+
+struct BlasKey {
+  int dev;
+  cudaStream_t st;
+  bool operator<(const BlasKey& o) const { return dev != o.dev ? dev < o.dev : st < o.st; }
+};
+
+// one cuBLAS handle per (device, stream), with its own workspace so calls are
+// capturable into CUDA graphs; created outside capture (first use / plan build)
+int blas_handle(cudaStream_t st, cublasHandle_t* out) {
+  static std::map<BlasKey, cublasHandle_t> handles;
+  static std::mutex mu;
+  int dev = 0;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = handles.find(BlasKey{dev, st});
+  if (it != handles.end()) {
+    *out = it->second;
+    return CJT_OK;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(CJT_EINVAL, "cuBLAS handle for this stream must exist before graph capture (run once uncaptured)");
+  cublasHandle_t h;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return fail(CJT_ECUDA, "cublasCreate failed");
+  void* ws = nullptr;
+  const size_t wsb = size_t(32) << 20;
+  CJT_CUDA_TRY(cudaMalloc(&ws, wsb));
+  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS || cublasSetWorkspace(h, ws, wsb) != CUBLAS_STATUS_SUCCESS)
+    return fail(CJT_ECUDA, "cublasSetStream / cublasSetWorkspace failed");
+  handles[BlasKey{dev, st}] = h;
+  *out = h;
+  return CJT_OK;
+}
+
 }  // namespace
+
+int launch_identity(double* buf, int64_t n1, int64_t b0, int64_t nb, cudaStream_t st) {
+  k_identity<<<grid_for(n1 * nb), 256, 0, st>>>(buf, n1, b0, nb);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int launch_to_bf16(const double* in, int64_t ldi, void* out, int64_t ldo, int64_t n1, int64_t rows, cudaStream_t st) {
+  k_to_bf16<<<grid_for(n1 * rows), 256, 0, st>>>(in, ldi, (__nv_bfloat16*)out, ldo, n1, rows);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* X, void* tbf,
+                      float* corr, const double* k, cudaStream_t st) {
+  if (batch <= 0) return CJT_OK;
+  if (int rc = launch_to_bf16(t, n1, tbf, n1, n1, batch, st)) return rc;
+  cublasHandle_t h;
+  if (int rc = blas_handle(st, &h)) return rc;
+  const float one = 1.0f, zero = 0.0f;
+  // column-major view: corr (n1 x B) = X^T-as-stored (n1 x n1, X[k][m] = M[m][k]) . t^T (n1 x B)
+  if (cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, (int)batch, (int)n1, &one, X, CUDA_R_16BF, (int)n1, tbf,
+                   CUDA_R_16BF, (int)n1, &zero, corr, CUDA_R_32F, (int)n1, CUBLAS_COMPUTE_32F,
+                   CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    return fail(CJT_ECUDA, "cublasGemmEx failed");
+  k_half_inv_finish<<<grid_for(n1 * batch), 256, 0, st>>>(t, n1, corr, n1, k, out, n1, n1, batch);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int half_gemm_prepare(cudaStream_t st) {
+  cublasHandle_t h;
+  return blas_handle(st, &h);
+}
 
 int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, const double* k,
                         int64_t n1, int64_t batch, cudaStream_t st) {

@@ -605,6 +605,15 @@ int build_device_spectra(const ChirpZDev& cz, const int64_t* tin_dev, const int6
 int permute_spectra(const double2* natural_host, int64_t L, int ntile, int mode, int log1, int log2,
                     std::vector<void*>& allocs, const double2** out);
 
+// alpha = beta = 1/2 inverse as exact conversion + bf16 tensor-core correction
+// (half_gemm plans), cjt_half.cu.  X: [n1][n1] bf16 (X[k][m] = M[m][k]),
+// tbf: [batch][n1] bf16 scratch, corr: [batch][n1] fp32 scratch.
+int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* X, void* tbf,
+                      float* corr, const double* k, cudaStream_t st);
+int half_gemm_prepare(cudaStream_t st);   // cuBLAS handle of `st` (outside capture)
+int launch_identity(double* buf, int64_t n1, int64_t b0, int64_t nb, cudaStream_t st);
+int launch_to_bf16(const double* in, int64_t ldi, void* out, int64_t ldo, int64_t n1, int64_t rows, cudaStream_t st);
+
 // alpha = beta = 1/2 forward (exact U -> T conversion), cjt_half.cu
 int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, const double* k,
                         int64_t n1, int64_t batch, cudaStream_t st);

@@ -135,6 +135,7 @@ class _DevicePlan:
         desc.scalings = arr(hp.scalings) if hp.scalings is not None else None
         desc.half_k = arr(hp.half_k) if hp.half_k is not None else None
         desc.thetas = arr(thetas)
+        desc.half_gemm = 1 if hp.half_gemm else 0
         desc.alpha, desc.beta = hp.p.alpha, hp.p.beta
         handle = ctypes.c_void_p()
         nat.check(L.cjt_plan_create(ctypes.byref(desc), ctypes.byref(handle)), "cjt_plan_create")

@@ -730,6 +730,7 @@ class HostPlan:
     scalings: np.ndarray | None = None
     # alpha = beta = 1/2 exact expansion (half_exact_enabled): k_n = P_n(1)/(n+1)
     half_k: np.ndarray | None = None
+    half_gemm: bool = False               # inverse: exact conversion + tensor-core correction
     exec_cuts: np.ndarray | None = None   # recurrence rows the device runs (None: cuts / rec_cuts)
 
     @property
@@ -773,6 +774,44 @@ def half_exact_tables(thetas: np.ndarray, regions: np.ndarray, g: int, n: int):
     return k, inv_sin, dos
 
 
+HALF_GEMM_MAX_N1 = 16384   # largest N+1 of the tensor-core correction ((N+1)^2 bf16 matrix per plan)
+
+
+def half_gemm_enabled(n: int) -> bool:
+    """alpha = beta = 1/2 inverse as exact conversion + correction GEMM for
+    N + 1 <= HALF_GEMM_MAX_N1 ($CJT_HALF_GEMM=0 keeps the one-chirp-z form)."""
+    import os
+    return n + 1 <= HALF_GEMM_MAX_N1 and os.environ.get("CJT_HALF_GEMM", "1") != "0"
+
+
+def half_correction_inverse(g: int, n: int, k: np.ndarray, inv_sin: np.ndarray, dos: np.ndarray,
+                            scalings: np.ndarray) -> ChirpZ:
+    """The reference's inverse minus the exact conversion, to first order in
+    the evaluation-point offsets delta_p (half_exact_tables):
+
+      M t [m] = k_m / A_m sum_p wv_p delta_p d/dtheta[sin(q theta)/sin theta](pi p/G)
+              = k_m / A_m [ q sum_p wv_p delta_p / sin theta_p cos(pi p q/G)
+                            - sum_p wv_p delta_p cos theta_p / sin^2 theta_p sin(pi p q/G) ],
+
+    q = m + 1, theta_p = pi p/G, wv = the weighted synthesis of t (edge);
+    endpoint rows have delta = 0.  The library applies it to the identity once
+    per plan to form the correction matrix (cjt_plan_desc.half_gemm)."""
+    p_ = np.arange(g + 1, dtype=np.float64)
+    th = np.pi * p_ / g
+    with np.errstate(divide="ignore", invalid="ignore"):
+        delta = np.where(inv_sin != 0.0, dos / inv_sin, 0.0)
+        s_, c_ = np.sin(th), np.cos(th)
+        pre = np.zeros((2, g + 1))
+        pre[0, 1:-1] = delta[1:-1] / s_[1:-1]
+        pre[1, 1:-1] = -delta[1:-1] * c_[1:-1] / (s_[1:-1] * s_[1:-1])
+    q = np.arange(1, n + 2, dtype=np.float64)
+    ks = k * scalings
+    post = np.empty((2, n + 1), dtype=np.complex128)
+    post[0] = ks * q
+    post[1] = -1j * ks
+    return chirpz(g, 0, g + 1, 1, n + 1, pre, post, accumulate=False, out_shift=1)
+
+
 def half_exact_inverse(g: int, n: int, k: np.ndarray, inv_sin: np.ndarray, dos: np.ndarray,
                        scalings: np.ndarray) -> ChirpZ:
     """The inverse's whole contraction for alpha = beta = 1/2 as ONE chirp-z
@@ -814,7 +853,11 @@ def _build_half_exact(hp: HostPlan) -> HostPlan:
         hp.weights = w
         hp.synthesis = chirpz(g, 0, n + 1, 0, g + 1, np.ones((1, n + 1)), w[None, :], accumulate=False)
         hp.scalings = 1.0 / orthonormality(hp.p, n)
-        hp.blocks = [half_exact_inverse(g, n, k, inv_sin, dos, hp.scalings)]
+        if half_gemm_enabled(n):
+            hp.half_gemm = True
+            hp.blocks = [half_correction_inverse(g, n, k, inv_sin, dos, hp.scalings)]
+        else:
+            hp.blocks = [half_exact_inverse(g, n, k, inv_sin, dos, hp.scalings)]
     return hp
 
 
