@@ -327,9 +327,17 @@ def remap_half_exact(model: dict, executed: dict, fhost, ihost, batch: int) -> N
         b["fwd_rec"], b["fwd_edge"] = batch * 8.0 * 2 * n1, 0.0
         executed["fwd_rec"] = None
     if ihost.half_k is not None:
-        f["inv_blocks"], f["inv_rec"] = f["inv_blocks"] + f["inv_rec"], 0.0
+        f["inv_blocks"], f["inv_rec"] = f["inv_blocks"] + f["inv_rec"] + f["inv_edge"], 0.0
         b["inv_blocks"], b["inv_rec"] = batch * 8.0 * ((ihost.grid_n + 1) + n1), 0.0
         executed["inv_rec"] = None
+        if getattr(ihost, "half_gemm", False):
+            # exact conversion + bf16 tensor-core correction (no fp64 FFT work per
+            # execution): it replaces the synthesis, blocks and recurrence
+            f["inv_edge"] = 0.0
+            b["inv_blocks"], b["inv_edge"] = batch * 16.0 * n1, 0.0
+            executed["inv_blocks"] = None
+        else:
+            f["inv_blocks"] -= f["inv_edge"]
 
 
 def survey_flops(fhost, ihost, batch: int) -> float:
@@ -804,20 +812,29 @@ def run_ours5(args, wl):
     graph.replay()
     torch.cuda.synchronize(dev)
     peak = ctypes_peak(L, st)
-    rec_flops = 0.0
+    # SURVEY 8(d) algorithmic work summed over the groups, per stage
+    model = {"flops": {k_: 0.0 for k_ in stage_ms}, "bytes": {k_: 0.0 for k_ in stage_ms}}
+    executed = {k_: 0.0 for k_ in stage_ms}
+    fft_exec = {"fwd": 0.0, "inv": 0.0}
     for g in range(len(rp.keys)):
-        for k in range(2):
+        fh, ih = rp.plans[g][0].host, rp.plans[g][1].host
+        m_ = stage_model(fh, ih, rp.sizes[g])
+        ex_ = {}
+        remap_half_exact(m_, ex_, fh, ih, rp.sizes[g])
+        for k_ in stage_ms:
+            model["flops"][k_] += m_["flops"][k_]
+            model["bytes"][k_] += m_["bytes"][k_]
+        for k, d in enumerate(("fwd", "inv")):
             s_ = rp.plans[g][k].device_plan(local).stats()
-            rec_flops += 2.0 * s_.rec_steps_executed * rp.sizes[g] + 5.0 * s_.rec_steps_executed
-    rec_ms = stage_ms["fwd_rec"] + stage_ms["inv_rec"]
-    achieved = rec_flops / (rec_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "bound_note": BOUND_NOTE, "kernel": "k_rec_gemm / k_rec_*_ws (K1+K2, all groups)", "stage": "fwd_rec+inv_rec",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                "traffic": None, "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains)",
-                "nominal_peak": NOMINAL_FP64_TFLOPS,
-                "flops_model": "2 flop per (point, degree, vector) contraction + 5 flop per (point, degree) generation",
-                "stage_ms": {k_: round(v, 4) for k_, v in stage_ms.items()},
-                "stage_share": {k_: round(v / sum(stage_ms.values()), 4) for k_, v in stage_ms.items()}}
+            executed[f"{d}_rec"] += 2.0 * s_.rec_steps_executed * rp.sizes[g] + 5.0 * s_.rec_steps_executed
+            fft_exec[d] += 5.0 * s_.fft_points_per_vector * rp.sizes[g]
+    for d in ("fwd", "inv"):
+        both = stage_ms[f"{d}_blocks"] + stage_ms[f"{d}_edge"]
+        for sname in ("blocks", "edge"):
+            executed[f"{d}_{sname}"] = fft_exec[d] * (stage_ms[f"{d}_{sname}"] / both if both > 0 else 0.0)
+    roofline = dominant_roofline(stage_ms, model, executed, peak, 5)
+    roofline["note"] = ("stage times are the groups' stages run back to back on one stream; the timed step "
+                        "overlaps groups on several streams")
     flop5 = sum(survey_flops(rp.plans[g][0].host, rp.plans[g][1].host, rp.sizes[g]) for g in range(len(rp.keys)))
     roofline["step"] = step_roofline(flop5, peak, ms_per_step, float(rp.total))
     e2e = None
