@@ -846,6 +846,7 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
 // products, rounded to bf16 (row b of X = column b of M).
 int build_half_gemm_matrix(cjt_plan* P) {
   const int64_t n1 = P->n + 1, G1 = P->G + 1;
+  CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));   // tables built on this thread's stream
   const int64_t chunk = std::min<int64_t>(n1, 512);
   std::vector<void*> tmp;
   struct Free {
@@ -1009,7 +1010,7 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   if (int rc = dalloc(A, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
   P->ck = (double2*)p;
   if (tot > 0) {
-    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, 0)) return rc;
+    if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, cudaStreamPerThread)) return rc;
   }
 
   // FFT twiddles exp(-2 pi i u / 8192)
@@ -1062,7 +1063,9 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     if (!d->scalings) return fail(CJT_EINVAL, "inverse plan requires scalings");
     if (int rc = upload(A, &P->scal, d->scalings, (size_t)(d->n + 1))) return rc;
   }
-  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  // plan-time kernels ran on this thread's stream (concurrent plan builds on
+  // several host threads do not serialise on the legacy stream)
+  CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
   *out = P.release();
   return CJT_OK;
 }

@@ -130,34 +130,68 @@ __global__ void k_permute_khat(const double2* __restrict__ src, double2* __restr
 
 struct FftKey {
   int dev;
-  int64_t L, batch;
-  bool operator<(const FftKey& o) const {
-    return dev != o.dev ? dev < o.dev : L != o.L ? L < o.L : batch < o.batch;
-  }
+  int64_t L;
+  bool operator<(const FftKey& o) const { return dev != o.dev ? dev < o.dev : L < o.L; }
 };
 
-int fft_plan(int64_t L, int64_t batch, cufftHandle* out) {
-  static std::map<FftKey, cufftHandle> cache;
+// one single-transform cuFFT plan per (device, length), shared by every
+// plan build (tiles are transformed one after another); cuFFT handles are not
+// safe to execute concurrently, so callers hold the returned lock
+int fft_plan(int64_t L, cufftHandle* out, std::unique_lock<std::mutex>* hold) {
+  static std::map<FftKey, std::pair<cufftHandle, std::mutex*>> cache;
   static std::mutex mu;
   int dev = 0;
   CJT_CUDA_TRY(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(FftKey{dev, L, batch});
-  if (it != cache.end()) {
-    *out = it->second;
-    return CJT_OK;
+  std::pair<cufftHandle, std::mutex*> entry;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(FftKey{dev, L});
+    if (it == cache.end()) {
+      cufftHandle h;
+      long long n = L;
+      size_t ws = 0;
+      if (cufftCreate(&h) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftCreate failed");
+      if (cufftMakePlanMany64(h, 1, &n, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, 1, &ws) != CUFFT_SUCCESS) {
+        cufftDestroy(h);
+        return fail(CJT_ECUDA, "cufftMakePlanMany64 failed (L = " + std::to_string(L) + ")");
+      }
+      it = cache.emplace(FftKey{dev, L}, std::make_pair(h, new std::mutex)).first;
+    }
+    entry = it->second;
   }
-  cufftHandle h;
-  long long n = L;
-  size_t ws = 0;
-  if (cufftCreate(&h) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftCreate failed");
-  if (cufftMakePlanMany64(h, 1, &n, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, (long long)batch, &ws) !=
-      CUFFT_SUCCESS) {
-    cufftDestroy(h);
-    return fail(CJT_ECUDA, "cufftMakePlanMany64 failed (L = " + std::to_string(L) + ")");
+  *hold = std::unique_lock<std::mutex>(*entry.second);
+  *out = entry.first;
+  return CJT_OK;
+}
+
+// per-thread grow-only scratch for the unpermuted spectra (no cudaFree, and
+// with it no implicit device synchronisation, per plan build)
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+  ~Scratch() {
+    if (p) cudaFree(p);
   }
-  cache[FftKey{dev, L, batch}] = h;
-  *out = h;
+};
+int scratch(size_t bytes, void** out) {
+  thread_local Scratch s;
+  int dev = 0;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  if (s.bytes < bytes || s.dev != dev) {
+    if (s.p) {
+      int cur = dev;
+      cudaSetDevice(s.dev);
+      cudaFree(s.p);
+      cudaSetDevice(cur);
+    }
+    s.p = nullptr;
+    s.bytes = 0;
+    CJT_CUDA_TRY(cudaMalloc(&s.p, bytes));
+    s.bytes = bytes;
+    s.dev = dev;
+  }
+  *out = s.p;
   return CJT_OK;
 }
 
@@ -184,13 +218,14 @@ int build_device_diag(const DevDiag& dd, int64_t len, int m_count, int64_t base,
   double2* d = (double2*)p;
   if (dd.kind == CJT_DIAG_MODULATION) {
     if (!grid.thetas || !grid.wa || !grid.wb) return fail(CJT_EINVAL, "modulation diagonal needs the plan grid");
-    k_modulation<<<blocks_for(len, 128), 128>>>(d, len, m_count, dd.row0, grid.thetas, grid.alpha, grid.beta,
+    k_modulation<<<blocks_for(len, 128), 128, 0, cudaStreamPerThread>>>(d, len, m_count, dd.row0, grid.thetas, grid.alpha, grid.beta,
                                                  grid.wa, grid.wb);
     CJT_CUDA_TRY(cudaGetLastError());
   } else {
-    CJT_CUDA_TRY(cudaMemcpy(d, dd.host, (size_t)m_count * len * sizeof(double2), cudaMemcpyHostToDevice));
+    CJT_CUDA_TRY(cudaMemcpyAsync(d, dd.host, (size_t)m_count * len * sizeof(double2), cudaMemcpyHostToDevice,
+                                 cudaStreamPerThread));
   }
-  k_fold_chirp<<<blocks_for(len, 256), 256>>>(d, len, m_count, base, G);
+  k_fold_chirp<<<blocks_for(len, 256), 256, 0, cudaStreamPerThread>>>(d, len, m_count, base, G);
   CJT_CUDA_TRY(cudaGetLastError());
   *out = d;
   return CJT_OK;
@@ -202,22 +237,24 @@ int build_device_spectra(const ChirpZDev& cz, const int64_t* tin_dev, const int6
   const int ntile = cz.n_in * cz.n_out;
   void *kp = nullptr, *dp = nullptr;
   if (int rc = dalloc_list(allocs, &dp, (size_t)ntile * L * sizeof(double2))) return rc;
-  CJT_CUDA_TRY(cudaMalloc(&kp, (size_t)ntile * L * sizeof(double2)));
-  struct Free {
-    void* p;
-    ~Free() { cudaFree(p); }
-  } fr{kp};
+  if (int rc = scratch((size_t)ntile * L * sizeof(double2), &kp)) return rc;
+  cudaStream_t st = cudaStreamPerThread;
   dim3 g1(blocks_for(L, 256), (unsigned)ntile);
-  k_spectrum_kernels<<<g1, 256>>>((double2*)kp, L, cz.n_in, cz.n_out, tin_dev, tout_dev, cz.p0, cz.q0, G);
+  k_spectrum_kernels<<<g1, 256, 0, st>>>((double2*)kp, L, cz.n_in, cz.n_out, tin_dev, tout_dev, cz.p0, cz.q0, G);
   CJT_CUDA_TRY(cudaGetLastError());
-  cufftHandle h;
-  if (int rc = fft_plan(L, ntile, &h)) return rc;
-  if (cufftSetStream(h, 0) != CUFFT_SUCCESS || cufftExecZ2Z(h, (cufftDoubleComplex*)kp, (cufftDoubleComplex*)kp,
-                                                           CUFFT_FORWARD) != CUFFT_SUCCESS)
-    return fail(CJT_ECUDA, "cufftExecZ2Z failed");
-  k_permute_khat<<<g1, 256>>>((const double2*)kp, (double2*)dp, L, mode, cz.log1, cz.log2, 1.0 / (double)L);
+  {
+    cufftHandle h;
+    std::unique_lock<std::mutex> hold;
+    if (int rc = fft_plan(L, &h, &hold)) return rc;
+    if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftSetStream failed");
+    for (int t = 0; t < ntile; ++t) {
+      cufftDoubleComplex* x = (cufftDoubleComplex*)kp + (size_t)t * L;
+      if (cufftExecZ2Z(h, x, x, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftExecZ2Z failed");
+    }
+  }
+  k_permute_khat<<<g1, 256, 0, st>>>((const double2*)kp, (double2*)dp, L, mode, cz.log1, cz.log2, 1.0 / (double)L);
   CJT_CUDA_TRY(cudaGetLastError());
-  CJT_CUDA_TRY(cudaDeviceSynchronize());   // kp is freed on return
+  CJT_CUDA_TRY(cudaStreamSynchronize(st));   // the scratch is reused by this thread's next build
   *out = (const double2*)dp;
   return CJT_OK;
 }
@@ -231,16 +268,13 @@ int permute_spectra(const double2* natural_host, int64_t L, int ntile, int mode,
     *out = (const double2*)dp;
     return CJT_OK;
   }
-  CJT_CUDA_TRY(cudaMalloc(&sp, (size_t)ntile * L * sizeof(double2)));
-  struct Free {
-    void* p;
-    ~Free() { cudaFree(p); }
-  } fr{sp};
-  CJT_CUDA_TRY(cudaMemcpy(sp, natural_host, (size_t)ntile * L * sizeof(double2), cudaMemcpyHostToDevice));
+  if (int rc = scratch((size_t)ntile * L * sizeof(double2), &sp)) return rc;
+  cudaStream_t st = cudaStreamPerThread;
+  CJT_CUDA_TRY(cudaMemcpyAsync(sp, natural_host, (size_t)ntile * L * sizeof(double2), cudaMemcpyHostToDevice, st));
   dim3 g1(blocks_for(L, 256), (unsigned)ntile);
-  k_permute_khat<<<g1, 256>>>((const double2*)sp, (double2*)dp, L, mode, log1, log2, 1.0);
+  k_permute_khat<<<g1, 256, 0, st>>>((const double2*)sp, (double2*)dp, L, mode, log1, log2, 1.0);
   CJT_CUDA_TRY(cudaGetLastError());
-  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  CJT_CUDA_TRY(cudaStreamSynchronize(st));
   *out = (const double2*)dp;
   return CJT_OK;
 }

@@ -26,7 +26,7 @@ class RaggedPlan:
     """Plans and device layout for a ragged list of (alpha, beta, N), one per vector."""
 
     def __init__(self, params, m_terms: int = DEFAULT_M, eps: float = DEFAULT_EPS,
-                 groups_subset=None, threads: int = 8):
+                 groups_subset=None, threads: int = 16, device: int | None = None, upload: bool = True):
         params = [(float(a), float(b), int(n)) for a, b, n in params]
         order = collections.OrderedDict()
         for i, key in enumerate(params):
@@ -38,10 +38,18 @@ class RaggedPlan:
         self.members = [order[k] for k in keys]        # original vector indices per group
         self.sizes = [len(m) for m in self.members]
 
+        device = engine._current_device() if device is None else device
+
         def build(key):
+            # host plan and device upload in the same worker: the library's
+            # plan builds run on per-thread streams and overlap
             a, b, n = key
             p = JacobiParameters(a, b)
-            return (engine.plan("forward", p, n, m_terms, eps), engine.plan("inverse", p, n, m_terms, eps))
+            pair = (engine.plan("forward", p, n, m_terms, eps), engine.plan("inverse", p, n, m_terms, eps))
+            if upload:
+                for tp in pair:
+                    tp.device_plan(device)
+            return pair
 
         with cf.ThreadPoolExecutor(max_workers=threads) as ex:
             self.plans = list(ex.map(build, keys))
