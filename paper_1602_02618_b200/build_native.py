@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = True, out: Path | None = None) ->
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(target),
-           *map(str, objs), "-lquadmath", "-lcufft", "-lcublas", "-lpthread"]
+           *map(str, objs), "-lquadmath", "-lcublas", "-lpthread"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

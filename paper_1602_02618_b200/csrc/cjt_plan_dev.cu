@@ -2,7 +2,7 @@
 // chirp phases, the diagonal tables with their chirps folded in, the
 // modulation functions u_m - i v_m of the asymptotic blocks
 // (asymptotics.py:36-75), and the Bluestein kernel spectra of every tile
-// (planner._spectrum; cuFFT at plan time), laid out in the order the
+// (planner._spectrum; a radix-2 Stockham FFT at plan time), laid out in the order the
 // execution kernels read them.  The host only decides the tiling.
 //
 // Numerics: chirp(k) = exp(i pi k^2 / (2G)) with k^2 reduced exactly mod 4G in
@@ -12,10 +12,7 @@
 // whose last-bit differences are far below the transform tolerance
 // (tests/test_gpu_plan_dev.py compares device- and host-built plans).
 
-#include <cufft.h>
-
-#include <map>
-#include <mutex>
+#include <utility>
 
 #include "cjt_internal.cuh"
 
@@ -128,40 +125,26 @@ __global__ void k_permute_khat(const double2* __restrict__ src, double2* __restr
   d[e] = make_double2(v.x * scale, v.y * scale);
 }
 
-struct FftKey {
-  int dev;
-  int64_t L;
-  bool operator<(const FftKey& o) const { return dev != o.dev ? dev < o.dev : L < o.L; }
-};
-
-// one single-transform cuFFT plan per (device, length), shared by every
-// plan build (tiles are transformed one after another); cuFFT handles are not
-// safe to execute concurrently, so callers hold the returned lock
-int fft_plan(int64_t L, cufftHandle* out, std::unique_lock<std::mutex>* hold) {
-  static std::map<FftKey, std::pair<cufftHandle, std::mutex*>> cache;
-  static std::mutex mu;
-  int dev = 0;
-  CJT_CUDA_TRY(cudaGetDevice(&dev));
-  std::pair<cufftHandle, std::mutex*> entry;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(FftKey{dev, L});
-    if (it == cache.end()) {
-      cufftHandle h;
-      long long n = L;
-      size_t ws = 0;
-      if (cufftCreate(&h) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftCreate failed");
-      if (cufftMakePlanMany64(h, 1, &n, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, 1, &ws) != CUFFT_SUCCESS) {
-        cufftDestroy(h);
-        return fail(CJT_ECUDA, "cufftMakePlanMany64 failed (L = " + std::to_string(L) + ")");
-      }
-      it = cache.emplace(FftKey{dev, L}, std::make_pair(h, new std::mutex)).first;
-    }
-    entry = it->second;
-  }
-  *hold = std::unique_lock<std::mutex>(*entry.second);
-  *out = entry.first;
-  return CJT_OK;
+// One radix-2 Stockham pass (forward, exp(-2 pi i ...)) over `ntile`
+// independent transforms of length L = 2^n: pass with Ns = 2^p reads
+// in[j], in[j + L/2] and writes the butterfly at (j / Ns) 2 Ns + j % Ns (+ Ns).
+// Plan-time only (every tile's Bluestein kernel spectrum): log2 L launches,
+// twiddles from sincospi, error O(log L) ulp like any radix-2 FFT.
+__global__ void k_fft_r2_pass(const double2* __restrict__ in, double2* __restrict__ out, int64_t L, int64_t ns) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tile = blockIdx.y;
+  const int64_t half = L / 2;
+  if (j >= half) return;
+  const double2* x = in + tile * L;
+  double2* y = out + tile * L;
+  const int64_t k = j & (ns - 1);
+  double s, c;
+  sincospi(-(double)k / (double)ns, &s, &c);
+  const double2 v0 = x[j];
+  const double2 v1 = cmul(x[j + half], make_double2(c, s));
+  const int64_t d = (j - k) * 2 + k;
+  y[d] = cadd(v0, v1);
+  y[d + ns] = csub(v0, v1);
 }
 
 // per-thread grow-only scratch for the unpermuted spectra (no cudaFree, and
@@ -235,24 +218,23 @@ int build_device_spectra(const ChirpZDev& cz, const int64_t* tin_dev, const int6
                          int mode, std::vector<void*>& allocs, const double2** out) {
   const int64_t L = cz.length;
   const int ntile = cz.n_in * cz.n_out;
+  const size_t elems = (size_t)ntile * L;
   void *kp = nullptr, *dp = nullptr;
-  if (int rc = dalloc_list(allocs, &dp, (size_t)ntile * L * sizeof(double2))) return rc;
-  if (int rc = scratch((size_t)ntile * L * sizeof(double2), &kp)) return rc;
+  if (int rc = dalloc_list(allocs, &dp, elems * sizeof(double2))) return rc;
+  if (int rc = scratch(2 * elems * sizeof(double2), &kp)) return rc;
+  double2* a = (double2*)kp;
+  double2* b = a + elems;
   cudaStream_t st = cudaStreamPerThread;
   dim3 g1(blocks_for(L, 256), (unsigned)ntile);
-  k_spectrum_kernels<<<g1, 256, 0, st>>>((double2*)kp, L, cz.n_in, cz.n_out, tin_dev, tout_dev, cz.p0, cz.q0, G);
+  k_spectrum_kernels<<<g1, 256, 0, st>>>(a, L, cz.n_in, cz.n_out, tin_dev, tout_dev, cz.p0, cz.q0, G);
   CJT_CUDA_TRY(cudaGetLastError());
-  {
-    cufftHandle h;
-    std::unique_lock<std::mutex> hold;
-    if (int rc = fft_plan(L, &h, &hold)) return rc;
-    if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftSetStream failed");
-    for (int t = 0; t < ntile; ++t) {
-      cufftDoubleComplex* x = (cufftDoubleComplex*)kp + (size_t)t * L;
-      if (cufftExecZ2Z(h, x, x, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(CJT_ECUDA, "cufftExecZ2Z failed");
-    }
+  dim3 gh(blocks_for(L / 2, 256), (unsigned)ntile);
+  for (int64_t ns = 1; ns < L; ns *= 2) {
+    k_fft_r2_pass<<<gh, 256, 0, st>>>(a, b, L, ns);
+    std::swap(a, b);
   }
-  k_permute_khat<<<g1, 256, 0, st>>>((const double2*)kp, (double2*)dp, L, mode, cz.log1, cz.log2, 1.0 / (double)L);
+  CJT_CUDA_TRY(cudaGetLastError());
+  k_permute_khat<<<g1, 256, 0, st>>>(a, (double2*)dp, L, mode, cz.log1, cz.log2, 1.0 / (double)L);
   CJT_CUDA_TRY(cudaGetLastError());
   CJT_CUDA_TRY(cudaStreamSynchronize(st));   // the scratch is reused by this thread's next build
   *out = (const double2*)dp;
