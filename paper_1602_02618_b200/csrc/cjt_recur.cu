@@ -40,25 +40,6 @@ __device__ __forceinline__ void rec_init(int reg, double& s0, double& s1) {
     s1 = 0.0;
   }
 }
-// degree n -> n+1 (reference arithmetic, _kernels_cy.pyx:144-147, 186-188)
-__device__ __forceinline__ void rec_step(int reg, double x, double xm, const RecTablesDev& t,
-                                         int64_t n, double& s0, double& s1) {
-  const double a = __ldg(t.A + n);
-  const double c = __ldg(t.C + n);
-  if (reg == 0) {
-    const double bb = __ldg(t.B + n);
-    const double pn = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(a, x), bb), s1), __dmul_rn(c, s0));
-    s0 = s1;
-    s1 = pn;
-  } else {
-    const double rf = __ldg((reg > 0 ? t.rfp : t.rfm) + n);
-    const double rfi = __ldg((reg > 0 ? t.rfpi : t.rfmi) + n);
-    const double d = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, xm), s0), __dmul_rn(c, s1)), rfi);
-    s0 = __dmul_rn(__dadd_rn(s0, d), rf);
-    s1 = d;
-  }
-}
-
 __device__ __forceinline__ void load_state(const RecRowsDev& rows, const int64_t* ck_off,
                                            const double2* ck, int64_t i, int64_t n0, int reg,
                                            double& s0, double& s1) {
@@ -251,19 +232,56 @@ __global__ void k_build_inv_gen(RecRowsDev rows, const int64_t* __restrict__ ck_
   out[gi] = st;
 }
 
-__global__ void k_checkpoints(RecRowsDev rows, RecTablesDev tab, const int64_t* __restrict__ ck_off,
-                              double2* __restrict__ ck) {
+// Plan-time recurrence checkpoints (s0, s1) every CK degrees of every row,
+// in the reference's exact rounding (rec_step).  Each row is a serial chain;
+// the table entries of a window of degrees are staged in shared memory once
+// per CTA (all its rows step through the same degrees), so a step costs the
+// chain's own latency instead of a global load round trip.
+constexpr int CKW = 256;   // degrees per staged window
+__global__ void __launch_bounds__(128) k_checkpoints(RecRowsDev rows, RecTablesDev tab,
+                                                     const int64_t* __restrict__ ck_off, double2* __restrict__ ck) {
+  __shared__ double w[7][CKW];
+  __shared__ int64_t s_max;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows.nrows) return;
-  const int reg = rows.reg[i];
-  const double x = rows.x[i], xm = rows.xm[i];
-  const int64_t nc = rows.cut[i];
+  const bool live = i < rows.nrows;
+  const int reg = live ? rows.reg[i] : 0;
+  const double x = live ? rows.x[i] : 0.0, xm = live ? rows.xm[i] : 0.0;
+  const int64_t nc = live ? rows.cut[i] : 0;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  atomicMax((unsigned long long*)&s_max, (unsigned long long)nc);
+  __syncthreads();
+  const int64_t top = s_max;   // the CTA's longest chain
   double s0, s1;
   rec_init(reg, s0, s1);
-  double2* out = ck + ck_off[i];
-  for (int64_t n = 0; n + 1 < nc; ++n) {
-    rec_step(reg, x, xm, tab, n, s0, s1);
-    if (((n + 1) % CK) == 0) out[(n + 1) / CK - 1] = make_double2(s0, s1);
+  double2* out = live ? ck + ck_off[i] : nullptr;
+  const double* rf_t = reg > 0 ? &w[3][0] : &w[4][0];
+  const double* rfi_t = reg > 0 ? &w[5][0] : &w[6][0];
+  for (int64_t n0 = 0; n0 + 1 < top; n0 += CKW) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 7 * CKW; e += blockDim.x) {
+      const int r = e / CKW, k = e % CKW;
+      const int64_t n = n0 + k;
+      const double* src = r == 0 ? tab.A : r == 1 ? tab.B : r == 2 ? tab.C : r == 3 ? tab.rfp
+                        : r == 4 ? tab.rfm : r == 5 ? tab.rfpi : tab.rfmi;
+      w[r][k] = n < tab.n_tab ? __ldg(src + n) : 0.0;
+    }
+    __syncthreads();
+    const int64_t n1 = min(n0 + CKW, nc - 1);
+    for (int64_t n = n0; n < n1; ++n) {
+      const int k = (int)(n - n0);
+      const double a = w[0][k], c = w[2][k];
+      if (reg == 0) {
+        const double pn = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(a, x), w[1][k]), s1), __dmul_rn(c, s0));
+        s0 = s1;
+        s1 = pn;
+      } else {
+        const double d = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, xm), s0), __dmul_rn(c, s1)), rfi_t[k]);
+        s0 = __dmul_rn(__dadd_rn(s0, d), rf_t[k]);
+        s1 = d;
+      }
+      if (((n + 1) % CK) == 0) out[(n + 1) / CK - 1] = make_double2(s0, s1);
+    }
   }
 }
 
