@@ -14,6 +14,8 @@
 //     3. K2 recurrence contraction (degrees <= N only)   -> partials
 //     4. fixed-order reduction, + acc, * 1/A_n           -> out[b][0..N]
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -234,6 +236,38 @@ inline void unit_root(int64_t num, int64_t den, double* re, double* im) {
   *im = (double)sinl(ang);
 }
 
+// Twiddle tables shared by every plan of a device (immutable, built once per
+// length with long-double trigonometry and kept for the process lifetime):
+// L = 8192: exp(-2 pi i u / 8192), u < 8192; multi-pass L: the hi table
+// exp(-2 pi i a 4096 / L), a < max(1, L / 4096), followed by the lo table
+// exp(-2 pi i b / L), b < 4096.
+int shared_twiddles(int64_t L, const double2** out) {
+  static std::map<std::pair<int, int64_t>, void*> cache;
+  static std::mutex mu;
+  int dev = 0;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, L});
+  if (it == cache.end()) {
+    std::vector<double2> tw;
+    if (L == 8192) {
+      tw.resize(8192);
+      for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
+    } else {
+      const int64_t nhi = std::max<int64_t>(1, L / 4096);
+      tw.resize((size_t)(nhi + 4096));
+      for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, L, &tw[a].x, &tw[a].y);
+      for (int64_t b = 0; b < 4096; ++b) unit_root(b, L, &tw[nhi + b].x, &tw[nhi + b].y);
+    }
+    void* p = nullptr;
+    CJT_CUDA_TRY(cudaMalloc(&p, tw.size() * sizeof(double2)));
+    CJT_CUDA_TRY(cudaMemcpy(p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    it = cache.emplace(std::make_pair(dev, L), p).first;
+  }
+  *out = (const double2*)it->second;
+  return CJT_OK;
+}
+
 int log2_exact(int64_t v) {
   int l = 0;
   while ((int64_t(1) << l) < v) ++l;
@@ -326,12 +360,10 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
       return rc;
   }
   if (lg >= 14) {
-    const int64_t nhi = std::max<int64_t>(1, d.length / 4096);
-    std::vector<double2> hi((size_t)nhi), lo(4096);
-    for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, d.length, &hi[a].x, &hi[a].y);
-    for (int64_t b = 0; b < 4096; ++b) unit_root(b, d.length, &lo[b].x, &lo[b].y);
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_hi), hi.data(), hi.size())) return rc;
-    if (int rc = upload(P->allocs, const_cast<double2**>(&cz.tw_lo), lo.data(), lo.size())) return rc;
+    const double2* t = nullptr;
+    if (int rc = shared_twiddles(d.length, &t)) return rc;
+    cz.tw_hi = t;
+    cz.tw_lo = t + std::max<int64_t>(1, d.length / 4096);
   }
   if (lg >= 14 && !cluster) {
     // one slot per input or output tile per (vector, term)
@@ -941,6 +973,20 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   if (G != (d->direction == CJT_FORWARD ? d->n : 2 * d->n)) return fail(CJT_EINVAL, "grid_n inconsistent with direction");
   int ndev = 0;
   if (cjt_device_count(&ndev) || ndev == 0) return fail(CJT_ENODEV, "no CUDA device visible");
+  // $CJT_PLAN_TIMING=1 (diagnostics): phase times of this build on stderr
+  static const bool timing = [] {
+    const char* e = getenv("CJT_PLAN_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(cudaStreamPerThread);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[cjt plan G=%lld] %-12s %8.3f ms\n", (long long)d->grid_n, what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   std::unique_ptr<cjt_plan> P(new cjt_plan());
   CJT_CUDA_TRY(cudaGetDevice(&P->device));
   P->direction = d->direction;
@@ -996,6 +1042,7 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     P->nrows_fold = G / 2 + 1;   // rows 0 .. G/2 (G even: the middle row is its own mirror)
   }
 
+  phase("upload");
   // recurrence checkpoints every CK degrees
   std::vector<int64_t> off((size_t)nr);
   int64_t tot = 0;
@@ -1013,10 +1060,13 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     if (int rc = launch_checkpoints(P->rows, P->tab, P->ck_off, P->ck, cudaStreamPerThread)) return rc;
   }
 
-  // FFT twiddles exp(-2 pi i u / 8192)
-  std::vector<double2> tw(8192);
-  for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
-  if (int rc = upload(A, &P->tw8192, tw.data(), tw.size())) return rc;
+  phase("checkpoints");
+  // FFT twiddles exp(-2 pi i u / 8192), shared by every plan of the device
+  {
+    const double2* t = nullptr;
+    if (int rc = shared_twiddles(8192, &t)) return rc;
+    P->tw8192 = const_cast<double2*>(t);
+  }
 
   if (d->thetas) {
     double* th = nullptr;
@@ -1047,6 +1097,7 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     if (int rc = build_chirpz(P.get(), d->blocks[k], &cz)) return rc;
     P->blocks.push_back(cz);
   }
+  phase("blocks");
   if (d->edge.length > 0) {
     if (int rc = build_chirpz(P.get(), d->edge, &P->edge)) return rc;
     P->has_edge = true;
@@ -1066,6 +1117,7 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   // plan-time kernels ran on this thread's stream (concurrent plan builds on
   // several host threads do not serialise on the legacy stream)
   CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
+  phase("edge+finish");
   *out = P.release();
   return CJT_OK;
 }
@@ -1521,9 +1573,11 @@ int cjt_chirpz_create(const cjt_chirpz_desc* d, cjt_chirpz_plan** out) {
   C->owner.reset(new cjt_plan());
   cjt_plan* P = C->owner.get();
   CJT_CUDA_TRY(cudaGetDevice(&P->device));
-  std::vector<double2> tw(8192);
-  for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
-  if (int rc = upload(P->allocs, &P->tw8192, tw.data(), tw.size())) return rc;
+  {
+    const double2* t = nullptr;
+    if (int rc = shared_twiddles(8192, &t)) return rc;
+    P->tw8192 = const_cast<double2*>(t);
+  }
   if (int rc = build_chirpz(P, *d, &C->cz)) return rc;
   C->in_len = d->p0 + d->width;
   C->out_len = d->q0 - d->out_shift + d->count;
