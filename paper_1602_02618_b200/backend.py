@@ -60,9 +60,10 @@ class _KernelPlan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value and nat._lib is not None:
+        lib_ = getattr(nat, "_lib", None) if nat is not None else None   # None at interpreter exit
+        if h is not None and h.value and lib_ is not None:
             try:
-                nat._lib.cjt_kernel_plan_destroy(h)
+                lib_.cjt_kernel_plan_destroy(h)
             except Exception:
                 pass
 
