@@ -338,6 +338,18 @@ def remap_half_exact(model: dict, executed: dict, fhost, ihost, batch: int) -> N
             executed["inv_blocks"] = None
         else:
             f["inv_blocks"] -= f["inv_edge"]
+    # the kernels' own rooflines (what bounds the work they actually do): the
+    # U -> T scan moves 16 B per coefficient (HBM); the correction GEMM does
+    # 2 (N+1)^2 bf16 flop per vector on the tensor cores
+    kinds = model.setdefault("kind", {})
+    if fhost.half_k is not None:
+        kinds["fwd_rec"] = ("hbm", batch * 16.0 * n1,
+                            "k_half_fwd_scan (alpha = beta = 1/2 exact U -> T conversion): read c, write cheb")
+    if ihost.half_k is not None and getattr(ihost, "half_gemm", False):
+        kinds["inv_blocks"] = ("tensor", batch * 2.0 * n1 * n1,
+                               "alpha = beta = 1/2 inverse: k_to_bf16 + cuBLAS bf16 GEMM (first-order "
+                               "correction to the reference's points) + k_half_inv_finish (exact T -> U); "
+                               "achieved = the GEMM's 2 (N+1)^2 flop per vector over the whole stage time")
 
 
 def survey_flops(fhost, ihost, batch: int) -> float:
@@ -383,6 +395,26 @@ def dominant_roofline(stages_ms: dict, model: dict, executed: dict, peak: float,
             traffic = None
     ex = executed.get(dom)
     ab = model["bytes"][dom]
+    stage_ms = {k: round(v, 4) for k, v in stages_ms.items()}
+    stage_share = {k: round(v / sum(stages_ms.values()), 4) for k, v in stages_ms.items()}
+    kind = model.get("kind", {}).get(dom)
+    if kind is not None:
+        bound, work, kname = kind
+        peaks = measured_peaks()
+        if bound == "hbm":
+            achieved, pk, unit = work / t / 1e9, peaks["hbm_gbs"], "GB/s"
+        else:
+            achieved, pk, unit = work / t / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+        return {
+            "bound": bound, "kernel": kname, "stage": dom, "achieved": achieved, "peak": pk, "unit": unit,
+            "frac": achieved / pk, "traffic": traffic,
+            "traffic_note": "ncu dram__bytes_read+write of one execution of this stage (profiles/ncu_traffic.json)",
+            "algorithmic_bytes" if bound == "hbm" else "algorithmic_flop": work,
+            "peak_source": peaks["source"] + (" (hbm_gbs)" if bound == "hbm" else " (bf16_tflops, burst: the stage "
+                                                                                  "is timed alone)"),
+            "fp64_peak_measured": peak,
+            "stage_ms": stage_ms, "stage_share": stage_share,
+        }
     return {
         "bound": "fp64", "bound_note": BOUND_NOTE, "kernel": kern, "stage": dom,
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -399,9 +431,19 @@ def dominant_roofline(stages_ms: dict, model: dict, executed: dict, peak: float,
                     "generation; FFT 5 L log2 L per complex FFT executed)"},
         "peak_source": "measured on this GPU by cjt_probe_fp64_peak (DFMA chains); nominal 37.2",
         "nominal_peak": NOMINAL_FP64_TFLOPS,
-        "stage_ms": {k: round(v, 4) for k, v in stages_ms.items()},
-        "stage_share": {k: round(v / sum(stages_ms.values()), 4) for k, v in stages_ms.items()},
+        "stage_ms": stage_ms, "stage_share": stage_share,
     }
+
+
+def measured_peaks() -> dict:
+    """HBM GB/s and bf16 TF/s from the driver-written MEASURED_PEAKS.json, else
+    the profiling recipe's fallback (6650 GB/s, 1590 TF/s)."""
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "source": "of measured (MEASURED_PEAKS.json)"}
+    except (OSError, ValueError, KeyError, TypeError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "of fallback (B200_PROFILING.md)"}
 
 
 def shard_batch(config: int, n: int, total: int, world: int, rank: int) -> tuple[int, int, np.ndarray]:

@@ -120,6 +120,7 @@ struct cjt_plan {
     double* io_out = nullptr;
     void* tbf = nullptr;       // half_gemm: bf16 copy of the input [B][N+1]
     float* corr = nullptr;     // half_gemm: fp32 correction [B][N+1]
+    double* htot = nullptr;    // half forward: per-chunk (even, odd) totals
   };
   std::map<cudaStream_t, Workspace> ws;
   std::mutex ws_mu;
@@ -729,6 +730,11 @@ int get_workspace(cjt_plan* P, cudaStream_t st, cjt_plan::Workspace** out) {
   if (int rc = dalloc(W.allocs, &p, (size_t)(part_elems * batch) * 8)) return rc;
   W.part = (double*)p;
   bytes += part_elems * batch * 8;
+  if (P->half_exact && P->direction == CJT_FORWARD && half_forward_scratch(N1) > 0) {
+    if (int rc = dalloc(W.allocs, &p, (size_t)(half_forward_scratch(N1) * batch) * 8)) return rc;
+    W.htot = (double*)p;
+    bytes += half_forward_scratch(N1) * batch * 8;
+  }
   if (!(P->half_exact && P->direction == CJT_FORWARD)) {   // the exact forward needs no grid values
     if (int rc = dalloc(W.allocs, &p, (size_t)(G1 * batch) * 8)) return rc;
     W.vals = (double*)p;
@@ -794,8 +800,8 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
   const bool rec = stages & CJT_STAGE_REC, blk = stages & CJT_STAGE_BLOCKS, edge = stages & CJT_STAGE_EDGE;
   if (P->half_exact && P->direction == CJT_FORWARD) {
     if (rec) {
-      if (int rc = launch_half_forward(in, N1, out, N1, P->half_k, N1, batch, st)) return rc;
-      launches += 1;
+      if (int rc = launch_half_forward(in, N1, out, N1, P->half_k, N1, batch, W.htot, st)) return rc;
+      launches += half_forward_scratch(N1) > 0 ? 2 : 1;
     }
   } else if (P->half_gemm) {
     if (blk) {

@@ -10,16 +10,18 @@
 // closed form matches its results to rounding (tests/test_gpu_half.py).
 //
 // HBM-bound: 16 B per coefficient (read c, write cheb) plus the k table
-// (L2-resident).  One CTA per vector walks the vector from the top in tiles
-// of 4 * kThreads pairs: every thread forms the exact products k_n c_n
-// (two_prod) and its local suffix sums in double-double, a block-wide
-// exclusive suffix scan of the thread totals (warp shuffles + one shared
-// exchange) adds the higher part, and the carry moves to the next tile; the
-// result is rounded once.
+// (L2-resident).  A CTA of 512 threads takes a 4096-coefficient chunk of one
+// vector (8 consecutive coefficients per thread): every thread forms its
+// local (even, odd) sums with fused products, a block-wide exclusive suffix
+// scan (warp shuffles + one shared-memory exchange) adds the part above it,
+// and the local suffix sums are re-formed from there.  Vectors longer than
+// one chunk add a first launch of per-chunk totals; each chunk then sums the
+// totals above it in a fixed order (no atomics: bit-identical re-executions).
 
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -28,124 +30,397 @@
 namespace cjt {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kPairs = 4;              // (even, odd) coefficient pairs per thread per tile
-constexpr int kTile = 2 * kPairs * kThreads;
+// Chunks of kFChunk coefficients: kFThreads threads x kFE consecutive
+// coefficients each.  A vector longer than one chunk is scanned in two
+// launches: per-chunk (even, odd) totals, then every chunk adds the totals of
+// the chunks above it (fixed order) as its carry.
+constexpr int kFThreads = 512;
+constexpr int kFE = 8;
+constexpr int kFChunk = kFThreads * kFE;   // 4096
+constexpr int kFRun = kFE + 1;             // odd smem stride per thread (bank spread)
+constexpr int kFWarps = kFThreads / 32;
 
-struct dd {
-  double hi, lo;
+// (even, odd) running sums.  Plain fp64 with fused products: every result is
+// a sum along a path of at most ~4 sequential + 9 tree + log2(chunks) adds,
+// so its rounding error is <= ~20 eps sum |k_n c_n| <= 5e-15 ||c||_1 in the
+// worst case (~1e-17 for random-sign data); a double-double scan would cost
+// 6x the fp64 work and make this HBM-bound kernel fp64-bound on B200.
+struct eo {
+  double e, o;
 };
-
-__device__ __forceinline__ dd dd_add(dd a, dd b) {
-  const double s = a.hi + b.hi;
-  const double bb = s - a.hi;
-  double e = (a.hi - (s - bb)) + (b.hi - bb);
-  e += a.lo + b.lo;
-  const double h = s + e;
-  return dd{h, e - (h - s)};
+__device__ __forceinline__ eo eo_add(eo a, eo b) { return eo{a.e + b.e, a.o + b.o}; }
+__device__ __forceinline__ eo shfl_down_eo(eo v, int d) {
+  return eo{__shfl_down_sync(0xffffffffu, v.e, d), __shfl_down_sync(0xffffffffu, v.o, d)};
 }
 
-__device__ __forceinline__ dd dd_prod(double a, double b) {
-  const double p = a * b;
-  return dd{p, fma(a, b, -p)};
+// k_n of this thread's kFE coefficients (the table is L2-resident, shared by
+// every vector)
+__device__ __forceinline__ void load_k(const double* __restrict__ kt, int64_t base, int64_t n1,
+                                       double (&k)[kFE]) {
+  if (base + kFE <= n1) {
+    const double2* k2 = reinterpret_cast<const double2*>(kt + base);
+#pragma unroll
+    for (int q = 0; q < kFE / 2; ++q) {
+      const double2 w = __ldg(k2 + q);
+      k[2 * q] = w.x;
+      k[2 * q + 1] = w.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kFE; ++e) k[e] = base + e < n1 ? __ldg(kt + base + e) : 0.0;
+  }
 }
 
-__device__ __forceinline__ dd shfl_down_dd(dd v, int d) {
-  return dd{__shfl_down_sync(0xffffffffu, v.hi, d), __shfl_down_sync(0xffffffffu, v.lo, d)};
+// this thread's (even, odd) totals of k_n c_n over its kFE coefficients
+__device__ __forceinline__ eo thread_totals(const double (&v)[kFE], const double (&k)[kFE]) {
+  eo s{0.0, 0.0};
+#pragma unroll
+  for (int e = kFE - 1; e >= 0; --e) {
+    if (e & 1) s.o = fma(k[e], v[e], s.o); else s.e = fma(k[e], v[e], s.e);
+  }
+  return s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_half_forward(const double* __restrict__ c, int64_t ldc,
-                                                           double* __restrict__ out, int64_t ldo,
-                                                           const double* __restrict__ kt, int64_t n1) {
-  const int64_t b = blockIdx.x;
-  const double* cb = c + b * ldc;
-  double* ob = out + b * ldo;
+// carry from the chunks above chunk ch (fixed order), lanes of one warp
+__device__ __forceinline__ eo chunk_carry(const eo* __restrict__ tot, int64_t b, int64_t nch, int64_t ch,
+                                          int lane) {
+  eo c{0.0, 0.0};
+  if (tot == nullptr) return c;
+  for (int64_t q = nch - 1 - lane; q > ch; q -= 32) c = eo_add(c, tot[b * nch + q]);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) c = eo_add(c, shfl_down_eo(c, d));
+  return eo{__shfl_sync(0xffffffffu, c.e, 0), __shfl_sync(0xffffffffu, c.o, 0)};
+}
+
+// Block-wide exclusive suffix of the thread totals s plus the chunk carry:
+// the (even, odd) sums of every coefficient of the chunk above this thread's.
+__device__ __forceinline__ eo block_suffix(eo s, eo* s_w, const eo* __restrict__ tot, int64_t b, int64_t nch,
+                                           int64_t ch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ dd s_warp[2][kThreads / 32];
-  // thread-owned runs of 2 kPairs entries, padded to an odd stride (bank spread)
-  constexpr int kRun = 2 * kPairs + 1;
-  __shared__ double s_tile[kThreads * kRun];
-  dd carry_e{0.0, 0.0}, carry_o{0.0, 0.0};   // sums of all higher tiles (even / odd degrees)
-  const int64_t ntiles = (n1 + kTile - 1) / kTile;
-  for (int64_t t = ntiles - 1; t >= 0; --t) {
-    const int64_t t0 = t * kTile;
-    // coalesced tile load, then each thread takes 2 kPairs consecutive entries
+  eo inc = s;
 #pragma unroll
-    for (int e = 0; e < 2 * kPairs; ++e) {
-      const int64_t j = t0 + e * kThreads + threadIdx.x;
-      const int l = e * kThreads + threadIdx.x;
-      s_tile[(l / (2 * kPairs)) * kRun + l % (2 * kPairs)] = j < n1 ? cb[j] : 0.0;
+  for (int d = 1; d < 32; d <<= 1) {
+    const eo u = shfl_down_eo(inc, d);
+    if (lane + d < 32) inc = eo_add(inc, u);
+  }
+  if (lane == 0) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const eo carry = chunk_carry(tot, b, nch, ch, lane);
+    eo w = lane < kFWarps ? s_w[lane] : eo{0.0, 0.0};
+#pragma unroll
+    for (int d = 1; d < kFWarps; d <<= 1) {
+      const eo u = shfl_down_eo(w, d);
+      if (lane + d < kFWarps) w = eo_add(w, u);
     }
-    __syncthreads();
-    const int64_t base = t0 + (int64_t)threadIdx.x * (2 * kPairs);
-    double v[2 * kPairs];
+    const eo x = shfl_down_eo(w, 1);
+    __syncwarp();
+    if (lane < kFWarps) s_w[lane] = lane + 1 < kFWarps ? eo_add(carry, x) : carry;
+  }
+  __syncthreads();
+  eo h = s_w[warp];
+  const eo x = shfl_down_eo(inc, 1);
+  if (lane < 31) h = eo_add(h, x);
+  return h;
+}
+
+// results: v[e] <- e_j * (suffix sum at j = base + e), from the exclusive part h
+__device__ __forceinline__ void thread_results(double (&v)[kFE], const double (&k)[kFE], int64_t base, eo h) {
 #pragma unroll
-    for (int e = 0; e < 2 * kPairs; ++e) v[e] = s_tile[threadIdx.x * kRun + e];
-    // local suffix sums, exact products
-    dd se{0.0, 0.0}, so{0.0, 0.0};
-    dd loc[2 * kPairs];
-#pragma unroll
-    for (int e = 2 * kPairs - 1; e >= 0; --e) {
-      const int64_t j = base + e;
-      const dd pr = j < n1 ? dd_prod(__ldg(kt + j), v[e]) : dd{0.0, 0.0};
-      if (e & 1) {
-        so = dd_add(so, pr);
-        loc[e] = so;
-      } else {
-        se = dd_add(se, pr);
-        loc[e] = se;
-      }
+  for (int e = kFE - 1; e >= 0; --e) {
+    if (e & 1) {
+      h.o = fma(k[e], v[e], h.o);
+      v[e] = 2.0 * h.o;
+    } else {
+      h.e = fma(k[e], v[e], h.e);
+      v[e] = (base + e == 0 ? 1.0 : 2.0) * h.e;
     }
-    // inclusive suffix scan of (se, so) over the threads of the block
-    dd ie = se, io = so;
+  }
+}
+
+// this thread's kFE coefficients j0 + 8t .. j0 + 8t + 7, coalesced through
+// shared memory (padded runs)
+__device__ __forceinline__ void half_load(const double* __restrict__ cb, int64_t j0, int64_t n1, double* s,
+                                          double (&v)[kFE]) {
+  const int t = threadIdx.x;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const dd ue = shfl_down_dd(ie, d), uo = shfl_down_dd(io, d);
-      if (lane + d < 32) {
-        ie = dd_add(ie, ue);
-        io = dd_add(io, uo);
-      }
-    }
+  for (int e = 0; e < kFE; ++e) {
+    const int l = e * kFThreads + t;
+    const int64_t j = j0 + l;
+    s[(l / kFE) * kFRun + l % kFE] = j < n1 ? __ldcs(cb + j) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kFE; ++e) v[e] = s[t * kFRun + e];
+}
+
+// block totals (even, odd) of one chunk: phase 1 of a multi-chunk scan
+__global__ void __launch_bounds__(kFThreads) k_half_fwd_totals(const double* __restrict__ c, int64_t ldc,
+                                                               const double* __restrict__ kt, int64_t n1,
+                                                               eo* __restrict__ tot) {
+  __shared__ double s[kFThreads * kFRun];
+  __shared__ eo s_w[kFWarps];
+  const int64_t b = blockIdx.y;
+  const int64_t j0 = (int64_t)blockIdx.x * kFChunk;
+  double v[kFE], k[kFE];
+  half_load(c + b * ldc, j0, n1, s, v);
+  load_k(kt, j0 + (int64_t)threadIdx.x * kFE, n1, k);
+  eo sum = thread_totals(v, k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) sum = eo_add(sum, shfl_down_eo(sum, d));
+  if (lane == 0) s_w[warp] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    eo tt{0.0, 0.0};
+    for (int w = kFWarps - 1; w >= 0; --w) tt = eo_add(tt, s_w[w]);
+    tot[b * gridDim.x + blockIdx.x] = tt;
+  }
+}
+
+// cheb_j = e_j * sum_{n >= j, n = j (mod 2)} k_n c_n over one chunk (general
+// strides; the aligned case runs k_half_fwd_stream)
+__global__ void __launch_bounds__(kFThreads, 2) k_half_fwd_scan(const double* __restrict__ c, int64_t ldc,
+                                                                double* __restrict__ out, int64_t ldo,
+                                                                const double* __restrict__ kt, int64_t n1,
+                                                                const eo* __restrict__ tot) {
+  __shared__ double s[kFThreads * kFRun];
+  __shared__ eo s_w[kFWarps];
+  const int64_t b = blockIdx.y, ch = blockIdx.x;
+  const int64_t j0 = ch * kFChunk;
+  const int64_t base = j0 + (int64_t)threadIdx.x * kFE;
+  double v[kFE], k[kFE];
+  half_load(c + b * ldc, j0, n1, s, v);
+  load_k(kt, base, n1, k);
+  const eo h = block_suffix(thread_totals(v, k), s_w, tot, b, gridDim.x, ch);
+  thread_results(v, k, base, h);
+  // only this thread read its run of s (half_load's barrier precedes)
+#pragma unroll
+  for (int e = 0; e < kFE; ++e) s[threadIdx.x * kFRun + e] = v[e];
+  __syncthreads();
+  double* ob = out + b * ldo;
+#pragma unroll
+  for (int e = 0; e < kFE; ++e) {
+    const int l = e * kFThreads + threadIdx.x;
+    const int64_t j = j0 + l;
+    if (j < n1) __stcs(ob + j, s[(l / kFE) * kFRun + l % kFE]);
+  }
+}
+
+// Warp-per-vector form (rows 16-byte aligned, N+1 even, N+1 <= kWarpMaxN1):
+// one warp walks its vectors from the top in 256-coefficient sub-chunks.
+// Every global access is a 1-D TMA bulk copy: the k table is staged in
+// shared memory once per CTA, each sub-chunk arrives in the warp's own
+// kWStages-deep ring (one mbarrier per stage) and its results leave from the
+// same stage by a bulk store.  Lane l owns the coefficients l + 32 e (e < 8)
+// of a sub-chunk, so its shared-memory words are consecutive across the warp
+// (conflict-free 8-byte accesses, registers in natural order) and all of a
+// lane's coefficients have the parity of l: the suffix sum of (e, l) is a
+// same-parity shuffle scan of row e over the lanes >= l, plus the parity's
+// totals of the rows above and of the sub-chunks above (a register carry).
+// No CTA barriers after the k table.  The kernel is chosen by the layout only
+// (never by the batch size), so a vector's result does not depend on how
+// many share the call.
+constexpr int64_t kWarpMaxN1 = 8192;
+constexpr int kWStages = 3;
+constexpr int kWWarps = 24;
+constexpr int kWSmem = kWWarps * kWStages * 256 * 8 + (int)kWarpMaxN1 * 8;   // 208 KB
+
+__global__ void __launch_bounds__(kWWarps * 32, 1) k_half_fwd_warp(const double* __restrict__ c, int64_t ldc,
+                                                                   double* __restrict__ out, int64_t ldo,
+                                                                   const double* __restrict__ kt, int n1,
+                                                                   int64_t batch) {
+  extern __shared__ __align__(128) double wbuf[];   // [warp][kWStages][256], then k[n1]
+  __shared__ __align__(8) uint64_t wbar[kWWarps][kWStages];
+  __shared__ __align__(8) uint64_t kbar;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int par = lane & 1;
+  double* ks = wbuf + kWWarps * kWStages * 256;
+  double* mybuf = wbuf + wid * (kWStages * 256);
+  uint64_t* mybar = wbar[wid];
+  if (threadIdx.x == 0) {
+    mbar_init(&kbar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&kbar, (uint32_t)n1 * 8);
+    bulk_g2s(ks, kt, (uint32_t)n1 * 8, &kbar);
+  }
+  if (lane == 0) {
+    for (int q = 0; q < kWStages; ++q) mbar_init(&mybar[q], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int64_t w = (int64_t)blockIdx.x * kWWarps + wid, nw = (int64_t)gridDim.x * kWWarps;
+  const int nsub = (n1 + 255) / 256;
+  const int64_t nvec = w < batch ? (batch - 1 - w) / nw + 1 : 0;
+  const int64_t items = nvec * nsub;
+  // sub-chunk i of this warp's sequence: vector w + (i / nsub) nw, rows from the top
+  auto issue = [&](int64_t i) {   // lane 0
+    if (i >= items) return;
+    const int64_t r = i / nsub;
+    const int j0 = (nsub - 1 - (int)(i - r * nsub)) * 256;
+    const uint32_t bytes = (uint32_t)((n1 - j0 < 256 ? n1 - j0 : 256) * 8);
+    uint64_t* br = &mybar[i % kWStages];
+    mbar_expect_tx(br, bytes);
+    bulk_g2s(mybuf + (i % kWStages) * 256, c + (w + r * nw) * ldc + j0, bytes, br);
+  };
+  if (lane == 0)
+    for (int q = 0; q < kWStages - 1; ++q) issue(q);
+  __syncthreads();                 // barrier inits visible; k table requested
+  mbar_wait(&kbar, 0);
+  double carry = 0.0;              // this lane's parity: sum over the sub-chunks above
+  int64_t r = 0;
+  int sc = nsub - 1;
+  for (int64_t i = 0; i < items; ++i) {
     if (lane == 0) {
-      s_warp[0][warp] = ie;
-      s_warp[1][warp] = io;
+      bulk_wait_read0();           // the store of iteration i - 1 has read its stage
+      issue(i + kWStages - 1);     // ... which is the stage refilled now
     }
-    __syncthreads();
-    // higher warps' totals and the carry of the higher tiles
-    dd he = carry_e, ho = carry_o;
-    for (int w = kThreads / 32 - 1; w > warp; --w) {
-      he = dd_add(he, s_warp[0][w]);
-      ho = dd_add(ho, s_warp[1][w]);
-    }
-    // exclusive (this thread's higher neighbours within the warp)
-    const dd xe = shfl_down_dd(ie, 1), xo = shfl_down_dd(io, 1);
-    if (lane < 31) {
-      he = dd_add(he, xe);
-      ho = dd_add(ho, xo);
-    }
-    __syncthreads();   // every thread has read its inputs from s_tile
+    const int j0 = sc * 256;
+    const int cnt = n1 - j0 < 256 ? n1 - j0 : 256;
+    double* sb = mybuf + (i % kWStages) * 256;
+    const double* kb = ks + j0;
+    mbar_wait(&mybar[i % kWStages], (uint32_t)((i / kWStages) & 1));
+    double x[kFE];
 #pragma unroll
-    for (int e = 0; e < 2 * kPairs; ++e) {
-      const int64_t j = base + e;
-      const dd s = dd_add(loc[e], (e & 1) ? ho : he);
-      s_tile[threadIdx.x * kRun + e] = (j == 0 ? 1.0 : 2.0) * s.hi;
+    for (int e = 0; e < kFE; ++e) {
+      const int l = lane + 32 * e;
+      x[e] = l < cnt ? kb[l] * sb[l] : 0.0;   // past N+1: stale shared memory, masked
     }
-    __syncthreads();
+    // row e: inclusive same-parity suffix over the lanes >= lane
 #pragma unroll
-    for (int e = 0; e < 2 * kPairs; ++e) {
-      const int64_t j = t0 + e * kThreads + threadIdx.x;
-      const int l = e * kThreads + threadIdx.x;
-      if (j < n1) ob[j] = s_tile[(l / (2 * kPairs)) * kRun + l % (2 * kPairs)];
+    for (int d = 2; d < 32; d <<= 1) {
+#pragma unroll
+      for (int e = 0; e < kFE; ++e) {
+        const double u = __shfl_down_sync(0xffffffffu, x[e], d);
+        if (lane + d < 32) x[e] += u;
+      }
     }
-    // carry for the next (lower) tile: every warp's total
-    dd te = carry_e, to = carry_o;
-    for (int w = kThreads / 32 - 1; w >= 0; --w) {
-      te = dd_add(te, s_warp[0][w]);
-      to = dd_add(to, s_warp[1][w]);
+    double acc = carry;
+#pragma unroll
+    for (int e = kFE - 1; e >= 0; --e) {
+      const double row = __shfl_sync(0xffffffffu, x[e], par);   // the row's total of this parity
+      const int l = lane + 32 * e;
+      if (l < cnt) sb[l] = (j0 + l == 0 ? 1.0 : 2.0) * (x[e] + acc);
+      acc += row;
     }
-    carry_e = te;
-    carry_o = to;
+    carry = acc;
+    fence_proxy_async();     // this lane's generic writes -> the async proxy (bulk store)
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(out + (w + r * nw) * ldo + j0, sb, (uint32_t)cnt * 8);
+      bulk_commit();
+    }
+    if (--sc < 0) {
+      sc = nsub - 1;
+      ++r;
+      carry = 0.0;
+    }
+  }
+  if (lane == 0) bulk_wait0();   // stores complete before the CTA's shared memory goes away
+}
+
+// Streaming form (rows 16-byte aligned, N+1 even): a persistent grid of 2
+// CTAs per SM walks the (vector, chunk) units; each chunk arrives by one 1-D
+// TMA bulk copy into a kSStages-deep shared-memory ring (mbarrier
+// completion), so the next chunks' HBM reads run under this chunk's scan.
+// Each thread reads its 8 consecutive coefficients as 4 rotated 16-byte
+// words (bank-conflict free), writes its results back the same way, and the
+// CTA stores the chunk coalesced.
+constexpr int kSStages = 3;
+
+__device__ __forceinline__ void rot_load8(const double* sb, int t, double (&v)[kFE]) {
+  const double2* s2 = reinterpret_cast<const double2*>(sb + kFE * t);
+  const int rot = (t >> 1) & 3;
+  double2 w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) w[q] = s2[(q + rot) & 3];
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    const int idx = (sl - rot) & 3;
+    double2 a = w[0];
+    a = idx == 1 ? w[1] : a;
+    a = idx == 2 ? w[2] : a;
+    a = idx == 3 ? w[3] : a;
+    v[2 * sl] = a.x;
+    v[2 * sl + 1] = a.y;
+  }
+}
+
+__device__ __forceinline__ void rot_store8(double* sb, int t, const double (&r)[kFE]) {
+  double2* s2 = reinterpret_cast<double2*>(sb + kFE * t);
+  const int rot = (t >> 1) & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int sl = (q + rot) & 3;
+    double x = r[0], y = r[1];
+#pragma unroll
+    for (int c = 1; c < 4; ++c) {
+      x = sl == c ? r[2 * c] : x;
+      y = sl == c ? r[2 * c + 1] : y;
+    }
+    s2[sl] = make_double2(x, y);
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads, 2) k_half_fwd_stream(const double* __restrict__ c, int64_t ldc,
+                                                                  double* __restrict__ out, int64_t ldo,
+                                                                  const double* __restrict__ kt, int64_t n1,
+                                                                  int64_t nch, int64_t units,
+                                                                  const eo* __restrict__ tot) {
+  extern __shared__ __align__(128) double sbuf[];   // [kSStages][kFChunk]
+  __shared__ __align__(8) uint64_t bar[kSStages];
+  __shared__ eo s_w[kFWarps];
+  const int t = threadIdx.x;
+  auto issue = [&](int64_t i) {   // thread 0: TMA the chunk of this CTA's i-th unit
+    const int64_t u = (int64_t)blockIdx.x + i * gridDim.x;
+    if (u >= units) return;
+    const int64_t b = u / nch, j0 = (u % nch) * kFChunk;
+    const uint32_t bytes = (uint32_t)((n1 - j0 < kFChunk ? n1 - j0 : (int64_t)kFChunk) * 8);
+    uint64_t* br = &bar[i % kSStages];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(br, bytes);
+    bulk_g2s(sbuf + (i % kSStages) * kFChunk, c + b * ldc + j0, bytes, br);
+  };
+  if (t == 0) {
+    for (int q = 0; q < kSStages; ++q) mbar_init(&bar[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int q = 0; q < kSStages - 1; ++q) issue(q);
+  // k_n of this thread's positions: kept in registers across units of the
+  // same chunk index (every unit when the vector is one chunk)
+  double k[kFE];
+  int64_t kch = -1;
+  for (int64_t i = 0; (int64_t)blockIdx.x + i * gridDim.x < units; ++i) {
+    if (t == 0) issue(i + kSStages - 1);   // its stage was released by iteration i - 1
+    const int64_t u = (int64_t)blockIdx.x + i * gridDim.x;
+    const int64_t b = u / nch, ch = u % nch, j0 = ch * kFChunk;
+    double* sb = sbuf + (i % kSStages) * kFChunk;
+    mbar_wait(&bar[i % kSStages], (uint32_t)((i / kSStages) & 1));
+    double v[kFE];
+    rot_load8(sb, t, v);
+    const int64_t base = j0 + (int64_t)t * kFE;
+    if (base + kFE > n1) {   // the tail past N+1 holds stale shared memory
+#pragma unroll
+      for (int e = 0; e < kFE; ++e) v[e] = base + e < n1 ? v[e] : 0.0;
+    }
+    if (ch != kch) {
+      load_k(kt, base, n1, k);
+      kch = ch;
+    }
+    const eo h = block_suffix(thread_totals(v, k), s_w, tot, b, nch, ch);
+    thread_results(v, k, base, h);
+    rot_store8(sb, t, v);
     __syncthreads();
+    double* ob = out + b * ldo;
+    const int64_t cnt = n1 - j0 < kFChunk ? n1 - j0 : (int64_t)kFChunk;
+#pragma unroll
+    for (int e = 0; e < kFE; ++e) {
+      const int l = e * kFThreads + t;
+      if (l < cnt) __stcs(ob + j0 + l, sb[l]);
+    }
+    __syncthreads();   // the stage and s_w are free for later units
   }
 }
 
@@ -162,13 +437,26 @@ __global__ void __launch_bounds__(kThreads) k_half_forward(const double* __restr
 // accurate than needed: the contraction runs on the tensor cores (cuBLAS
 // GemmEx; 2 (N+1)^2 flop per vector).
 
-__global__ void k_to_bf16(const double* __restrict__ in, int64_t ldi, __nv_bfloat16* __restrict__ out,
-                          int64_t ldo, int64_t n1, int64_t rows) {
-  const int64_t total = n1 * rows;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / n1, c = e % n1;
-    out[r * ldo + c] = __double2bfloat16(in[r * ldi + c]);
+// row-major [rows][n1] f64 -> bf16 (contiguous rows: ldi == ldo == n1 in every
+// caller), 4 elements per thread (two 16-byte loads, one 8-byte store)
+__global__ void k_to_bf16(const double* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t total) {
+  const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nq = total / 4;
+  for (int64_t q = q0; q < nq; q += stride) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(in) + 2 * q);
+    const double2 b = __ldcs(reinterpret_cast<const double2*>(in) + 2 * q + 1);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(0.f, 0.f), hi = lo;
+    lo.x = __double2bfloat16(a.x);
+    lo.y = __double2bfloat16(a.y);
+    hi.x = __double2bfloat16(b.x);
+    hi.y = __double2bfloat16(b.y);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&lo);
+    w.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(out)[q] = w;
   }
+  for (int64_t e = 4 * nq + q0; e < total; e += stride) out[e] = __double2bfloat16(in[e]);
 }
 
 __global__ void k_identity(double* buf, int64_t n1, int64_t b0, int64_t nb) {
@@ -179,16 +467,42 @@ __global__ void k_identity(double* buf, int64_t n1, int64_t b0, int64_t nb) {
   }
 }
 
-__global__ void k_half_inv_finish(const double* __restrict__ t, int64_t ldt, const float* __restrict__ corr,
-                                  int64_t ldc, const double* __restrict__ kt, double* __restrict__ out,
-                                  int64_t ldo, int64_t n1, int64_t batch) {
-  const int64_t total = n1 * batch;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = e / n1, m = e % n1;
-    const double* tb = t + b * ldt;
-    const double hi = m + 2 < n1 ? tb[m + 2] : 0.0;
-    const double u = (m == 0 ? tb[0] - 0.5 * hi : 0.5 * (tb[m] - hi));
-    out[b * ldo + m] = u / kt[m] + (double)corr[b * ldc + m];
+// out[b][m] = u_m / k_m + corr[b][m], u = E t (T_0 = U_0, T_j = (U_j -
+// U_{j-2}) / 2): persistent CTAs walk the rows, two coefficients per thread
+// per step (16-byte loads of t[m..m+1] and t[m+2..m+3]; N+1 even)
+__global__ void __launch_bounds__(256) k_half_inv_finish(const double* __restrict__ t,
+                                                         const float* __restrict__ corr,
+                                                         const double* __restrict__ kt,
+                                                         double* __restrict__ out, int64_t n1, int64_t batch) {
+  const int64_t h = n1 / 2;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const double2* tb = reinterpret_cast<const double2*>(t + b * n1);
+    const float2* cb = reinterpret_cast<const float2*>(corr + b * n1);
+    double2* ob = reinterpret_cast<double2*>(out + b * n1);
+    for (int64_t q = threadIdx.x; q < h; q += blockDim.x) {
+      const double2 lo = __ldcs(tb + q);
+      const double2 hi = q + 1 < h ? __ldcs(tb + q + 1) : make_double2(0.0, 0.0);
+      const float2 cr = __ldcs(cb + q);
+      const double2 k2 = __ldg(reinterpret_cast<const double2*>(kt) + q);
+      const double u0 = q == 0 ? lo.x - 0.5 * hi.x : 0.5 * (lo.x - hi.x);
+      const double u1 = 0.5 * (lo.y - hi.y);
+      __stcs(ob + q, make_double2(u0 / k2.x + (double)cr.x, u1 / k2.y + (double)cr.y));
+    }
+  }
+}
+
+// odd N+1 (any layout): one coefficient per thread per step
+__global__ void __launch_bounds__(256) k_half_inv_finish1(const double* __restrict__ t,
+                                                          const float* __restrict__ corr,
+                                                          const double* __restrict__ kt,
+                                                          double* __restrict__ out, int64_t n1, int64_t batch) {
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const double* tb = t + b * n1;
+    for (int64_t m = threadIdx.x; m < n1; m += blockDim.x) {
+      const double hi = m + 2 < n1 ? tb[m + 2] : 0.0;
+      const double u = (m == 0 ? tb[0] - 0.5 * hi : 0.5 * (tb[m] - hi));
+      out[b * n1 + m] = u / kt[m] + (double)corr[b * n1 + m];
+    }
   }
 }
 
@@ -238,7 +552,8 @@ int launch_identity(double* buf, int64_t n1, int64_t b0, int64_t nb, cudaStream_
 }
 
 int launch_to_bf16(const double* in, int64_t ldi, void* out, int64_t ldo, int64_t n1, int64_t rows, cudaStream_t st) {
-  k_to_bf16<<<grid_for(n1 * rows), 256, 0, st>>>(in, ldi, (__nv_bfloat16*)out, ldo, n1, rows);
+  if (ldi != n1 || ldo != n1) return fail(CJT_EINVAL, "launch_to_bf16: rows must be contiguous");
+  k_to_bf16<<<grid_for((n1 * rows + 3) / 4), 256, 0, st>>>(in, (__nv_bfloat16*)out, n1 * rows);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -255,7 +570,11 @@ int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, c
                    CUDA_R_16BF, (int)n1, &zero, corr, CUDA_R_32F, (int)n1, CUBLAS_COMPUTE_32F,
                    CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
     return fail(CJT_ECUDA, "cublasGemmEx failed");
-  k_half_inv_finish<<<grid_for(n1 * batch), 256, 0, st>>>(t, n1, corr, n1, k, out, n1, n1, batch);
+  const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 8);
+  if (n1 % 2 == 0 && ((uintptr_t)t & 15) == 0 && ((uintptr_t)out & 15) == 0)
+    k_half_inv_finish<<<grid, 256, 0, st>>>(t, corr, k, out, n1, batch);
+  else
+    k_half_inv_finish1<<<grid, 256, 0, st>>>(t, corr, k, out, n1, batch);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }
@@ -265,11 +584,56 @@ int half_gemm_prepare(cudaStream_t st) {
   return blas_handle(st, &h);
 }
 
+int64_t half_forward_scratch(int64_t n1) {
+  const int64_t nch = (n1 + kFChunk - 1) / kFChunk;
+  return nch > 1 ? nch * 2 : 0;   // doubles per vector: (even, odd) totals per chunk
+}
+
 int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, const double* k,
-                        int64_t n1, int64_t batch, cudaStream_t st) {
+                        int64_t n1, int64_t batch, double* scratch, cudaStream_t st) {
   if (batch <= 0) return CJT_OK;
-  if (batch > 0x7fffffffLL) return fail(CJT_EINVAL, "batch too large");
-  k_half_forward<<<(unsigned)batch, kThreads, 0, st>>>(c, ldc, out, ldo, k, n1);
+  const int64_t nch = (n1 + kFChunk - 1) / kFChunk;
+  if (nch > 1 && scratch == nullptr) return fail(CJT_EINVAL, "half forward: missing chunk-total scratch");
+  const bool stream = n1 % 2 == 0 && ldc % 2 == 0 && ((uintptr_t)c & 15) == 0 && !getenv("CJT_HALF_NOSTREAM");
+  static DeviceOnce once;
+  constexpr int smem = kSStages * kFChunk * 8;
+  if (stream)
+    if (int rc = once([] {
+          CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_fwd_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          return CJT_OK;
+        }))
+      return rc;
+  int dev = 0, sms = 148;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // the kernel is chosen by the layout only (never by the batch size), so a
+  // vector's result does not depend on how many vectors share the call
+  if (stream && n1 <= kWarpMaxN1 && ((uintptr_t)k & 15) == 0 && ldo % 2 == 0 && ((uintptr_t)out & 15) == 0 && !getenv("CJT_HALF_NOWARP")) {
+    static DeviceOnce wonce;
+    if (int rc = wonce([] {
+          CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_fwd_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
+          return CJT_OK;
+        }))
+      return rc;
+    const unsigned ctas = (unsigned)std::min<int64_t>((batch + kWWarps - 1) / kWWarps, (int64_t)sms);
+    k_half_fwd_warp<<<ctas, kWWarps * 32, kWSmem, st>>>(c, ldc, out, ldo, k, (int)n1, batch);
+    CJT_CUDA_TRY(cudaGetLastError());
+    return CJT_OK;
+  }
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    const dim3 grid((unsigned)nch, (unsigned)nb);
+    eo* tot = nch > 1 ? reinterpret_cast<eo*>(scratch) + b0 * nch : nullptr;
+    if (tot) k_half_fwd_totals<<<grid, kFThreads, 0, st>>>(c + b0 * ldc, ldc, k, n1, tot);
+    if (stream) {
+      const int64_t units = nb * nch;
+      const unsigned ctas = (unsigned)std::min<int64_t>(units, 2LL * sms);
+      k_half_fwd_stream<<<ctas, kFThreads, smem, st>>>(c + b0 * ldc, ldc, out + b0 * ldo, ldo, k, n1, nch, units,
+                                                       tot);
+    } else {
+      k_half_fwd_scan<<<grid, kFThreads, 0, st>>>(c + b0 * ldc, ldc, out + b0 * ldo, ldo, k, n1, tot);
+    }
+  }
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }

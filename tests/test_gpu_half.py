@@ -41,7 +41,7 @@ def test_half_exact_vs_reference_goldens(cuda, name, monkeypatch):
         assert O.parity(i[v], g["inv"][v], g["fwd"][v]) <= 1e-13
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 17, 255, 1000, 2047, 8191])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 17, 255, 1000, 2047, 4095, 4096, 8191, 12288])
 def test_half_exact_vs_recurrence_layout(cuda, n, monkeypatch):
     """Same inputs through both device paths (the recurrence layout is the
     reference's own algorithm, parity-pinned elsewhere), and the oracle."""
