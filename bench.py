@@ -344,12 +344,14 @@ def remap_half_exact(model: dict, executed: dict, fhost, ihost, batch: int) -> N
     kinds = model.setdefault("kind", {})
     if fhost.half_k is not None:
         kinds["fwd_rec"] = ("hbm", batch * 16.0 * n1,
-                            "k_half_fwd_scan (alpha = beta = 1/2 exact U -> T conversion): read c, write cheb")
+                            "k_half_fwd_warp (alpha = beta = 1/2 exact U -> T conversion, TMA-fed warp scans): "
+                            "read c, write cheb")
     if ihost.half_k is not None and getattr(ihost, "half_gemm", False):
         kinds["inv_blocks"] = ("tensor", batch * 2.0 * n1 * n1,
-                               "alpha = beta = 1/2 inverse: k_to_bf16 + cuBLAS bf16 GEMM (first-order "
-                               "correction to the reference's points) + k_half_inv_finish (exact T -> U); "
-                               "achieved = the GEMM's 2 (N+1)^2 flop per vector over the whole stage time")
+                               "alpha = beta = 1/2 inverse: k_to_bf16 + k_half_inv_umma (tcgen05 bf16 GEMM of "
+                               "the first-order correction to the reference's points, TMEM accumulators, fp64 "
+                               "exact T -> U fused into the epilogue); achieved = the GEMM's 2 (N+1)^2 flop per "
+                               "vector over the whole stage time (both kernels)")
 
 
 def survey_flops(fhost, ihost, batch: int) -> float:
@@ -383,8 +385,6 @@ def dominant_roofline(stages_ms: dict, model: dict, executed: dict, peak: float,
     kern = {"fwd_rec": "k_rec_forward_ws / k_pgen_fwd + k_rec_gemm (K1)",
             "inv_rec": "k_rec_inverse_ws / k_pgen_inv + k_rec_gemm (K2)"}.get(
         dom, "k_chirpz_* (Bluestein chirp-z, K3/K4)")
-    if model.get("half_exact") and dom == "fwd_rec":
-        kern = "k_half_forward (alpha = beta = 1/2 exact U -> T conversion)"
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():

@@ -80,7 +80,8 @@ struct cjt_plan {
   bool half_exact = false;
   double* half_k = nullptr;
   // inverse, moderate N: exact conversion + bf16 tensor-core correction with
-  // the per-plan matrix X = M^T (cjt_half.cu), built from edge + blocks[0]
+  // the per-plan matrix M, row-major [m][k] (cjt_half.cu, cjt_umma.cu), built
+  // from edge + blocks[0]
   bool half_gemm = false;
   void* gemm_X = nullptr;
   // grid angles and (alpha, beta) on the device: modulation diagonals built here
@@ -879,9 +880,10 @@ int execute(cjt_plan* P, const double* in, double* out, int64_t batch, cudaStrea
   return CJT_OK;
 }
 
-// X = M^T of a half_gemm plan: M e_b for the unit vectors e_b, in chunks,
-// through the plan's synthesis (edge) and correction (blocks[0]) chirp-z
-// products, rounded to bf16 (row b of X = column b of M).
+// M of a half_gemm plan: M e_b for the unit vectors e_b, in chunks, through
+// the plan's synthesis (edge) and correction (blocks[0]) chirp-z products,
+// rounded to bf16 (row b of X = column b of M), then transposed in place to
+// row-major M[m][k] (gemm_X).
 int build_half_gemm_matrix(cjt_plan* P) {
   const int64_t n1 = P->n + 1, G1 = P->G + 1;
   CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));   // tables built on this thread's stream
@@ -931,6 +933,10 @@ int build_half_gemm_matrix(cjt_plan* P) {
       return rc;
     if (int rc = launch_to_bf16(eout, n1, (char*)P->gemm_X + (size_t)(b0 * n1) * 2, n1, n1, nb, 0)) return rc;
   }
+  // row-major M[m][k] (K-major operand of the tensor-core GEMM): transpose X
+  if (int rc = dalloc(tmp, &p, (size_t)(n1 * n1) * 2)) return rc;
+  if (int rc = launch_transpose_bf16(P->gemm_X, p, n1, n1, 0)) return rc;
+  CJT_CUDA_TRY(cudaMemcpyAsync(P->gemm_X, p, (size_t)(n1 * n1) * 2, cudaMemcpyDeviceToDevice, 0));
   CJT_CUDA_TRY(cudaDeviceSynchronize());
   return CJT_OK;
 }

@@ -558,15 +558,18 @@ int launch_to_bf16(const double* in, int64_t ldi, void* out, int64_t ldo, int64_
   return CJT_OK;
 }
 
-int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* X, void* tbf,
+int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, void* tbf,
                       float* corr, const double* k, cudaStream_t st) {
   if (batch <= 0) return CJT_OK;
   if (int rc = launch_to_bf16(t, n1, tbf, n1, n1, batch, st)) return rc;
+  // tcgen05 GEMM with the fp64 finish fused into its epilogue (cjt_umma.cu)
+  if (umma_half_supported(n1, batch) && ((uintptr_t)tbf & 15) == 0 && ((uintptr_t)Mrow & 15) == 0)
+    return umma_half_inverse(t, out, n1, batch, Mrow, tbf, k, st);
   cublasHandle_t h;
   if (int rc = blas_handle(st, &h)) return rc;
   const float one = 1.0f, zero = 0.0f;
-  // column-major view: corr (n1 x B) = X^T-as-stored (n1 x n1, X[k][m] = M[m][k]) . t^T (n1 x B)
-  if (cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, (int)batch, (int)n1, &one, X, CUDA_R_16BF, (int)n1, tbf,
+  // column-major view: corr (n1 x B) = (Mrow as stored = M^T col-major)^T . t^T (n1 x B)
+  if (cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n1, (int)batch, (int)n1, &one, Mrow, CUDA_R_16BF, (int)n1, tbf,
                    CUDA_R_16BF, (int)n1, &zero, corr, CUDA_R_32F, (int)n1, CUBLAS_COMPUTE_32F,
                    CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
     return fail(CJT_ECUDA, "cublasGemmEx failed");
@@ -575,6 +578,29 @@ int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, c
     k_half_inv_finish<<<grid, 256, 0, st>>>(t, corr, k, out, n1, batch);
   else
     k_half_inv_finish1<<<grid, 256, 0, st>>>(t, corr, k, out, n1, batch);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+// [rows][cols] bf16 -> [cols][rows] (plan time: the correction matrix)
+__global__ void k_transpose_bf16(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                 int64_t rows, int64_t cols) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+int launch_transpose_bf16(const void* in, void* out, int64_t rows, int64_t cols, cudaStream_t st) {
+  const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  k_transpose_bf16<<<grid, dim3(32, 8), 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, rows, cols);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
 }

@@ -1,0 +1,354 @@
+// alpha = beta = 1/2 inverse on the 5th-generation tensor cores (sm_100a):
+//
+//   out[b][m] = u_m / k_m + sum_k M[m][k] t[b][k],   u = E t (exact T -> U)
+//
+// M is the plan's (N+1) x (N+1) first-order correction to the reference's
+// evaluation points (cjt_half.cu, cjt_capi.cu: build_half_gemm_matrix), bf16,
+// row-major [m][k]; t the Chebyshev input, fp64, and tbf its bf16 copy.  The
+// correction is ~1e-12 ||t||_1, so bf16 operands with fp32 accumulation carry
+// it to ~1e-15 ||t||_1; the exact part and the sum stay fp64.
+//
+// One persistent CTA per SM, warp-specialised:
+//   warp 0  TMA producer: 128 x 64 tiles of M (A, K-major) and 256 x 64
+//           tiles of tbf (B, K-major), 128-byte swizzled, into a kStages ring
+//           (mbarrier full / empty per stage);
+//   warp 1  allocates 512 TMEM columns (two 128 x 256 fp32 accumulators) and
+//           one elected lane issues tcgen05.mma (M = 128, N = 256, K = 16);
+//           tcgen05.commit releases smem stages and hands a finished
+//           accumulator to the epilogue;
+//   warps 2-17 epilogue, four groups of four warps (one per TMEM lane
+//           quarter): tcgen05.ld (32x32b.x8) gives each thread one output
+//           coefficient m (its TMEM lane) for 8 consecutive vectors b; the
+//           fp64 rows t[b][m0 .. m0 + 129] of those vectors arrive by a TMA
+//           tile load into the group's double buffer (one chunk ahead), the
+//           exact part E t / k is added in fp64 and written straight to HBM,
+//           coalesced across the warp, while the MMA warp already
+//           accumulates the next tile in the other TMEM buffer.
+// Measured on B200 (config 3, N = 4095, 8192 vectors): 253 us, of which the
+// MMA side alone (epilogue skipped, CJT_UMMA_DBG=1) is 195 us = 1.41 PF/s;
+// 3 operand stages because the epilogue's t buffers need 66 KB of shared
+// memory (4 stages and half the epilogue buffers: 262 us).
+// Tiles: 128 output coefficients m x 256 vectors b, K = N + 1 in steps of 64.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "cjt_internal.cuh"
+
+namespace cjt {
+namespace {
+
+constexpr int kBM = 128;            // output coefficients per tile (TMEM lanes)
+constexpr int kBN = 256;            // vectors per tile (accumulator columns)
+constexpr int kBK = 64;             // bf16 elements per 128-byte swizzled row
+constexpr int kStages = 3;
+constexpr int kABytes = kBM * kBK * 2;    // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;    // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kEpiGroupsC = 4;
+constexpr int kTW = kBM + 2;                              // t tile width: m0 .. m0 + 129
+constexpr int kTRows = 8;                                 // vectors per epilogue chunk
+constexpr int kTBytes = kTRows * kTW * 8;                 // 8.3 KB
+constexpr int kSmem = kStages * kStageBytes + kEpiGroupsC * 2 * kTBytes + 1024;   // + alignment slack
+constexpr int kEpiGroups = kEpiGroupsC;       // epilogue warp groups (4 warps: one per TMEM lane quarter)
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kTmemCols = 512;
+
+// instruction descriptor: kind::f16, A = B = bf16 (K-major), D = f32, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+// shared-memory matrix descriptor, K-major, 128-byte swizzle: 8-row core
+// groups 1024 bytes apart (SBO), version 1 (sm_100), layout type 2
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 8 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_half_inv_umma(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_t,
+                    const __grid_constant__ CUtensorMap map_x,
+                    const double* __restrict__ t, const double* __restrict__ kt, double* __restrict__ out, int n1,
+                    int batch, int dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t xbar[kEpiGroups][2];   // fp64 t tiles of the epilogue groups
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = (n1 + kBM - 1) / kBM, bt = (batch + kBN - 1) / kBN;
+  const int tiles = mt * bt;
+  const int kblocks = (n1 + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
+      for (int g = 0; g < kEpiGroups; ++g) mbar_init(&xbar[g][a], 1);
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_m)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_t)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile % mt) * kBM, b0 = (tile / mt) * kBN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * kStageBytes;
+          mbar_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(sa, &map_m, kb * kBK, m0, &full[s]);
+          tma_load_2d(sa + kABytes, &map_t, kb * kBK, b0, &full[s]);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // MMA issuer
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * kBN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * kStageBytes);
+          const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)   // 32 bytes along K per step: +2 in the 16-byte address field
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+          umma_commit(&empty[s]);              // smem stage free once these MMAs completed
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);              // accumulator complete
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31; group g = (w - 2) / 4
+    // takes the 16-vector chunks g, g + kEpiGroups, ... of every tile.  The
+    // fp64 rows t[b][m0 .. m0 + 129] of a chunk arrive by one TMA tile load
+    // into the group's double buffer (issued one chunk ahead), so the HBM
+    // reads need no registers; the results go out as coalesced stores.
+    const int q = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const bool leader = (warp == 2 + 4 * grp) && lane == 0;
+    double* xb = reinterpret_cast<double*>(smem + kStages * kStageBytes + grp * 2 * kTBytes);
+    constexpr int kChunks = kBN / (kTRows * kEpiGroups);   // per tile and group
+    const int my_tiles = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int nseq = my_tiles * kChunks;
+    auto issue_x = [&](int sq) {   // leader: t tile of chunk sq of this group's sequence
+      if (sq >= nseq) return;
+      const int tile = blockIdx.x + (sq / kChunks) * gridDim.x;
+      const int c0 = kTRows * (grp + kEpiGroups * (sq % kChunks));
+      uint64_t* br = &xbar[grp][sq & 1];
+      mbar_expect_tx(br, kTBytes);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(xb + (sq & 1) * (kTRows * kTW))),
+          "l"(reinterpret_cast<uint64_t>(&map_x)), "r"((tile % mt) * kBM), "r"((tile / mt) * kBN + c0),
+          "r"(smem_u32(br))
+          : "memory");
+    };
+    if (leader && dbg != 1) issue_x(0);
+    int it = 0, sq = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int m0 = (tile % mt) * kBM, b0 = (tile / mt) * kBN;
+      const int ml = q * 32 + lane;          // row of the t tile
+      const int m = m0 + ml;
+      const bool mv = m < n1;
+      const double inv_k = mv ? 1.0 / __ldg(kt + m) : 0.0;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      if (dbg == 1) {   // timing experiment: accumulator read only, no HBM traffic
+        float v[8];
+        tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN), v);
+        if (v[0] == 12345.f) out[0] = v[1];
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        sq += kChunks;
+        continue;
+      }
+#pragma unroll 1
+      for (int c0 = kTRows * grp; c0 < kBN; c0 += kTRows * kEpiGroups, ++sq) {
+        if (leader) issue_x(sq + 1);         // its buffer was released by the barrier below
+        float v[kTRows];
+        tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN + c0), v);
+        mbar_wait(&xbar[grp][sq & 1], (uint32_t)((sq >> 1) & 1));
+        const double* xr = xb + (sq & 1) * (kTRows * kTW);
+#pragma unroll
+        for (int j = 0; j < kTRows; ++j) {
+          const int b = b0 + c0 + j;
+          const double tm = xr[j * kTW + ml], hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
+          const double u = (m == 0 ? tm - 0.5 * hi : 0.5 * (tm - hi));
+          if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, fma(u, inv_k, (double)v[j]));
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group is done with this buffer
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// row-major [rows][cols] bf16, box = box_rows x 64, 128-byte swizzle
+int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CJT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CJT_ECUDA, "cuTensorMapEncodeTiled failed");
+  return CJT_OK;
+}
+
+// row-major [rows][cols] fp64, box = box_rows x box_cols, no swizzle
+int make_map_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CJT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CJT_ECUDA, "cuTensorMapEncodeTiled (f64) failed");
+  return CJT_OK;
+}
+
+}  // namespace
+
+bool umma_half_supported(int64_t n1, int64_t batch) {
+  return n1 % 8 == 0 && n1 <= 0x7fffffff && batch <= 0x7fffffff && !getenv("CJT_HALF_CUBLAS");
+}
+
+int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
+                      const double* k, cudaStream_t st) {
+  if (batch <= 0) return CJT_OK;
+  static DeviceOnce once;
+  if (int rc = once([] {
+        CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        return CJT_OK;
+      }))
+    return rc;
+  if (((uintptr_t)t & 15) != 0) return fail(CJT_EINVAL, "umma_half_inverse: input must be 16-byte aligned");
+  CUtensorMap mm, mt, mx;
+  if (int rc = make_map(&mm, Mrow, n1, n1, kBM)) return rc;
+  if (int rc = make_map(&mt, tbf, batch, n1, kBN)) return rc;
+  if (int rc = make_map_f64(&mx, t, batch, n1, kTRows, kTW)) return rc;
+  int dev = 0, sms = 148;
+  CJT_CUDA_TRY(cudaGetDevice(&dev));
+  CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t tiles = ((n1 + kBM - 1) / kBM) * ((batch + kBN - 1) / kBN);
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
+  k_half_inv_umma<<<grid, kThreads, kSmem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, dbg);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+}  // namespace cjt
