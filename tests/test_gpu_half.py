@@ -79,3 +79,21 @@ def test_half_exact_large_batch_and_host_api(cuda, monkeypatch):
     assert np.array_equal(one.data, f[137])
     back = cj.inverse(ip, cj.chebyshev(f[137]))
     assert np.max(np.abs(back.data - i[137])) <= 1e-15 * np.abs(f[137]).sum()
+
+
+@pytest.mark.parametrize("n,batch", [(255, 5), (1023, 300), (4095, 257), (8191, 40)])
+def test_tcgen05_inverse_matches_cublas_path(cuda, n, batch, monkeypatch):
+    """The tcgen05 correction GEMM with its fused fp64 epilogue (cjt_umma.cu)
+    against the cuBLAS GEMM + separate finish on the same plan: the two differ
+    only in the fp32 accumulation order of a ~1e-12 ||t||_1 correction."""
+    import torch
+    p = cj.JacobiParameters(0.5, 0.5)
+    ip = cj.plan("inverse", p, n)
+    assert ip.host.half_gemm
+    t = torch.from_numpy(np.stack([O.seeded_vector(3, v, n) for v in range(batch)])).to(cuda)
+    monkeypatch.delenv("CJT_HALF_CUBLAS", raising=False)
+    a = cj.inverse_batched(ip, t).cpu().numpy()
+    monkeypatch.setenv("CJT_HALF_CUBLAS", "1")
+    b = cj.inverse_batched(ip, t).cpu().numpy()
+    l1 = np.abs(t.cpu().numpy()).sum(axis=1)
+    assert np.all(np.max(np.abs(a - b), axis=1) <= 1e-16 * l1)
