@@ -26,6 +26,7 @@
 #include <mutex>
 
 #include "cjt_internal.cuh"
+#include "cjt_tma.cuh"
 
 namespace cjt {
 namespace {
@@ -207,42 +208,53 @@ __global__ void __launch_bounds__(kFThreads, 2) k_half_fwd_scan(const double* __
   }
 }
 
-// Warp-per-vector form (rows 16-byte aligned, N+1 even, N+1 <= kWarpMaxN1):
-// one warp walks its vectors from the top in 256-coefficient sub-chunks.
-// Every global access is a 1-D TMA bulk copy: the k table is staged in
-// shared memory once per CTA, each sub-chunk arrives in the warp's own
-// kWStages-deep ring (one mbarrier per stage) and its results leave from the
-// same stage by a bulk store.  Lane l owns the coefficients l + 32 e (e < 8)
-// of a sub-chunk, so its shared-memory words are consecutive across the warp
-// (conflict-free 8-byte accesses, registers in natural order) and all of a
-// lane's coefficients have the parity of l: the suffix sum of (e, l) is a
-// same-parity shuffle scan of row e over the lanes >= l, plus the parity's
-// totals of the rows above and of the sub-chunks above (a register carry).
-// No CTA barriers after the k table.  The kernel is chosen by the layout only
-// (never by the batch size), so a vector's result does not depend on how
-// many share the call.
+// Warp-per-vector form (N+1 a multiple of 16, N+1 <= kWarpMaxN1): one warp
+// walks its vectors from the top in 256-coefficient sub-chunks, lane l owning
+// the 8 consecutive coefficients 8l .. 8l + 7.  Every global access is a TMA
+// tensor copy with the 128-byte swizzle: a vector is viewed as [N+1 / 16][16]
+// (128-byte rows), a sub-chunk is a 16-row box, and the swizzle (16-byte word
+// w of row r stored at w ^ (r & 7)) makes each lane's four 16-byte reads and
+// writes bank-conflict free with compile-time register targets.  The k table
+// is staged once per CTA with the same swizzle; each sub-chunk arrives in the
+// warp's own kWStages-deep ring (one mbarrier per stage) and its results
+// leave from the same stage by a TMA tensor store (rows past N+1 are
+// zero-filled on load and clipped on store).  The suffix over the lanes is one
+// shuffle scan of the lanes' (even, odd) totals; the running carry stays in
+// registers; no CTA barriers after the k table.  The kernel is chosen by the
+// layout only (never by the batch size), so a vector's result does not depend
+// on how many vectors share the call.
 constexpr int64_t kWarpMaxN1 = 8192;
 constexpr int kWStages = 3;
 constexpr int kWWarps = 24;
-constexpr int kWSmem = kWWarps * kWStages * 256 * 8 + (int)kWarpMaxN1 * 8;   // 208 KB
+constexpr int kWSmem = kWWarps * kWStages * 2048 + (int)kWarpMaxN1 * 8 + 1024;   // + alignment slack
 
-__global__ void __launch_bounds__(kWWarps * 32, 1) k_half_fwd_warp(const double* __restrict__ c, int64_t ldc,
-                                                                   double* __restrict__ out, int64_t ldo,
-                                                                   const double* __restrict__ kt, int n1,
-                                                                   int64_t batch) {
-  extern __shared__ __align__(128) double wbuf[];   // [warp][kWStages][256], then k[n1]
+// this lane's 4 x 16-byte words of a swizzled 16 x 128-byte box
+__device__ __forceinline__ const double2* sw_word(const double* box, int lane, int q) {
+  const int r = lane >> 1, w = ((lane & 1) << 2) | q;
+  return reinterpret_cast<const double2*>(reinterpret_cast<const char*>(box) + r * 128 + ((w ^ (r & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(kWWarps * 32, 1)
+    k_half_fwd_warp(const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
+                    const __grid_constant__ CUtensorMap map_k, int n1, int64_t batch, int krows_box, int kboxes) {
+  extern __shared__ uint8_t wraw[];
+  double* wbuf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(wraw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t wbar[kWWarps][kWStages];
   __shared__ __align__(8) uint64_t kbar;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int par = lane & 1;
-  double* ks = wbuf + kWWarps * kWStages * 256;
+  double* ks = wbuf + kWWarps * kWStages * 256;     // swizzled [rows][16]
   double* mybuf = wbuf + wid * (kWStages * 256);
   uint64_t* mybar = wbar[wid];
   if (threadIdx.x == 0) {
     mbar_init(&kbar, 1);
     fence_mbar_init();
-    mbar_expect_tx(&kbar, (uint32_t)n1 * 8);
-    bulk_g2s(ks, kt, (uint32_t)n1 * 8, &kbar);
+    mbar_expect_tx(&kbar, (uint32_t)(kboxes * krows_box * 128));
+    for (int i = 0; i < kboxes; ++i)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(ks + i * krows_box * 16)),
+          "l"(reinterpret_cast<uint64_t>(&map_k)), "r"(0), "r"(i * krows_box), "r"(smem_u32(&kbar))
+          : "memory");
   }
   if (lane == 0) {
     for (int q = 0; q < kWStages; ++q) mbar_init(&mybar[q], 1);
@@ -253,67 +265,83 @@ __global__ void __launch_bounds__(kWWarps * 32, 1) k_half_fwd_warp(const double*
   const int nsub = (n1 + 255) / 256;
   const int64_t nvec = w < batch ? (batch - 1 - w) / nw + 1 : 0;
   const int64_t items = nvec * nsub;
-  // sub-chunk i of this warp's sequence: vector w + (i / nsub) nw, rows from the top
-  auto issue = [&](int64_t i) {   // lane 0
-    if (i >= items) return;
-    const int64_t r = i / nsub;
-    const int j0 = (nsub - 1 - (int)(i - r * nsub)) * 256;
-    const uint32_t bytes = (uint32_t)((n1 - j0 < 256 ? n1 - j0 : 256) * 8);
-    uint64_t* br = &mybar[i % kWStages];
-    mbar_expect_tx(br, bytes);
-    bulk_g2s(mybuf + (i % kWStages) * 256, c + (w + r * nw) * ldc + j0, bytes, br);
+  // producer state (lane 0): the next item to load, as (vector slot, sub-chunk, stage)
+  int64_t pr_r = 0;
+  int pr_sc = nsub - 1, pr_st = 0;
+  int64_t pr_i = 0;
+  auto issue_next = [&]() {   // lane 0
+    if (pr_i >= items) return;
+    uint64_t* br = &mybar[pr_st];
+    mbar_expect_tx(br, 2048);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(mybuf + pr_st * 256)),
+        "l"(reinterpret_cast<uint64_t>(&map_c)), "r"(0), "r"(pr_sc * 16), "r"((int)(w + pr_r * nw)),
+        "r"(smem_u32(br))
+        : "memory");
+    ++pr_i;
+    if (++pr_st == kWStages) pr_st = 0;
+    if (--pr_sc < 0) {
+      pr_sc = nsub - 1;
+      ++pr_r;
+    }
   };
   if (lane == 0)
-    for (int q = 0; q < kWStages - 1; ++q) issue(q);
+    for (int q = 0; q < kWStages - 1; ++q) issue_next();
   __syncthreads();                 // barrier inits visible; k table requested
   mbar_wait(&kbar, 0);
-  double carry = 0.0;              // this lane's parity: sum over the sub-chunks above
+  eo carry{0.0, 0.0};
   int64_t r = 0;
-  int sc = nsub - 1;
+  int sc = nsub - 1, st = 0;
+  uint32_t ph = 0;
   for (int64_t i = 0; i < items; ++i) {
     if (lane == 0) {
       bulk_wait_read0();           // the store of iteration i - 1 has read its stage
-      issue(i + kWStages - 1);     // ... which is the stage refilled now
+      issue_next();                // ... which is the stage refilled now
     }
-    const int j0 = sc * 256;
-    const int cnt = n1 - j0 < 256 ? n1 - j0 : 256;
-    double* sb = mybuf + (i % kWStages) * 256;
-    const double* kb = ks + j0;
-    mbar_wait(&mybar[i % kWStages], (uint32_t)((i / kWStages) & 1));
-    double x[kFE];
+    const double* sb = mybuf + st * 256;
+    const double* kb = ks + sc * 256;
+    mbar_wait(&mybar[st], ph);
+    double v[kFE], k[kFE];
 #pragma unroll
-    for (int e = 0; e < kFE; ++e) {
-      const int l = lane + 32 * e;
-      x[e] = l < cnt ? kb[l] * sb[l] : 0.0;   // past N+1: stale shared memory, masked
+    for (int q = 0; q < 4; ++q) {
+      const double2 a = *sw_word(sb, lane, q), kk = *sw_word(kb, lane, q);
+      v[2 * q] = a.x;
+      v[2 * q + 1] = a.y;
+      k[2 * q] = kk.x;
+      k[2 * q + 1] = kk.y;
     }
-    // row e: inclusive same-parity suffix over the lanes >= lane
+    eo inc = thread_totals(v, k);  // rows past N+1 were zero-filled
 #pragma unroll
-    for (int d = 2; d < 32; d <<= 1) {
-#pragma unroll
-      for (int e = 0; e < kFE; ++e) {
-        const double u = __shfl_down_sync(0xffffffffu, x[e], d);
-        if (lane + d < 32) x[e] += u;
-      }
+    for (int d = 1; d < 32; d <<= 1) {
+      const eo u = shfl_down_eo(inc, d);
+      if (lane + d < 32) inc = eo_add(inc, u);
     }
-    double acc = carry;
+    const eo total{__shfl_sync(0xffffffffu, inc.e, 0), __shfl_sync(0xffffffffu, inc.o, 0)};
+    eo x = shfl_down_eo(inc, 1);
+    if (lane == 31) x = eo{0.0, 0.0};
+    thread_results(v, k, sc * 256 + kFE * lane, eo_add(carry, x));
 #pragma unroll
-    for (int e = kFE - 1; e >= 0; --e) {
-      const double row = __shfl_sync(0xffffffffu, x[e], par);   // the row's total of this parity
-      const int l = lane + 32 * e;
-      if (l < cnt) sb[l] = (j0 + l == 0 ? 1.0 : 2.0) * (x[e] + acc);
-      acc += row;
-    }
-    carry = acc;
-    fence_proxy_async();     // this lane's generic writes -> the async proxy (bulk store)
+    for (int q = 0; q < 4; ++q)
+      *const_cast<double2*>(sw_word(sb, lane, q)) = make_double2(v[2 * q], v[2 * q + 1]);
+    fence_proxy_async();     // this lane's generic writes -> the async proxy (TMA store)
     __syncwarp();
     if (lane == 0) {
-      bulk_s2g(out + (w + r * nw) * ldo + j0, sb, (uint32_t)cnt * 8);
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                       reinterpret_cast<uint64_t>(&map_o)),
+                   "r"(0), "r"(sc * 16), "r"((int)(w + r * nw)), "r"(smem_u32(sb))
+                   : "memory");
       bulk_commit();
+    }
+    carry = eo_add(carry, total);
+    if (++st == kWStages) {
+      st = 0;
+      ph ^= 1;
     }
     if (--sc < 0) {
       sc = nsub - 1;
       ++r;
-      carry = 0.0;
+      carry = eo{0.0, 0.0};
     }
   }
   if (lane == 0) bulk_wait0();   // stores complete before the CTA's shared memory goes away
@@ -634,15 +662,36 @@ int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, 
   CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // the kernel is chosen by the layout only (never by the batch size), so a
   // vector's result does not depend on how many vectors share the call
-  if (stream && n1 <= kWarpMaxN1 && ((uintptr_t)k & 15) == 0 && ldo % 2 == 0 && ((uintptr_t)out & 15) == 0 && !getenv("CJT_HALF_NOWARP")) {
+  if (n1 % 16 == 0 && n1 <= kWarpMaxN1 && ldc % 2 == 0 && ldo % 2 == 0 && ((uintptr_t)c & 15) == 0 &&
+      ((uintptr_t)out & 15) == 0 && ((uintptr_t)k & 15) == 0 && batch <= 0x7fffffff && !getenv("CJT_HALF_NOWARP")) {
     static DeviceOnce wonce;
     if (int rc = wonce([] {
           CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_fwd_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
           return CJT_OK;
         }))
       return rc;
+    const cuuint64_t rows = (cuuint64_t)(n1 / 16);
+    CUtensorMap mc, mo, mk;
+    {
+      const cuuint64_t dims[3] = {16, rows, (cuuint64_t)batch};
+      const cuuint64_t strc[2] = {128, (cuuint64_t)ldc * 8}, stro[2] = {128, (cuuint64_t)ldo * 8};
+      const cuuint32_t box[3] = {16, 16, 1};
+      if (int rc = tmap_make(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c, dims, strc, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        return rc;
+      if (int rc = tmap_make(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, out, dims, stro, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        return rc;
+    }
+    const int krows = (int)std::min<cuuint64_t>(rows, 256);
+    const int kboxes = (int)((rows + krows - 1) / krows);
+    {
+      const cuuint64_t dims[2] = {16, rows};
+      const cuuint64_t str[1] = {128};
+      const cuuint32_t box[2] = {16, (cuuint32_t)krows};
+      if (int rc = tmap_make(&mk, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, k, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        return rc;
+    }
     const unsigned ctas = (unsigned)std::min<int64_t>((batch + kWWarps - 1) / kWWarps, (int64_t)sms);
-    k_half_fwd_warp<<<ctas, kWWarps * 32, kWSmem, st>>>(c, ldc, out, ldo, k, (int)n1, batch);
+    k_half_fwd_warp<<<ctas, kWWarps * 32, kWSmem, st>>>(mc, mo, mk, (int)n1, batch, krows, kboxes);
     CJT_CUDA_TRY(cudaGetLastError());
     return CJT_OK;
   }
