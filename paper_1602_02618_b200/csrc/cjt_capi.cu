@@ -203,29 +203,77 @@ int upload(std::vector<void*>& list, T** dst, const T* src, size_t count) {
   void* p = nullptr;
   if (int rc = dalloc(list, &p, count * sizeof(T))) return rc;
   *dst = static_cast<T*>(p);
-  if (count) CJT_CUDA_TRY(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  // this thread's stream, not the legacy default stream: a legacy-stream copy
+  // would wait for the plan kernels other host threads have in flight
+  if (count) {
+    CJT_CUDA_TRY(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, cudaStreamPerThread));
+    CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
+  }
   return CJT_OK;
 }
+
+// Many host -> device uploads into ONE allocation, synchronised once (plan
+// builds: a cudaMalloc and a synchronised copy per table were most of
+// configuration 5's plan-build time).  Sources must stay valid until flush();
+// add_owned() keeps a temporary alive inside the batch.
+struct UploadBatch {
+  struct Item {
+    void** dst;
+    const void* src;
+    size_t bytes, off;
+  };
+  std::vector<Item> items;
+  std::vector<std::vector<double>> owned;
+  size_t total = 0;
+  template <typename T>
+  void add(T** dst, const T* src, size_t count) {
+    const size_t bytes = count * sizeof(T);
+    items.push_back({reinterpret_cast<void**>(dst), src, bytes, total});
+    total += (bytes + 255) & ~size_t(255);
+  }
+  void add_owned(const double** dst, std::vector<double>&& v) {
+    owned.push_back(std::move(v));
+    add(const_cast<double**>(dst), owned.back().data(), owned.back().size());
+  }
+  int flush(std::vector<void*>& list) {
+    if (items.empty()) return CJT_OK;
+    void* base = nullptr;
+    if (int rc = dalloc(list, &base, std::max<size_t>(total, 256))) return rc;
+    for (const Item& it : items) {
+      *it.dst = static_cast<char*>(base) + it.off;
+      if (it.bytes)
+        CJT_CUDA_TRY(cudaMemcpyAsync(*it.dst, it.src, it.bytes, cudaMemcpyHostToDevice, cudaStreamPerThread));
+    }
+    CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
+    items.clear();
+    owned.clear();
+    total = 0;
+    return CJT_OK;
+  }
+};
 
 // Device recurrence tables: the reference's seven (A, B, C, rf+-, 1/rf+-) and
 // the FMA-form Reinsch tables A/rf+-, C/rf+- (products with the tabulated
 // reciprocals) used by the generation kernels.
-int upload_tables(std::vector<void*>& A, const double* const src[7], size_t tl, RecTablesDev* tab) {
-  double* t[7];
-  for (int k = 0; k < 7; ++k)
-    if (int rc = upload(A, &t[k], src[k], tl)) return rc;
-  *tab = RecTablesDev{t[0], t[1], t[2], t[3], t[4], t[5], t[6], (int64_t)tl};
-  std::vector<double> prod(tl);
+void batch_tables(UploadBatch& ub, const double* const src[7], size_t tl, RecTablesDev* tab) {
+  *tab = RecTablesDev{};
+  tab->n_tab = (int64_t)tl;
+  const double** t[7] = {&tab->A, &tab->B, &tab->C, &tab->rfp, &tab->rfm, &tab->rfpi, &tab->rfmi};
+  for (int k = 0; k < 7; ++k) ub.add(const_cast<double**>(t[k]), src[k], tl);
   const double* num[4] = {src[0], src[0], src[2], src[2]};
   const double* den[4] = {src[5], src[6], src[5], src[6]};
   const double** dst[4] = {&tab->Ap, &tab->Am, &tab->Cp, &tab->Cm};
   for (int k = 0; k < 4; ++k) {
+    std::vector<double> prod(tl);
     for (size_t i = 0; i < tl; ++i) prod[i] = num[k][i] * den[k][i];
-    double* d = nullptr;
-    if (int rc = upload(A, &d, prod.data(), tl)) return rc;
-    *dst[k] = d;
+    ub.add_owned(dst[k], std::move(prod));
   }
-  return CJT_OK;
+}
+
+int upload_tables(std::vector<void*>& A, const double* const src[7], size_t tl, RecTablesDev* tab) {
+  UploadBatch ub;
+  batch_tables(ub, src, tl, tab);
+  return ub.flush(A);
 }
 
 // exp(-2 pi i num / den), long-double accurate
@@ -455,7 +503,10 @@ int upload_ws(cjt_plan* P, T** dst, const std::vector<T>& v) {
   void* p;
   if (int rc = dalloc(P->ws_allocs, &p, std::max<size_t>(1, v.size()) * sizeof(T))) return rc;
   *dst = (T*)p;
-  if (!v.empty()) CJT_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  if (!v.empty()) {
+    CJT_CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, cudaStreamPerThread));
+    CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
+  }
   return CJT_OK;
 }
 
@@ -926,18 +977,18 @@ int build_half_gemm_matrix(cjt_plan* P) {
   int launches = 0;
   for (int64_t b0 = 0; b0 < n1; b0 += chunk) {
     const int64_t nb = std::min(chunk, n1 - b0);
-    if (int rc = launch_identity(ein, n1, b0, nb, 0)) return rc;
-    if (int rc = launch_chirpz(P->edge, P->tw8192, ein, n1, vals, G1, nb, scratch, part, spec, 0, &launches))
+    if (int rc = launch_identity(ein, n1, b0, nb, cudaStreamPerThread)) return rc;
+    if (int rc = launch_chirpz(P->edge, P->tw8192, ein, n1, vals, G1, nb, scratch, part, spec, cudaStreamPerThread, &launches))
       return rc;
-    if (int rc = launch_chirpz(P->blocks[0], P->tw8192, vals, G1, eout, n1, nb, scratch, part, spec, 0, &launches))
+    if (int rc = launch_chirpz(P->blocks[0], P->tw8192, vals, G1, eout, n1, nb, scratch, part, spec, cudaStreamPerThread, &launches))
       return rc;
-    if (int rc = launch_to_bf16(eout, n1, (char*)P->gemm_X + (size_t)(b0 * n1) * 2, n1, n1, nb, 0)) return rc;
+    if (int rc = launch_to_bf16(eout, n1, (char*)P->gemm_X + (size_t)(b0 * n1) * 2, n1, n1, nb, cudaStreamPerThread)) return rc;
   }
   // row-major M[m][k] (K-major operand of the tensor-core GEMM): transpose X
   if (int rc = dalloc(tmp, &p, (size_t)(n1 * n1) * 2)) return rc;
-  if (int rc = launch_transpose_bf16(P->gemm_X, p, n1, n1, 0)) return rc;
-  CJT_CUDA_TRY(cudaMemcpyAsync(P->gemm_X, p, (size_t)(n1 * n1) * 2, cudaMemcpyDeviceToDevice, 0));
-  CJT_CUDA_TRY(cudaDeviceSynchronize());
+  if (int rc = launch_transpose_bf16(P->gemm_X, p, n1, n1, cudaStreamPerThread)) return rc;
+  CJT_CUDA_TRY(cudaMemcpyAsync(P->gemm_X, p, (size_t)(n1 * n1) * 2, cudaMemcpyDeviceToDevice, cudaStreamPerThread));
+  CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));   // before the temporaries are freed
   return CJT_OK;
 }
 
@@ -1021,14 +1072,14 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
   double *x, *xm;
   int8_t* reg;
   int64_t* cut;
-  if (int rc = upload(A, &x, d->x, nr)) return rc;
-  if (int rc = upload(A, &xm, d->xm, nr)) return rc;
-  if (int rc = upload(A, &reg, d->regions, nr)) return rc;
-  if (int rc = upload(A, &cut, d->cuts, nr)) return rc;
-  P->rows = RecRowsDev{x, xm, reg, cut, nr};
+  UploadBatch ub;   // rows, tables and checkpoint offsets: one allocation, one copy
+  ub.add(&x, d->x, nr);
+  ub.add(&xm, d->xm, nr);
+  ub.add(&reg, d->regions, nr);
+  ub.add(&cut, d->cuts, nr);
   const size_t tl = (size_t)d->table_len;
   const double* src[7] = {d->A, d->B, d->C, d->rf_plus, d->rf_minus, d->rf_plus_inv, d->rf_minus_inv};
-  if (int rc = upload_tables(A, src, tl, &P->tab)) return rc;
+  batch_tables(ub, src, tl, &P->tab);
 
   // parity folding (alpha = beta): B_n = 0, rf- = -rf+, symmetric cuts,
   // antisymmetric regions.  The forward is insensitive to the mirrored rows'
@@ -1064,7 +1115,9 @@ int cjt_plan_create(const cjt_plan_desc* d, cjt_plan** out) {
     tot += (c >= 1) ? (c - 1) / CK : 0;
   }
   P->ck_count = tot;
-  if (int rc = upload(A, &P->ck_off, off.data(), off.size())) return rc;
+  ub.add(&P->ck_off, off.data(), off.size());
+  if (int rc = ub.flush(A)) return rc;
+  P->rows = RecRowsDev{x, xm, reg, cut, nr};
   void* p;
   if (int rc = dalloc(A, &p, (size_t)std::max<int64_t>(tot, 1) * sizeof(double2))) return rc;
   P->ck = (double2*)p;

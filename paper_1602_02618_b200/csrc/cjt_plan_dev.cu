@@ -246,7 +246,9 @@ int permute_spectra(const double2* natural_host, int64_t L, int ntile, int mode,
   void *sp = nullptr, *dp = nullptr;
   if (int rc = dalloc_list(allocs, &dp, (size_t)ntile * L * sizeof(double2))) return rc;
   if (mode == 0) {
-    CJT_CUDA_TRY(cudaMemcpy(dp, natural_host, (size_t)ntile * L * sizeof(double2), cudaMemcpyHostToDevice));
+    CJT_CUDA_TRY(cudaMemcpyAsync(dp, natural_host, (size_t)ntile * L * sizeof(double2), cudaMemcpyHostToDevice,
+                                 cudaStreamPerThread));
+    CJT_CUDA_TRY(cudaStreamSynchronize(cudaStreamPerThread));
     *out = (const double2*)dp;
     return CJT_OK;
   }

@@ -38,7 +38,9 @@ for every configuration.
 
 from __future__ import annotations
 
+import dataclasses
 import math
+import threading
 from dataclasses import dataclass, field
 
 import functools
@@ -177,7 +179,7 @@ def cnm_scalar(p: JacobiParameters, n: int, m: int) -> float:
     return val
 
 
-def cnm_table(p: JacobiParameters, nmax: int, m_count: int) -> np.ndarray:
+def _cnm_table(p: JacobiParameters, nmax: int, m_count: int) -> np.ndarray:
     """C_{n,m}, n = 0..nmax, m < m_count, shape (nmax+1, m_count)
     (kernels.py:231-252)."""
     a, b = p.alpha, p.beta
@@ -218,7 +220,7 @@ def _an_stirling(a, b, n):
     return front * g1 * g2 * rat
 
 
-def orthonormality(p: JacobiParameters, nmax: int) -> np.ndarray:
+def _orthonormality(p: JacobiParameters, nmax: int) -> np.ndarray:
     """A_n = ||P_n||^2 for n = 0..nmax (kernels.py:298-307)."""
     a, b = p.alpha, p.beta
     lo = min(a, b, a + b, 0.0)
@@ -250,7 +252,7 @@ class RecurrenceTables:
     rb_minus_inv: np.ndarray
 
 
-def recurrence_tables(p: JacobiParameters, nmax: int) -> RecurrenceTables:
+def _recurrence_tables(p: JacobiParameters, nmax: int) -> RecurrenceTables:
     a, b = p.alpha, p.beta
     s = a + b
     deg = np.arange(nmax + 1, dtype=float)
@@ -276,6 +278,72 @@ def recurrence_tables(p: JacobiParameters, nmax: int) -> RecurrenceTables:
     for arr in arrays:
         arr.flags.writeable = False
     return RecurrenceTables(*arrays)
+
+
+# ---------------------------------------------------------------------------
+# Per-(alpha, beta) prefix caches.  Every entry of these tables is a function
+# of its degree alone (elementwise formulas; the downward recursions stop at
+# the Stirling switch degree, below any length the planner asks for), so a
+# shorter table is bit-for-bit the prefix of a longer one (checked for the
+# configuration-5 parameter set in tests/test_planner.py).  Ragged batches
+# (configuration 5: 25 parameter pairs x 9 degrees x 2 directions) then build
+# each table once per pair.
+
+_PREFIX_CACHE: dict = {}
+_PREFIX_LOCK = threading.Lock()
+_PREFIX_MIN = 64            # below this the tables are cheap: no caching
+
+
+def _prefix(kind: str, p: JacobiParameters, n: int, extra, build):
+    if n + 1 < _PREFIX_MIN:
+        return n, build(n)
+    key = (kind, p.alpha, p.beta, extra)
+    with _PREFIX_LOCK:
+        hit = _PREFIX_CACHE.get(key)
+    if hit is None or hit[0] < n:
+        val = build(n)
+        if isinstance(val, np.ndarray):
+            val.flags.writeable = False
+        hit = (n, val)
+        with _PREFIX_LOCK:
+            cur = _PREFIX_CACHE.get(key)
+            if cur is None or cur[0] < n:
+                _PREFIX_CACHE[key] = hit
+    return hit
+
+
+def cnm_table(p: JacobiParameters, nmax: int, m_count: int) -> np.ndarray:
+    """C_{n,m}, n = 0..nmax, m < m_count, shape (nmax+1, m_count)
+    (kernels.py:231-252); prefix-cached per (alpha, beta, M)."""
+    if nmax < _cnm_switch(p.alpha, p.beta):
+        return _cnm_table(p, nmax, m_count)
+    top, tab = _prefix("cnm", p, nmax, m_count, lambda n: _cnm_table(p, n, m_count))
+    return tab if top == nmax else tab[: nmax + 1]
+
+
+def orthonormality(p: JacobiParameters, nmax: int) -> np.ndarray:
+    """A_n = ||P_n||^2 for n = 0..nmax (kernels.py:298-307); prefix-cached."""
+    top, tab = _prefix("an", p, nmax, None, lambda n: _orthonormality(p, n))
+    return tab if top == nmax else tab[: nmax + 1]
+
+
+def recurrence_tables(p: JacobiParameters, nmax: int) -> RecurrenceTables:
+    """Three-term and Reinsch tables for degrees 0..nmax (kernels.py:336-364);
+    prefix-cached per (alpha, beta)."""
+    top, t = _prefix("rec", p, nmax, None, lambda n: _recurrence_tables(p, n))
+    if top == nmax:
+        return t
+    return RecurrenceTables(*(getattr(t, f.name)[: nmax + 1] for f in dataclasses.fields(t)))
+
+
+def prewarm(p: JacobiParameters, n_max: int, m_terms: int = 7) -> None:
+    """Build the prefix-cached tables of `p` once at the largest size plans of
+    degree <= n_max ask for (forward and inverse), so those plans slice them
+    (ragged batches: one build per parameter pair instead of one per plan)."""
+    g = 2 * n_max
+    recurrence_tables(p, g + 1)
+    orthonormality(p, n_max)
+    cnm_table(p, min(g, max(n_max, _cnm_switch(p.alpha, p.beta))), m_terms)
 
 
 # ---------------------------------------------------------------------------

@@ -19,6 +19,7 @@ import numpy as np
 
 from . import engine
 from . import sharding
+from . import planner
 from .planner import DEFAULT_EPS, DEFAULT_M, JacobiParameters
 
 
@@ -51,7 +52,13 @@ class RaggedPlan:
                     tp.device_plan(device)
             return pair
 
+        # per-(alpha, beta) tables at the largest degree first: every plan of
+        # the pair then slices them (planner.prewarm)
+        top = {}
+        for a, b, n in keys:
+            top[(a, b)] = max(top.get((a, b), 0), n)
         with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(lambda kv: planner.prewarm(JacobiParameters(*kv[0]), kv[1], m_terms), top.items()))
             self.plans = list(ex.map(build, keys))
         # packed layout: group g occupies [offsets[g], offsets[g] + B_g (N_g + 1))
         lens = [b * (n + 1) for (a, bb, n), b in zip(keys, self.sizes)]

@@ -272,3 +272,16 @@ def test_device_decomposition_matches_reference(name, monkeypatch):
     out += (pm * (np.arange(n + 1)[:, None] < hi.rec_cuts[None, :])) @ wv
     got_i = out * hi.scalings
     assert O.parity(got_i, ref_i, ref_f) <= 1e-13
+
+
+def test_prefix_cached_tables_equal_direct():
+    """The per-(alpha, beta) prefix caches return exactly the directly built
+    tables (every entry depends on its degree alone), in any request order."""
+    for a, b in ((-0.45, 0.25), (0.5, -0.2), (0.0, 0.0)):
+        p = P.JacobiParameters(a, b)
+        for n in (70, 4095, 300, 65535, 1000):
+            assert np.array_equal(P.cnm_table(p, n, 7), P._cnm_table(p, n, 7))
+            assert np.array_equal(P.orthonormality(p, n), P._orthonormality(p, n))
+            r, d = P.recurrence_tables(p, n), P._recurrence_tables(p, n)
+            for f in ("A", "B", "C", "rf_plus", "rf_minus", "rb_plus", "rb_minus", "rf_plus_inv", "rf_minus_inv"):
+                assert np.array_equal(getattr(r, f), getattr(d, f), equal_nan=True)
