@@ -354,16 +354,19 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
              device: int | None = None, sync: bool = True):
     """Apply `plans` in sequence (e.g. ``(forward_plan, inverse_plan)``) to a
     (B, N+1) float64 host array, with host<->device copies overlapped with the
-    transforms: the batch is cut into chunks that alternate between `streams`
-    CUDA streams (H2D of chunk k+1 and D2H of chunk k-1 run under chunk k's
-    kernels).  Pinned host memory (e.g. ``torch.empty(..., pin_memory=True)``)
-    is required for the copies to be asynchronous.  Returns host_out.
+    transforms: the batch is cut into chunks that flow through three CUDA
+    streams -- host->device copies, transforms, device->host copies -- linked
+    by events over a ring of `streams` device buffer slots, so the two copy
+    directions and the compute proceed independently (chunk k+1 arrives and
+    chunk k-1 leaves while chunk k is transformed).  Pinned host memory (e.g.
+    ``torch.empty(..., pin_memory=True)``) is required for the copies to be
+    asynchronous.  Returns host_out.
 
     ``sync=False`` returns as soon as the work is enqueued (host_out is valid
-    after ``torch.cuda.synchronize()``); consecutive calls then continue the
-    stream rotation, so one call's copies overlap the neighbouring calls'
-    transforms (streaming many batches through the GPU).  The caller must
-    not modify host_in / read host_out of a call before synchronizing."""
+    after ``torch.cuda.synchronize()``); consecutive calls continue the slot
+    rotation, so one call's copies overlap the neighbouring calls' transforms
+    (streaming many batches through the GPU).  The caller must not modify
+    host_in / read host_out of a call before synchronizing."""
     import torch
     if not plans:
         raise ValueError("no plans")
@@ -382,36 +385,46 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
     batch = hin.shape[0]
     chunk = batch if chunk is None else max(1, min(int(chunk), batch))
     dev = torch.device("cuda", _current_device() if device is None else device)
-    nstreams = max(1, min(streams, -(-batch // chunk))) if sync else max(1, streams)
-    # streams and device buffers are cached: plan workspaces are per stream, so
-    # fresh streams would re-allocate them on every call
-    key = (dev.index, nstreams, chunk, n1)
+    nslots = max(1, int(streams))
+    # streams, events and device buffers are cached: plan workspaces are per
+    # (compute) stream, so fresh streams would re-allocate them on every call
+    key = (dev.index, nslots, chunk, n1)
     cached = _PIPE_CACHE.get(key)
     if cached is None:
-        ss = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+        h2d, comp, d2h = (torch.cuda.Stream(dev) for _ in range(3))
         bufs = [(torch.empty((chunk, n1), dtype=torch.float64, device=dev),
-                 torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nstreams)]
-        cached = _PIPE_CACHE[key] = (ss, bufs)
-    ss, bufs = cached
+                 torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nslots)]
+        ev_in = [torch.cuda.Event() for _ in range(nslots)]     # slot filled
+        ev_done = [torch.cuda.Event() for _ in range(nslots)]   # slot transformed
+        ev_free = [torch.cuda.Event() for _ in range(nslots)]   # slot's result copied out
+        cached = _PIPE_CACHE[key] = (h2d, comp, d2h, bufs, ev_in, ev_done, ev_free)
+    h2d, comp, d2h, bufs, ev_in, ev_done, ev_free = cached
     cur = torch.cuda.current_stream(dev)
-    for s in ss:
+    for s in (h2d, comp, d2h):
         s.wait_stream(cur)
     k0 = _PIPE_NEXT.get(key, 0) if not sync else 0
     for k, r0 in enumerate(range(0, batch, chunk), start=k0):
         r1 = min(batch, r0 + chunk)
-        s = ss[k % nstreams]
-        a, b = bufs[k % nstreams]
-        with torch.cuda.stream(s):
+        slot = k % nslots
+        a, b = bufs[slot]
+        h2d.wait_event(ev_free[slot])          # the slot's previous chunk has left (no-op if unused)
+        with torch.cuda.stream(h2d):
             a[: r1 - r0].copy_(hin[r0:r1], non_blocking=True)
-            src, dst = a[: r1 - r0], b[: r1 - r0]
+            ev_in[slot].record(h2d)
+        comp.wait_event(ev_in[slot])
+        src, dst = a[: r1 - r0], b[: r1 - r0]
+        with torch.cuda.stream(comp):
             for tp in plans:
                 _execute_batched(tp, src, out=dst, check_finite=False)
                 src, dst = dst, src
+            ev_done[slot].record(comp)
+        d2h.wait_event(ev_done[slot])
+        with torch.cuda.stream(d2h):
             hout[r0:r1].copy_(src, non_blocking=True)
+            ev_free[slot].record(d2h)
     if not sync:
-        _PIPE_NEXT[key] = (k0 + -(-batch // chunk)) % nstreams
+        _PIPE_NEXT[key] = (k0 + -(-batch // chunk)) % nslots
         return host_out
-    for s in ss:
-        cur.wait_stream(s)
+    cur.wait_stream(d2h)
     torch.cuda.synchronize(dev)
     return host_out

@@ -18,7 +18,7 @@ for name, fn in (("h2d", lambda: d.copy_(pin_in, non_blocking=True)), ("d2h", la
     fn(); torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(5): fn()
     torch.cuda.synchronize(); print(json.dumps({name: pin_in.nbytes * 5 / (time.perf_counter() - t0) / 1e9}))
-for chunk, streams in ((2048, 2), (1024, 2), (1024, 3), (512, 3), (512, 4), (2048, 3), (256, 4)):
+for chunk, streams in ((2048, 2), (2048, 3), (1024, 2), (1024, 3), (1024, 4), (512, 4), (4096, 2), (8192, 1)):
     for w in range(2):
         cj.pipeline((fp, ip), pin_in, outs[w], chunk=chunk, streams=streams, sync=False)
     torch.cuda.synchronize()
