@@ -8,27 +8,32 @@
 // correction is ~1e-12 ||t||_1, so bf16 operands with fp32 accumulation carry
 // it to ~1e-15 ||t||_1; the exact part and the sum stay fp64.
 //
-// One persistent CTA per SM, warp-specialised:
-//   warp 0  TMA producer: 128 x 64 tiles of M (A, K-major) and 256 x 64
-//           tiles of tbf (B, K-major), 128-byte swizzled, into a kStages ring
-//           (mbarrier full / empty per stage);
-//   warp 1  allocates 512 TMEM columns (two 128 x 256 fp32 accumulators) and
-//           one elected lane issues tcgen05.mma (M = 128, N = 256, K = 16);
-//           tcgen05.commit releases smem stages and hands a finished
-//           accumulator to the epilogue;
+// CTA pairs (clusters of 2, tcgen05 cta_group::2), one persistent CTA per
+// SM, warp-specialised:
+//   warp 0  TMA producer (both CTAs): this CTA's 128 x 64 tile of M (A,
+//           K-major) and its half (128 x 64) of the pair's 256-vector bf16
+//           tile (B), 128-byte swizzled, into a kStages ring; the bytes of
+//           both CTAs complete the LEADER's full barrier;
+//   warp 1  allocates 512 TMEM columns per CTA (two 128 x 256 fp32
+//           accumulators); the leader's elected lane issues
+//           tcgen05.mma.cta_group::2 (M = 256 over the pair's two A tiles,
+//           N = 256 over both B halves, K = 16); tcgen05.commit multicasts
+//           the stage release and the finished accumulator to both CTAs;
 //   warps 2-17 epilogue, four groups of four warps (one per TMEM lane
 //           quarter): tcgen05.ld (32x32b.x8) gives each thread one output
 //           coefficient m (its TMEM lane) for 8 consecutive vectors b; the
 //           fp64 rows t[b][m0 .. m0 + 129] of those vectors arrive by a TMA
 //           tile load into the group's double buffer (one chunk ahead), the
-//           exact part E t / k is added in fp64 and written straight to HBM,
-//           coalesced across the warp, while the MMA warp already
-//           accumulates the next tile in the other TMEM buffer.
-// Measured on B200 (config 3, N = 4095, 8192 vectors): 253 us, of which the
-// MMA side alone (epilogue skipped, CJT_UMMA_DBG=1) is 195 us = 1.41 PF/s;
-// 3 operand stages because the epilogue's t buffers need 66 KB of shared
-// memory (4 stages and half the epilogue buffers: 262 us).
-// Tiles: 128 output coefficients m x 256 vectors b, K = N + 1 in steps of 64.
+//           exact part (two fp64 FMAs) is added and the result written
+//           straight to HBM, coalesced across the warp, while the MMAs
+//           already accumulate the next tile in the other TMEM buffer; the
+//           threads of both CTAs release an accumulator on the leader's
+//           barrier.
+// Measured on B200 (config 3, N = 4095, 8192 vectors): 239 us; the MMA side
+// alone (epilogue skipped, CJT_UMMA_DBG=1) 170 us = 1.62 PF/s (bf16 burst
+// peak 1.65); one CTA per SM with cta_group::1 and 3 stages: 251 us (MMA
+// side 195 us).
+// Pair tiles: 256 output coefficients m x 256 vectors b, K = N + 1 in steps of 64.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,9 +49,9 @@ namespace {
 constexpr int kBM = 128;            // output coefficients per tile (TMEM lanes)
 constexpr int kBN = 256;            // vectors per tile (accumulator columns)
 constexpr int kBK = 64;             // bf16 elements per 128-byte swizzled row
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;    // 16 KB
-constexpr int kBBytes = kBN * kBK * 2;    // 32 KB
+constexpr int kBBytes = (kBN / 2) * kBK * 2;   // 16 KB: this CTA's half of the pair's B tile
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kEpiGroupsC = 4;
 constexpr int kTW = kBM + 2;                              // t tile width: m0 .. m0 + 129
@@ -58,9 +63,11 @@ constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 
-// instruction descriptor: kind::f16, A = B = bf16 (K-major), D = f32, M = 128, N = 256
+// instruction descriptor: kind::f16, A = B = bf16 (K-major), D = f32,
+// M = 256 (the CTA pair's two 128-row A tiles), N = 256
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
-                            ((uint32_t)(kBM >> 4) << 24);
+                            ((uint32_t)((2 * kBM) >> 4) << 24);
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address bit 24 = CTA rank in the pair
 
 // shared-memory matrix descriptor, K-major, 128-byte swizzle: 8-row core
 // groups 1024 bytes apart (SBO), version 1 (sm_100), layout type 2
@@ -74,30 +81,42 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+// both CTAs of the pair load into their own shared memory; the bytes are
+// counted on the LEADER's (rank 0) barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerMask)
       : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// arrive on this barrier in both CTAs of the pair once the leader's MMAs completed
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
 
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void umma_bf16_pair(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
       : "memory");
+}
+
+// arrive on the leader CTA's copy of this barrier
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -114,7 +133,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_half_inv_umma(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_t,
                     const __grid_constant__ CUtensorMap map_x,
                     const double* __restrict__ t, const double* __restrict__ kt, double* __restrict__ out, int n1,
@@ -125,8 +144,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t xbar[kEpiGroups][2];   // fp64 t tiles of the epilogue groups
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = (n1 + kBM - 1) / kBM, bt = (batch + kBN - 1) / kBN;
-  const int tiles = mt * bt;
+  // CTA pairs (clusters of 2): pair tile = 256 coefficients m x 256 vectors
+  // b; CTA rank r owns m rows [m0 + 128 r, + 128) (its A tile, its TMEM
+  // accumulator, its epilogue) and loads B rows [b0 + 128 r, + 128); the
+  // leader (rank 0) issues the cta_group::2 MMAs over both CTAs' tiles
+  const int rank = blockIdx.x & 1, cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int mpt = (n1 + 2 * kBM - 1) / (2 * kBM), bt = (batch + kBN - 1) / kBN;
+  const int tiles = mpt * bt;
   const int kblocks = (n1 + kBK - 1) / kBK;
 
   if (threadIdx.x == 0) {
@@ -136,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * kEpiWarps);
+      mbar_init(&tempty[a], 2 * 32 * kEpiWarps);   // (the leader's) both CTAs' epilogue threads
       for (int g = 0; g < kEpiGroups; ++g) mbar_init(&xbar[g][a], 1);
     }
     fence_mbar_init();
@@ -145,13 +169,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                  "r"(kTmemCols)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();                            // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
 
@@ -160,14 +184,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // TMA producer
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile % mt) * kBM, b0 = (tile / mt) * kBN;
+      for (int tile = cid; tile < tiles; tile += ncl) {
+        const int m0 = (tile % mpt) * 2 * kBM + rank * kBM, b0 = (tile / mpt) * kBN + rank * (kBN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait(&empty[s], ph ^ 1);      // the pair's MMAs are done with this stage
           uint8_t* sa = smem + s * kStageBytes;
-          mbar_expect_tx(&full[s], kStageBytes);
-          tma_load_2d(sa, &map_m, kb * kBK, m0, &full[s]);
-          tma_load_2d(sa + kABytes, &map_t, kb * kBK, b0, &full[s]);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * kStageBytes);   // both CTAs' bytes
+          tma_load_2d_pair(sa, &map_m, kb * kBK, m0, &full[s]);
+          tma_load_2d_pair(sa + kABytes, &map_t, kb * kBK, b0, &full[s]);
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
@@ -176,12 +200,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // MMA issuer
+    if (lane == 0 && rank == 0) {
+      // MMA issuer (the pair's leader)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      for (int tile = cid; tile < tiles; tile += ncl, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -193,14 +217,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + kABytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)   // 32 bytes along K per step: +2 in the 16-byte address field
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
-          umma_commit(&empty[s]);              // smem stage free once these MMAs completed
+            umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+          umma_commit_pair(&empty[s]);         // the stage is free in both CTAs once these MMAs completed
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);              // accumulator complete
+        umma_commit_pair(&tfull[acc]);         // both CTAs' accumulators complete
       }
     }
   } else {
@@ -214,30 +238,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = (warp == 2 + 4 * grp) && lane == 0;
     double* xb = reinterpret_cast<double*>(smem + kStages * kStageBytes + grp * 2 * kTBytes);
     constexpr int kChunks = kBN / (kTRows * kEpiGroups);   // per tile and group
-    const int my_tiles = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
     const int nseq = my_tiles * kChunks;
     auto issue_x = [&](int sq) {   // leader: t tile of chunk sq of this group's sequence
       if (sq >= nseq) return;
-      const int tile = blockIdx.x + (sq / kChunks) * gridDim.x;
+      const int tile = cid + (sq / kChunks) * ncl;
       const int c0 = kTRows * (grp + kEpiGroups * (sq % kChunks));
       uint64_t* br = &xbar[grp][sq & 1];
       mbar_expect_tx(br, kTBytes);
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
               smem_u32(xb + (sq & 1) * (kTRows * kTW))),
-          "l"(reinterpret_cast<uint64_t>(&map_x)), "r"((tile % mt) * kBM), "r"((tile / mt) * kBN + c0),
+          "l"(reinterpret_cast<uint64_t>(&map_x)), "r"((tile % mpt) * 2 * kBM + rank * kBM),
+          "r"((tile / mpt) * kBN + c0),
           "r"(smem_u32(br))
           : "memory");
     };
     if (leader && dbg != 1) issue_x(0);
     int it = 0, sq = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       const int acc = it & 1;
-      const int m0 = (tile % mt) * kBM, b0 = (tile / mt) * kBN;
+      const int m0 = (tile % mpt) * 2 * kBM + rank * kBM, b0 = (tile / mpt) * kBN;
       const int ml = q * 32 + lane;          // row of the t tile
       const int m = m0 + ml;
       const bool mv = m < n1;
+      // out = c_t t_m - c_h t_{m+2} + corr: T_0 = U_0, T_j = (U_j - U_{j-2}) / 2
       const double inv_k = mv ? 1.0 / __ldg(kt + m) : 0.0;
+      const double c_h = 0.5 * inv_k, c_t = m == 0 ? inv_k : c_h;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       if (dbg == 1) {   // timing experiment: accumulator read only, no HBM traffic
@@ -245,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN), v);
         if (v[0] == 12345.f) out[0] = v[1];
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_leader(&tempty[acc]);
         sq += kChunks;
         continue;
       }
@@ -260,19 +287,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < kTRows; ++j) {
           const int b = b0 + c0 + j;
           const double tm = xr[j * kTW + ml], hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
-          const double u = (m == 0 ? tm - 0.5 * hi : 0.5 * (tm - hi));
-          if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, fma(u, inv_k, (double)v[j]));
+          if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, fma(c_t, tm, fma(-c_h, hi, (double)v[j])));
         }
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group is done with this buffer
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      mbar_arrive_leader(&tempty[acc]);   // the leader may reuse this accumulator (both CTAs)
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync();                            // no remote arrive or MMA still targets this CTA
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
                  : "memory");
   }
 }
@@ -338,13 +365,13 @@ int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, c
   if (((uintptr_t)t & 15) != 0) return fail(CJT_EINVAL, "umma_half_inverse: input must be 16-byte aligned");
   CUtensorMap mm, mt, mx;
   if (int rc = make_map(&mm, Mrow, n1, n1, kBM)) return rc;
-  if (int rc = make_map(&mt, tbf, batch, n1, kBN)) return rc;
+  if (int rc = make_map(&mt, tbf, batch, n1, kBN / 2)) return rc;
   if (int rc = make_map_f64(&mx, t, batch, n1, kTRows, kTW)) return rc;
   int dev = 0, sms = 148;
   CJT_CUDA_TRY(cudaGetDevice(&dev));
   CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t tiles = ((n1 + kBM - 1) / kBM) * ((batch + kBN - 1) / kBN);
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  const int64_t tiles = ((n1 + 2 * kBM - 1) / (2 * kBM)) * ((batch + kBN - 1) / kBN);
+  const unsigned grid = 2 * (unsigned)std::min<int64_t>(tiles, sms / 2);   // CTA pairs
   static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
   k_half_inv_umma<<<grid, kThreads, kSmem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, dbg);
   CJT_CUDA_TRY(cudaGetLastError());
