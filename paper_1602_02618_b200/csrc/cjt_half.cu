@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kFThreads, 2) k_half_fwd_scan(const double* __
 // on how many vectors share the call.
 constexpr int64_t kWarpMaxN1 = 8192;
 constexpr int kWStages = 3;
-constexpr int kWWarps = 24;
+constexpr int kWWarps = 24;   // most warps per CTA (one CTA per SM); small batches use fewer
 constexpr int kWSmem = kWWarps * kWStages * 2048 + (int)kWarpMaxN1 * 8 + 1024;   // + alignment slack
 
 // this lane's 4 x 16-byte words of a swizzled 16 x 128-byte box
@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(kWWarps * 32, 1)
   __shared__ __align__(8) uint64_t wbar[kWWarps][kWStages];
   __shared__ __align__(8) uint64_t kbar;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* ks = wbuf + kWWarps * kWStages * 256;     // swizzled [rows][16]
+  const int nwarps = blockDim.x >> 5;
+  double* ks = wbuf + nwarps * kWStages * 256;      // swizzled [rows][16]
   double* mybuf = wbuf + wid * (kWStages * 256);
   uint64_t* mybar = wbar[wid];
   if (threadIdx.x == 0) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kWWarps * 32, 1)
     fence_mbar_init();
   }
   __syncwarp();
-  const int64_t w = (int64_t)blockIdx.x * kWWarps + wid, nw = (int64_t)gridDim.x * kWWarps;
+  const int64_t w = (int64_t)blockIdx.x * nwarps + wid, nw = (int64_t)gridDim.x * nwarps;
   const int nsub = (n1 + 255) / 256;
   const int64_t nvec = w < batch ? (batch - 1 - w) / nw + 1 : 0;
   const int64_t items = nvec * nsub;
@@ -690,8 +691,12 @@ int launch_half_forward(const double* c, int64_t ldc, double* out, int64_t ldo, 
       if (int rc = tmap_make(&mk, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, k, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
         return rc;
     }
-    const unsigned ctas = (unsigned)std::min<int64_t>((batch + kWWarps - 1) / kWWarps, (int64_t)sms);
-    k_half_fwd_warp<<<ctas, kWWarps * 32, kWSmem, st>>>(mc, mo, mk, (int)n1, batch, krows, kboxes);
+    // a vector is always one warp's (the arithmetic does not depend on the
+    // grid); small batches spread their warps over all SMs
+    const int nwarps = (int)std::max<int64_t>(4, std::min<int64_t>(kWWarps, (batch + sms - 1) / sms));
+    const unsigned ctas = (unsigned)std::min<int64_t>((batch + nwarps - 1) / nwarps, (int64_t)sms);
+    const int smem = nwarps * kWStages * 2048 + kboxes * krows * 128 + 1024;
+    k_half_fwd_warp<<<ctas, nwarps * 32, smem, st>>>(mc, mo, mk, (int)n1, batch, krows, kboxes);
     CJT_CUDA_TRY(cudaGetLastError());
     return CJT_OK;
   }

@@ -41,7 +41,7 @@ def test_half_exact_vs_reference_goldens(cuda, name, monkeypatch):
         assert O.parity(i[v], g["inv"][v], g["fwd"][v]) <= 1e-13
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 17, 255, 1000, 2047, 4095, 4096, 8191, 12288])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 17, 255, 1000, 2047, 4095, 4096, 8191, 12288, 16383])
 def test_half_exact_vs_recurrence_layout(cuda, n, monkeypatch):
     """Same inputs through both device paths (the recurrence layout is the
     reference's own algorithm, parity-pinned elsewhere), and the oracle."""
@@ -97,3 +97,18 @@ def test_tcgen05_inverse_matches_cublas_path(cuda, n, batch, monkeypatch):
     b = cj.inverse_batched(ip, t).cpu().numpy()
     l1 = np.abs(t.cpu().numpy()).sum(axis=1)
     assert np.all(np.max(np.abs(a - b), axis=1) <= 1e-16 * l1)
+
+
+@pytest.mark.parametrize("n", [255, 4095, 8191, 16383])
+def test_half_forward_independent_of_batch(cuda, n):
+    """The exact forward picks its kernel by layout only and gives each vector
+    one warp (or one chunk chain) whatever the batch: a vector's result is
+    bit-identical in batches of 1, 5, 150 and 2000."""
+    import torch
+    p = cj.JacobiParameters(0.5, 0.5)
+    fp = cj.plan("forward", p, n)
+    c = torch.from_numpy(np.stack([O.seeded_vector(3, v, n) for v in range(2000)])).to(cuda)
+    full = cj.forward_batched(fp, c)
+    for b in (1, 5, 150):
+        part = cj.forward_batched(fp, c[:b].contiguous())
+        assert torch.equal(part, full[:b])
