@@ -14,7 +14,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 OUT = HERE / "_lib" / "libcjt_b200.so"
 SOURCES = ["cjt_capi.cu", "cjt_chirpz.cu", "cjt_recur.cu", "cjt_shift.cu", "cjt_half.cu", "cjt_umma.cu", "cjt_host.cpp", "cjt_plan_dev.cu"]
-HEADERS = ["cjt_internal.cuh"]
+HEADERS = ["cjt_internal.cuh", "cjt_tma.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
