@@ -354,11 +354,14 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
              device: int | None = None, sync: bool = True):
     """Apply `plans` in sequence (e.g. ``(forward_plan, inverse_plan)``) to a
     (B, N+1) float64 host array, with host<->device copies overlapped with the
-    transforms: the batch is cut into chunks that flow through three CUDA
-    streams -- host->device copies, transforms, device->host copies -- linked
-    by events over a ring of `streams` device buffer slots, so the two copy
-    directions and the compute proceed independently (chunk k+1 arrives and
-    chunk k-1 leaves while chunk k is transformed).  Pinned host memory (e.g.
+    transforms: the batch is cut into chunks that flow through a
+    host->device copy stream, two transform streams (alternating chunks) and
+    a device->host copy stream over a ring of `streams` device buffer slots,
+    linked by events, so the two copy directions and the transforms proceed
+    independently (chunk k+1 arrives and chunk k-1 leaves while chunk k is
+    transformed; compute-bound batches overlap the transforms of consecutive
+    chunks -- two at a time, more only contend: config 2 5.5e8 coeffs/s with
+    two, 4.7e8 with three).  Pinned host memory (e.g.
     ``torch.empty(..., pin_memory=True)``) is required for the copies to be
     asynchronous.  Returns host_out.
 
@@ -391,7 +394,8 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
     key = (dev.index, nslots, chunk, n1)
     cached = _PIPE_CACHE.get(key)
     if cached is None:
-        h2d, comp, d2h = (torch.cuda.Stream(dev) for _ in range(3))
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        comp = [torch.cuda.Stream(dev) for _ in range(min(nslots, 2))]
         bufs = [(torch.empty((chunk, n1), dtype=torch.float64, device=dev),
                  torch.empty((chunk, n1), dtype=torch.float64, device=dev)) for _ in range(nslots)]
         ev_in = [torch.cuda.Event() for _ in range(nslots)]     # slot filled
@@ -400,7 +404,7 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
         cached = _PIPE_CACHE[key] = (h2d, comp, d2h, bufs, ev_in, ev_done, ev_free)
     h2d, comp, d2h, bufs, ev_in, ev_done, ev_free = cached
     cur = torch.cuda.current_stream(dev)
-    for s in (h2d, comp, d2h):
+    for s in (h2d, d2h, *comp):
         s.wait_stream(cur)
     k0 = _PIPE_NEXT.get(key, 0) if not sync else 0
     for k, r0 in enumerate(range(0, batch, chunk), start=k0):
@@ -411,13 +415,14 @@ def pipeline(plans, host_in, host_out=None, chunk: int | None = None, streams: i
         with torch.cuda.stream(h2d):
             a[: r1 - r0].copy_(hin[r0:r1], non_blocking=True)
             ev_in[slot].record(h2d)
-        comp.wait_event(ev_in[slot])
+        cs = comp[k % len(comp)]
+        cs.wait_event(ev_in[slot])
         src, dst = a[: r1 - r0], b[: r1 - r0]
-        with torch.cuda.stream(comp):
+        with torch.cuda.stream(cs):
             for tp in plans:
                 _execute_batched(tp, src, out=dst, check_finite=False)
                 src, dst = dst, src
-            ev_done[slot].record(comp)
+            ev_done[slot].record(cs)
         d2h.wait_event(ev_done[slot])
         with torch.cuda.stream(d2h):
             hout[r0:r1].copy_(src, non_blocking=True)
