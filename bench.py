@@ -676,6 +676,11 @@ def run_ours(args, wl):
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roofline,
             "cpu_baseline": cpu, "e2e": e2e, "parity_check_vector0": chk, "coverage": coverage,
         }
+        if getattr(ip.host, "half_gemm", False):
+            line["numerics"] = ("fp64 throughout, except the alpha = beta = 1/2 inverse's first-order "
+                                "correction to the reference's evaluation points (|M t| ~ 1e-12 ||t||_1): "
+                                "bf16 operands with fp32 accumulation on the tensor cores, contributing "
+                                "<= ~1e-15 ||t||_1; the exact conversion and the sum are fp64 (DESIGN.md 3.5)")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -81,7 +81,7 @@ def test_half_exact_large_batch_and_host_api(cuda, monkeypatch):
     assert np.max(np.abs(back.data - i[137])) <= 1e-15 * np.abs(f[137]).sum()
 
 
-@pytest.mark.parametrize("n,batch", [(255, 5), (1023, 300), (4095, 257), (8191, 40)])
+@pytest.mark.parametrize("n,batch", [(7, 3), (15, 2), (63, 9), (255, 5), (1023, 300), (4095, 257), (8191, 40)])
 def test_tcgen05_inverse_matches_cublas_path(cuda, n, batch, monkeypatch):
     """The tcgen05 correction GEMM with its fused fp64 epilogue (cjt_umma.cu)
     against the cuBLAS GEMM + separate finish on the same plan: the two differ
