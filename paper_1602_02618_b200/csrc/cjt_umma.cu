@@ -45,27 +45,29 @@ namespace cjt {
 namespace {
 
 constexpr int kBM = 128;            // output coefficients per tile (TMEM lanes)
-constexpr int kBN = 256;            // vectors per tile (accumulator columns)
 constexpr int kBK = 64;             // bf16 elements per 128-byte swizzled row
-constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;    // 16 KB
-constexpr int kBBytes = (kBN / 2) * kBK * 2;   // 16 KB: this CTA's half of the pair's B tile
-constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kEpiGroupsC = 4;
 constexpr int kTW = kBM + 2;                              // t tile width: m0 .. m0 + 129
 constexpr int kTRows = 8;                                 // vectors per epilogue chunk
 constexpr int kTBytes = kTRows * kTW * 8;                 // 8.3 KB
-constexpr int kSmem = kStages * kStageBytes + kEpiGroupsC * 2 * kTBytes + 1024;   // + alignment slack
 constexpr int kEpiGroups = kEpiGroupsC;       // epilogue warp groups (4 warps: one per TMEM lane quarter)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kTmemCols = 512;
 
-// instruction descriptor: kind::f16, A = B = bf16 (K-major), D = f32,
-// M = 256 (the CTA pair's two 128-row A tiles), N = 256
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
-                            ((uint32_t)((2 * kBM) >> 4) << 24);
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address bit 24 = CTA rank in the pair
+
+// per vector-tile width BN (256, or 128 for small batches: more pair tiles)
+template <int BN>
+struct UCfg {
+  static constexpr int BBytes = (BN / 2) * kBK * 2;     // this CTA's half of the pair's B tile
+  static constexpr int StageBytes = kABytes + BBytes;
+  static constexpr int Stages = BN == 256 ? 4 : 6;
+  static constexpr int Smem = Stages * StageBytes + kEpiGroupsC * 2 * kTBytes + 1024;
+  static constexpr uint32_t TmemCols = 2 * BN;
+  static constexpr uint32_t Idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)((2 * kBM) >> 4) << 24);
+};
 
 // shared-memory matrix descriptor, K-major, 128-byte swizzle: 8-row core
 // groups 1024 bytes apart (SBO), version 1 (sm_100), layout type 2
@@ -98,12 +100,13 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void umma_bf16_pair(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void umma_bf16_pair(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
@@ -131,11 +134,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_half_inv_umma(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_t,
                     const __grid_constant__ CUtensorMap map_x,
                     const double* __restrict__ t, const double* __restrict__ kt, double* __restrict__ out, int n1,
                     int batch, int dbg) {
+  using C = UCfg<BN>;
+  constexpr int kBN = BN, kStages = C::Stages, kStageBytes = C::StageBytes;
+  constexpr uint32_t kTmemCols = C::TmemCols;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
@@ -215,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t ad = sw128_desc(sa), bd = sw128_desc(sa + kABytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)   // 32 bytes along K per step: +2 in the 16-byte address field
-            umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+            umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, C::Idesc, (kb | k) != 0);
           umma_commit_pair(&empty[s]);         // the stage is free in both CTAs once these MMAs completed
           if (++s == kStages) {
             s = 0;
@@ -324,29 +331,46 @@ bool umma_half_supported(int64_t n1, int64_t batch) {
   return n1 % 8 == 0 && n1 <= 0x7fffffff && batch <= 0x7fffffff && !getenv("CJT_HALF_CUBLAS");
 }
 
-int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
-                      const double* k, cudaStream_t st) {
-  if (batch <= 0) return CJT_OK;
+template <int BN>
+int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
+                double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
   static DeviceOnce once;
   if (int rc = once([] {
-        CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          UCfg<BN>::Smem));
         return CJT_OK;
       }))
     return rc;
+  CUtensorMap mt;
+  if (int rc = make_map(&mt, tbf, batch, n1, BN / 2)) return rc;
+  const int64_t tiles = ((n1 + 2 * kBM - 1) / (2 * kBM)) * ((batch + BN - 1) / BN);
+  const unsigned grid = 2 * (unsigned)std::min<int64_t>(tiles, sms / 2);   // CTA pairs
+  static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
+  k_half_inv_umma<BN><<<grid, kThreads, UCfg<BN>::Smem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, dbg);
+  CJT_CUDA_TRY(cudaGetLastError());
+  return CJT_OK;
+}
+
+int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
+                      const double* k, cudaStream_t st) {
+  if (batch <= 0) return CJT_OK;
   if (((uintptr_t)t & 15) != 0) return fail(CJT_EINVAL, "umma_half_inverse: input must be 16-byte aligned");
-  CUtensorMap mm, mt, mx;
+  CUtensorMap mm, mx;
   if (int rc = make_map(&mm, Mrow, n1, n1, kBM)) return rc;
-  if (int rc = make_map(&mt, tbf, batch, n1, kBN / 2)) return rc;
   if (int rc = make_map_f64(&mx, t, batch, n1, kTRows, kTW)) return rc;
   int dev = 0, sms = 148;
   CJT_CUDA_TRY(cudaGetDevice(&dev));
   CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t tiles = ((n1 + 2 * kBM - 1) / (2 * kBM)) * ((batch + kBN - 1) / kBN);
-  const unsigned grid = 2 * (unsigned)std::min<int64_t>(tiles, sms / 2);   // CTA pairs
-  static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
-  k_half_inv_umma<<<grid, kThreads, kSmem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, dbg);
-  CJT_CUDA_TRY(cudaGetLastError());
-  return CJT_OK;
+  // 256-vector tiles, or 128 when they would leave CTA pairs idle (small
+  // batches, e.g. one GPU's shard of a multi-GPU batch); the arithmetic of a
+  // vector does not depend on the tile width (same K order, same epilogue)
+  // (waves x tile time, tile time ~ width; ties go to the wider tile)
+  const int64_t mpt = (n1 + 2 * kBM - 1) / (2 * kBM), pairs = std::max(1, sms / 2);
+  const int64_t cost256 = 2 * ((mpt * ((batch + 255) / 256) + pairs - 1) / pairs);
+  const int64_t cost128 = (mpt * ((batch + 127) / 128) + pairs - 1) / pairs;
+  if (cost128 < cost256 && !getenv("CJT_UMMA_BN256"))
+    return launch_umma<128>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+  return launch_umma<256>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
 }
 
 }  // namespace cjt

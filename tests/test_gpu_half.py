@@ -112,3 +112,18 @@ def test_half_forward_independent_of_batch(cuda, n):
     for b in (1, 5, 150):
         part = cj.forward_batched(fp, c[:b].contiguous())
         assert torch.equal(part, full[:b])
+
+
+def test_tcgen05_inverse_tile_width_invariance(cuda, monkeypatch):
+    """Small batches run the tcgen05 GEMM with 128-vector tiles (more CTA
+    pairs busy), large ones with 256: same K order and epilogue, so the
+    results are bit-identical."""
+    import torch
+    p = cj.JacobiParameters(0.5, 0.5)
+    ip = cj.plan("inverse", p, 4095)
+    t = torch.from_numpy(np.stack([O.seeded_vector(3, v, 4095) for v in range(300)])).to(cuda)
+    monkeypatch.delenv("CJT_UMMA_BN256", raising=False)
+    a = cj.inverse_batched(ip, t)
+    monkeypatch.setenv("CJT_UMMA_BN256", "1")
+    b = cj.inverse_batched(ip, t)
+    assert torch.equal(a, b)
