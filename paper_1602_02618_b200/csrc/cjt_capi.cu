@@ -288,7 +288,7 @@ inline void unit_root(int64_t num, int64_t den, double* re, double* im) {
 
 // Twiddle tables shared by every plan of a device (immutable, built once per
 // length with long-double trigonometry and kept for the process lifetime):
-// L = 8192: exp(-2 pi i u / 8192), u < 8192; multi-pass L: the hi table
+// L = 8192: exp(-2 pi i u / 8192), u < 8192 (+ packed power tables); multi-pass L: the hi table
 // exp(-2 pi i a 4096 / L), a < max(1, L / 4096), followed by the lo table
 // exp(-2 pi i b / L), b < 4096.
 int shared_twiddles(int64_t L, const double2** out) {
@@ -301,8 +301,12 @@ int shared_twiddles(int64_t L, const double2** out) {
   if (it == cache.end()) {
     std::vector<double2> tw;
     if (L == 8192) {
-      tw.resize(8192);
+      // followed by the packed power tables exp(-2 pi i k / 2^c) at
+      // 8192 + 2^c + k (tw_pow, cjt_internal.cuh): decimations of the same values
+      tw.resize(TW_TABLE_ENTRIES);
       for (int u = 0; u < 8192; ++u) unit_root(u, 8192, &tw[u].x, &tw[u].y);
+      for (int c = 0; c <= 13; ++c)
+        for (int k = 0; k < (1 << c); ++k) tw[TW_PACKED_OFFSET + (1 << c) + k] = tw[(size_t)k << (13 - c)];
     } else {
       const int64_t nhi = std::max<int64_t>(1, L / 4096);
       tw.resize((size_t)(nhi + 4096));

@@ -35,6 +35,9 @@ namespace {
 template <int LOGL>
 struct FusedCfg {
   static constexpr int L = 1 << LOGL;
+#ifndef CJT_FUSED13_TWSMEM
+#define CJT_FUSED13_TWSMEM 0
+#endif
 #ifndef CJT_FUSED13_LEPT
 #define CJT_FUSED13_LEPT 4
 #endif
@@ -47,7 +50,7 @@ struct FusedCfg {
   static constexpr int T = E / EPT;                 // threads per CTA
   // 8192: the FFT buffer and accumulator leave ~23 KB of L1, less than the
   // global twiddle table's working set -> twiddles from shared memory
-  static constexpr bool TW_SMEM = LOGL == 13;
+  static constexpr bool TW_SMEM = CJT_FUSED13_TWSMEM && LOGL == 13;
   static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8 + (TW_SMEM ? 1024 * 16 : 0);
 };
 
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
 
 // column FFT twiddles from the shared-memory table (see CJT_ROWS_TWSMEM)
 #ifndef CJT_COLS_TWSMEM
-#define CJT_COLS_TWSMEM 1
+#define CJT_COLS_TWSMEM 0
 #endif
 template <int LOG1>
 struct ColCfg {
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
 // of the 8192-entry global table: the global table's scattered per-lane
 // loads cost L1 sectors the row kernels are short of
 #ifndef CJT_ROWS_TWSMEM
-#define CJT_ROWS_TWSMEM 1
+#define CJT_ROWS_TWSMEM 0
 #endif
 template <int LOG2>
 struct RowCfg {

@@ -265,16 +265,37 @@ __device__ __forceinline__ TwSmem tw_smem_init(double2* tab, const double2* __re
   return TwSmem{tab};
 }
 
-// v[r] *= w^r for r = 1..R-1 with w = W^u (conjugated for DIR > 0);
-// w^(2^j) are read from the table (u 2^j < 8192 since r k < NS R <= 8192).
-template <int R, int DIR, class TW>
-__device__ __forceinline__ void twiddle_powers(double2* v, const TW& tw, int u) {
+// Packed power tables behind the 8192-entry table (shared_twiddles, capi):
+//   tw[8192 + 2^c + k] = exp(-2 pi i k / 2^c),  c = 0..13, k < 2^c.
+// The thread with butterfly index k of a size-2^A pass needs w^(2^p),
+// w = exp(-2 pi i k / 2^A), i.e. entry k of table c = A - p: consecutive
+// threads read consecutive entries (coalesced 16-byte loads, 4 wavefronts
+// per warp) where the same values taken from the 8192-entry table are
+// 2^(13 - A + p) entries apart (one cache line per lane, up to 32 wavefronts
+// per load: measured 28 % of the row kernels' l1tex wavefronts).
+constexpr int TW_PACKED_OFFSET = 8192;
+constexpr int TW_TABLE_ENTRIES = 8192 + 16384;
+template <int A, int P>
+__device__ __forceinline__ double2 tw_pow(const double2* __restrict__ tw, int k) {
+  static_assert(A - P >= 0 && A <= 13, "tw_pow: table out of range");
+  return __ldg(&tw[TW_PACKED_OFFSET + (1 << (A - P)) + k]);
+}
+template <int A, int P>
+__device__ __forceinline__ double2 tw_pow(const TwSmem& tw, int k) {
+  return tw((k << (13 - A)) << P);
+}
+
+// v[r] *= w^r for r = 1..R-1 with w = exp(-2 pi i k / 2^A) (conjugated for
+// DIR > 0), k < 2^A / R; w^(2^j) are read from the tables (tw_pow), the other
+// powers are products of at most three of them.
+template <int R, int DIR, int A, class TW>
+__device__ __forceinline__ void twiddle_powers(double2* v, const TW& tw, int k) {
   double2 p[32];
-  p[1] = tw_at(tw, u);
-  if constexpr (R > 2) p[2] = tw_at(tw, 2 * u);
-  if constexpr (R > 4) p[4] = tw_at(tw, 4 * u);
-  if constexpr (R > 8) p[8] = tw_at(tw, 8 * u);
-  if constexpr (R > 16) p[16] = tw_at(tw, 16 * u);
+  p[1] = tw_pow<A, 0>(tw, k);
+  if constexpr (R > 2) p[2] = tw_pow<A, 1>(tw, k);
+  if constexpr (R > 4) p[4] = tw_pow<A, 2>(tw, k);
+  if constexpr (R > 8) p[8] = tw_pow<A, 3>(tw, k);
+  if constexpr (R > 16) p[16] = tw_pow<A, 4>(tw, k);
   if constexpr (DIR > 0) {
 #pragma unroll
     for (int j = 1; j < R; j <<= 1) p[j].y = -p[j].y;
@@ -350,8 +371,8 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
       const int j = t + q * TPG;
       const int k = j & (NS - 1);
       if constexpr (PASS > 0) {
-        constexpr int SH = 13 - (LNS + LR);
 #if CJT_TW_MODE == 0
+        constexpr int SH = 13 - (LNS + LR);
 #pragma unroll
         for (int r = 1; r < R; ++r) {
           double2 w = tw_at(tw, (r * k) << SH);
@@ -361,7 +382,7 @@ __device__ __forceinline__ void fft_pass(double2* s, int t, const TW& tw,
 #else
         // powers of w = W^k from the tabulated w, w^2, w^4, w^8 (at most three
         // rounded products per power)
-        twiddle_powers<R, DIR>(&v[q * R], tw, k << SH);
+        twiddle_powers<R, DIR, LNS + LR>(&v[q * R], tw, k);
 #endif
       }
       dft_reg<R, DIR>(&v[q * R]);
@@ -435,7 +456,7 @@ __device__ __forceinline__ void fft2_first(double2* s, int n2, const TW& tw, con
 #pragma unroll
   for (int n1 = 0; n1 < 16; ++n1) v[n1] = ld(n2 + F::S * n1);
   dft_reg<16, -1>(v);
-  twiddle_powers<16, -1>(v, tw, n2 << (13 - LOGL));
+  twiddle_powers<16, -1, LOGL>(v, tw, n2);
 #pragma unroll
   for (int k1 = 0; k1 < 16; ++k1) s[k1 * F::PS + pad16(n2)] = v[k1];
 }
@@ -446,7 +467,7 @@ __device__ __forceinline__ void fft2_last_inv(const double2* s, int n2, const TW
   double2 v[16];
 #pragma unroll
   for (int k1 = 0; k1 < 16; ++k1) v[k1] = s[k1 * F::PS + pad16(n2)];
-  twiddle_powers<16, +1>(v, tw, n2 << (13 - LOGL));
+  twiddle_powers<16, +1, LOGL>(v, tw, n2);
   dft_reg<16, +1>(v);
 #pragma unroll
   for (int n1 = 0; n1 < 16; ++n1) st(n2 + F::S * n1, v[n1]);
@@ -469,7 +490,7 @@ __device__ __forceinline__ void sub_pass(double2* s, int t, const TW& tw, const 
   for (int q = 0; q < NBF; ++q) {
     const int j = t + q * TPG;
     const int k = j & (NS - 1);
-    if constexpr (LNS > 0) twiddle_powers<R, DIR>(&v[q * R], tw, k << (13 - (LNS + LR)));
+    if constexpr (LNS > 0) twiddle_powers<R, DIR, LNS + LR>(&v[q * R], tw, k);
     dft_reg<R, DIR>(&v[q * R]);
     const int base = ((j - k) << LR) + k;
 #pragma unroll
@@ -514,7 +535,7 @@ __device__ __forceinline__ void sub_middle(double2* s, int t, const TW& tw, cons
 #pragma unroll
   for (int q = 0; q < NBF; ++q) {
     const int j = t + q * TPG;   // j < NS: this butterfly's outputs are j + r NS
-    if constexpr (LNS > 0) twiddle_powers<R, -1>(&v[q * R], tw, j << (13 - (LNS + LR)));
+    if constexpr (LNS > 0) twiddle_powers<R, -1, LNS + LR>(&v[q * R], tw, j);
     dft_reg<R, -1>(&v[q * R]);
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = op(j + r * NS, v[q * R + r]);
