@@ -540,8 +540,24 @@ __device__ __forceinline__ void sub_middle(double2* s, int t, const TW& tw, cons
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = op(j + r * NS, v[q * R + r]);
     dft_reg<R, +1>(&v[q * R]);
+    // R consecutive elements per thread: with pad16, the 16-byte bank groups of
+    // neighbouring lanes collide in pairs for R = 8 (lanes j, j + 1) and R = 2
+    // (lanes j, j + 4) -- ncu: 2-way conflicts, 11 % of the row kernels'
+    // shared-memory wavefronts.  Those lanes store their elements in the order
+    // r ^ R/2 instead (a register select), which makes every store conflict-free.
+    constexpr bool SWZ = (LR == 3) || (LR == 1 && LOGN >= 7);
+    if constexpr (SWZ) {
+      const bool f = LR == 3 ? (j & 1) : ((j >> 2) & 1);
+      const int x = f ? R / 2 : 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[pad16((j << LR) + r)] = v[q * R + r];
+      for (int r = 0; r < R; ++r) {
+        const double2 a = v[q * R + r], b = v[q * R + (r ^ (R / 2))];
+        s[pad16((j << LR) + (r ^ x))] = f ? b : a;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[pad16((j << LR) + r)] = v[q * R + r];
+    }
   }
   __syncwarp();
 }

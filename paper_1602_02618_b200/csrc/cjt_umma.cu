@@ -83,12 +83,27 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 
 // both CTAs of the pair load into their own shared memory; the bytes are
 // counted on the LEADER's (rank 0) barrier
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                                 uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerMask)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerMask), "l"(policy)
       : "memory");
+}
+
+// L2 eviction policies: the operand tiles (M: re-read by every vector tile;
+// the bf16 vectors: re-read by the 16 coefficient tiles of their vector tile)
+// must stay in L2 while the epilogue streams t in and the result out
+__device__ __forceinline__ uint64_t l2_policy(int kind) {   // 0 normal, 1 evict_last, 2 evict_first
+  uint64_t p;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 // arrive on this barrier in both CTAs of the pair once the leader's MMAs completed
@@ -134,12 +149,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+template <int BN, int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_half_inv_umma(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_t,
                     const __grid_constant__ CUtensorMap map_x,
                     const double* __restrict__ t, const double* __restrict__ kt, double* __restrict__ out, int n1,
-                    int batch, int dbg) {
+                    int batch, int hints) {
   using C = UCfg<BN>;
   constexpr int kBN = BN, kStages = C::Stages, kStageBytes = C::StageBytes;
   constexpr uint32_t kTmemCols = C::TmemCols;
@@ -189,14 +204,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // TMA producer
       int s = 0;
       uint32_t ph = 0;
+      const uint64_t pol_a = l2_policy(hints & 3), pol_b = l2_policy((hints >> 2) & 3);
       for (int tile = cid; tile < tiles; tile += ncl) {
         const int m0 = (tile % mpt) * 2 * kBM + rank * kBM, b0 = (tile / mpt) * kBN + rank * (kBN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);      // the pair's MMAs are done with this stage
           uint8_t* sa = smem + s * kStageBytes;
           if (rank == 0) mbar_expect_tx(&full[s], 2 * kStageBytes);   // both CTAs' bytes
-          tma_load_2d_pair(sa, &map_m, kb * kBK, m0, &full[s]);
-          tma_load_2d_pair(sa + kABytes, &map_t, kb * kBK, b0, &full[s]);
+          tma_load_2d_pair(sa, &map_m, kb * kBK, m0, &full[s], pol_a);
+          tma_load_2d_pair(sa + kABytes, &map_t, kb * kBK, b0, &full[s], pol_b);
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
@@ -245,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr int kChunks = kBN / (kTRows * kEpiGroups);   // per tile and group
     const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
     const int nseq = my_tiles * kChunks;
+    const uint64_t pol_x = l2_policy((hints >> 4) & 3);
     auto issue_x = [&](int sq) {   // leader: t tile of chunk sq of this group's sequence
       if (sq >= nseq) return;
       const int tile = cid + (sq / kChunks) * ncl;
@@ -252,14 +269,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint64_t* br = &xbar[grp][sq & 1];
       mbar_expect_tx(br, kTBytes);
       asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-              smem_u32(xb + (sq & 1) * (kTRows * kTW))),
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+          "%3}], [%4], %5;" ::"r"(smem_u32(xb + (sq & 1) * (kTRows * kTW))),
           "l"(reinterpret_cast<uint64_t>(&map_x)), "r"((tile % mpt) * 2 * kBM + rank * kBM),
           "r"((tile / mpt) * kBN + c0),
-          "r"(smem_u32(br))
+          "r"(smem_u32(br)), "l"(pol_x)
           : "memory");
     };
-    if (leader && dbg != 1) issue_x(0);
+    if (leader && !(DBG & 5)) issue_x(0);
     int it = 0, sq = 0;
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       const int acc = it & 1;
@@ -272,32 +289,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const double c_h = 0.5 * inv_k, c_t = m == 0 ? inv_k : c_h;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      if (dbg == 1) {   // timing experiment: accumulator read only, no HBM traffic
+      if constexpr (DBG & 1) {   // timing experiment: accumulator read only, no HBM traffic
         float v[8];
         tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN), v);
         if (v[0] == 12345.f) out[0] = v[1];
         tc_fence_before();
         mbar_arrive_leader(&tempty[acc]);
         sq += kChunks;
-        continue;
-      }
+      } else {
 #pragma unroll 1
       for (int c0 = kTRows * grp; c0 < kBN; c0 += kTRows * kEpiGroups, ++sq) {
-        if (leader) issue_x(sq + 1);         // its buffer was released by the barrier below
+        // (DBG bits, timing experiments only: 2 no result stores, 4 no t tiles,
+        // 8 no fp64 arithmetic, 16 no accumulator loads)
+        if (leader && !(DBG & 4)) issue_x(sq + 1);         // its buffer was released by the barrier below
         float v[kTRows];
-        tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN + c0), v);
-        mbar_wait(&xbar[grp][sq & 1], (uint32_t)((sq >> 1) & 1));
+        if constexpr (DBG & 16) {
+#pragma unroll
+          for (int j = 0; j < kTRows; ++j) v[j] = (float)(c0 + j);
+        } else {
+          tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN + c0), v);
+        }
+        if constexpr (!(DBG & 4)) mbar_wait(&xbar[grp][sq & 1], (uint32_t)((sq >> 1) & 1));
         const double* xr = xb + (sq & 1) * (kTRows * kTW);
 #pragma unroll
         for (int j = 0; j < kTRows; ++j) {
           const int b = b0 + c0 + j;
-          const double tm = xr[j * kTW + ml], hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
-          if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, fma(c_t, tm, fma(-c_h, hi, (double)v[j])));
+          double tm = 1.0, hi = 2.0;
+          if constexpr (!(DBG & 4)) {
+            tm = xr[j * kTW + ml];
+            hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
+          }
+          double r;
+          if constexpr (DBG & 8)
+            r = __hiloint2double(__double2hiint(tm) ^ __double2loint(hi), __double2loint(tm) ^ __float_as_int(v[j]));
+          else
+            r = fma(c_t, tm, fma(-c_h, hi, (double)v[j]));
+          if constexpr (DBG & 2) {
+            if (mv && b < batch && __double2loint(r) == 0x12345678 && __double2hiint(r) == 0x7654321)
+              __stcs(out + (int64_t)b * n1 + m, r);
+          } else {
+            if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, r);
+          }
         }
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group is done with this buffer
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);   // the leader may reuse this accumulator (both CTAs)
+      }
     }
   }
   tc_fence_before();
@@ -331,12 +369,12 @@ bool umma_half_supported(int64_t n1, int64_t batch) {
   return n1 % 8 == 0 && n1 <= 0x7fffffff && batch <= 0x7fffffff && !getenv("CJT_HALF_CUBLAS");
 }
 
-template <int BN>
-int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
-                double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
+template <int BN, int DBG>
+int launch_umma_dbg(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
+                    double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
   static DeviceOnce once;
   if (int rc = once([] {
-        CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma<BN, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           UCfg<BN>::Smem));
         return CJT_OK;
       }))
@@ -345,10 +383,28 @@ int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, c
   if (int rc = make_map(&mt, tbf, batch, n1, BN / 2)) return rc;
   const int64_t tiles = ((n1 + 2 * kBM - 1) / (2 * kBM)) * ((batch + BN - 1) / BN);
   const unsigned grid = 2 * (unsigned)std::min<int64_t>(tiles, sms / 2);   // CTA pairs
-  static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
-  k_half_inv_umma<BN><<<grid, kThreads, UCfg<BN>::Smem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, dbg);
+  // L2 policies of the TMA loads: M | vectors << 2 | fp64 t tiles << 4 (0 normal, 1 evict_last, 2 evict_first)
+  static const int hints = getenv("CJT_UMMA_HINTS") ? atoi(getenv("CJT_UMMA_HINTS")) : 37;
+  k_half_inv_umma<BN, DBG><<<grid, kThreads, UCfg<BN>::Smem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, hints);
   CJT_CUDA_TRY(cudaGetLastError());
   return CJT_OK;
+}
+
+template <int BN>
+int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
+                double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
+  // $CJT_UMMA_DBG (timing experiments): 1 = epilogue without HBM traffic;
+  // builds with -DCJT_UMMA_DBG_BUILD also have the partial epilogues (bit mask, see the kernel)
+  static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
+  switch (dbg) {
+#define CJT_UD(D) case D: return launch_umma_dbg<BN, D>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+    CJT_UD(1)
+#ifdef CJT_UMMA_DBG_BUILD
+    CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10)
+#endif
+#undef CJT_UD
+    default: return launch_umma_dbg<BN, 0>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+  }
 }
 
 int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
