@@ -384,7 +384,11 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
     // (8192-point rows only while the columns would otherwise fall below 16
     // points: 4096-point rows at 2 CTAs/SM win for 2^16 .. 2^19 too, config-4/5
     // A/B with CJT_MP_L2MAX: 58.9 -> 57.8 ms, 159.4 -> 155.5 ms)
-    const int l2 = std::min({l2max, lg - 4, lg >= 16 ? 12 : 13});
+    int l2 = std::min({l2max, lg - 4, lg >= 16 ? 12 : 13});
+    {   // $CJT_MP_L2_<lg>=<l2> (experiments): row length of one Bluestein length
+      const std::string key = "CJT_MP_L2_" + std::to_string(lg);
+      if (const char* e = getenv(key.c_str())) l2 = std::max(10, std::min({13, lg - 4, atoi(e)}));
+    }
     cz.log1 = lg - l2;
     cz.log2 = l2;
   }

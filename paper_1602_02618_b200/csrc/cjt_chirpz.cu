@@ -447,7 +447,9 @@ struct ColCfg {
   static constexpr int NC = E / L1;                  // columns per CTA
   static constexpr int T = E / 16;
   static constexpr int CS = padded_len(L1) + 1;      // odd column stride (conflict-free transpose)
-  static constexpr int SMEM = NC * CS * 16 + (CJT_COLS_TWSMEM ? 1024 * 16 : 0);
+  // + per-thread four-step twiddles (W_L^{n2 k1_0}, W_L^{n2 T/NC}), looked up once for all terms
+  static constexpr int TWO = NC * CS + (CJT_COLS_TWSMEM ? 1024 : 0);   // offset (double2) of that table
+  static constexpr int SMEM = (TWO + 2 * T) * 16;
 };
 
 // pass 1: x (real slice) * pre_m -> column FFTs over n1 -> * W_L^{n2 k1} -> buf[b][m][k1][n2]
@@ -474,6 +476,13 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
   const double* xb = x + b * ldx + cz.p0 + to;
   const int grp = threadIdx.x / (L1 / 16);
   const int t = threadIdx.x % (L1 / 16);
+  // this thread's column n2 is fixed and k1 = k1_0 + i T/NC: twiddles
+  // W_L^{n2 k1} by a running product from two table values, looked up once
+  // for all terms (scattered loads: one cache line per lane)
+  // (kept in shared memory: eight more live registers across the FFT spill)
+  double2* tws = smem + Cfg::TWO + 2 * threadIdx.x;
+  tws[0] = twiddle_L(cz, (c0 + threadIdx.x % NC) * (threadIdx.x / NC));
+  tws[1] = twiddle_L(cz, (c0 + threadIdx.x % NC) * (T / NC));
   for (int m = 0; m < cz.m_count; ++m) {
     const double2* pre = cz.pre + (int64_t)m * cz.width + to;
 #pragma unroll
@@ -493,13 +502,11 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
     fft_smem<LOG1, -1, 4, FftSync<LOG1, 4>>(smem + grp * CS, t, tw);
     __syncthreads();   // the transposed store reads other warps' columns
     double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L;
-    // this thread's column n2 is fixed and k1 = k1_0 + i T/NC: twiddles
-    // W_L^{n2 k1} by a running product from two table values
     const int c = threadIdx.x % NC;
     const int64_t n2 = c0 + c;
     const int k10 = threadIdx.x / NC;
-    double2 w = twiddle_L(cz, n2 * k10);
-    const double2 ws = twiddle_L(cz, n2 * (T / NC));
+    double2 w = tws[0];
+    const double2 ws = tws[1];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int k1 = k10 + i * (T / NC);
@@ -802,14 +809,18 @@ __global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 
   double acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  // W_L^{n2 k1} running product, looked up once for all terms (see k_chirpz_cols_fwd)
+  double2* tws = smem + Cfg::TWO + 2 * threadIdx.x;
+  tws[0] = twiddle_L(cz, (c0 + threadIdx.x % NC) * (threadIdx.x / NC));
+  tws[1] = twiddle_L(cz, (c0 + threadIdx.x % NC) * (T / NC));
   for (int m = 0; m < cz.m_count; ++m) {
     const double2* bm = buf + ((b * cz.m_count + m) * nslot + blockIdx.z) * L;
     {
       const int c = threadIdx.x % NC;
       const int64_t n2 = c0 + c;
       const int k10 = threadIdx.x / NC;
-      double2 w = twiddle_L(cz, n2 * k10);
-      const double2 ws = twiddle_L(cz, n2 * (T / NC));
+      double2 w = tws[0];
+      const double2 ws = tws[1];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int k1 = k10 + i * (T / NC);

@@ -590,10 +590,14 @@ int launch_to_bf16(const double* in, int64_t ldi, void* out, int64_t ldo, int64_
 int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, void* tbf,
                       float* corr, const double* k, cudaStream_t st) {
   if (batch <= 0) return CJT_OK;
+  // tcgen05 GEMM with the fp64 finish fused into its epilogue (cjt_umma.cu);
+  // the bf16 conversion of t runs concurrently with it (the unused fp32
+  // correction buffer holds the per-group progress counters)
+  const bool umma = umma_half_supported(n1, batch) && ((uintptr_t)tbf & 15) == 0 && ((uintptr_t)Mrow & 15) == 0;
+  if (umma && umma_overlap_enabled())
+    return umma_half_inverse(t, out, n1, batch, Mrow, tbf, k, reinterpret_cast<int*>(corr), st);
   if (int rc = launch_to_bf16(t, n1, tbf, n1, n1, batch, st)) return rc;
-  // tcgen05 GEMM with the fp64 finish fused into its epilogue (cjt_umma.cu)
-  if (umma_half_supported(n1, batch) && ((uintptr_t)tbf & 15) == 0 && ((uintptr_t)Mrow & 15) == 0)
-    return umma_half_inverse(t, out, n1, batch, Mrow, tbf, k, st);
+  if (umma) return umma_half_inverse(t, out, n1, batch, Mrow, tbf, k, nullptr, st);
   cublasHandle_t h;
   if (int rc = blas_handle(st, &h)) return rc;
   const float one = 1.0f, zero = 0.0f;

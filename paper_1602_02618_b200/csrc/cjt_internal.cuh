@@ -693,8 +693,9 @@ int permute_spectra(const double2* natural_host, int64_t L, int ntile, int mode,
 // tbf: [batch][n1] bf16 scratch, corr: [batch][n1] fp32 scratch.
 int launch_transpose_bf16(const void* in, void* out, int64_t rows, int64_t cols, cudaStream_t st);
 bool umma_half_supported(int64_t n1, int64_t batch);
-int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
-                      const double* k, cudaStream_t st);
+bool umma_overlap_enabled();   // $CJT_HALF_OVERLAP=1: conversion overlapped with the GEMM (opt-in, slower)
+int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, void* tbf,
+                      const double* k, int* flags, cudaStream_t st);
 int half_gemm_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* X, void* tbf,
                       float* corr, const double* k, cudaStream_t st);
 int half_gemm_prepare(cudaStream_t st);   // cuBLAS handle of `st` (outside capture)

@@ -149,12 +149,63 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---------------------------------------------------------------------------
+// fp64 -> bf16 conversion of the input, overlapped with the GEMM: the
+// conversion kernel lets its dependent launch at once (programmatic dependent
+// launch), walks the rows in order in units of kUnitElems elements and counts
+// finished units per 128-row group; the GEMM's TMA producers wait for a group's
+// count before their first load of its rows.  One persistent wave of small
+// CTAs (no shared memory), which stay resident next to the GEMM's CTAs.
+constexpr int kGroupRows = 128;
+constexpr int kUnitElems = 16384;
+
+__device__ __forceinline__ void wait_group(const int* flag, int need) {
+  int v = 0;
+  for (int spins = 0; spins < (1 << 22); ++spins) {   // (bounded: a lost signal must not hang the GPU)
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= need) break;
+    __nanosleep(100);
+  }
+  asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy writes -> TMA (async proxy) reads
+}
+
+__global__ void __launch_bounds__(256) k_to_bf16_flagged(const double* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                                         int64_t n1, int64_t rows, int* __restrict__ flags) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t gelems = (int64_t)kGroupRows * n1, total = rows * n1;
+  const int64_t upg = (gelems + kUnitElems - 1) / kUnitElems;
+  const int64_t nunits = ((rows + kGroupRows - 1) / kGroupRows) * upg;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t g = u / upg, gbeg = g * gelems, gend = min(total, gbeg + gelems);
+    const int64_t e0 = gbeg + (u % upg) * kUnitElems, e1 = min(gend, e0 + kUnitElems);
+#pragma unroll 4
+    for (int64_t q = e0 / 4 + threadIdx.x; q < e1 / 4; q += 256) {   // (N + 1) % 8 == 0: whole quads
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(in) + 2 * q);
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(in) + 2 * q + 1);
+      __nv_bfloat162 lo, hi;
+      lo.x = __double2bfloat16(a.x);
+      lo.y = __double2bfloat16(a.y);
+      hi.x = __double2bfloat16(b.x);
+      hi.y = __double2bfloat16(b.y);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&lo);
+      w.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[q] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(flags + g, 1);
+    }
+  }
+}
+
 template <int BN, int DBG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_half_inv_umma(const __grid_constant__ CUtensorMap map_m, const __grid_constant__ CUtensorMap map_t,
                     const __grid_constant__ CUtensorMap map_x,
                     const double* __restrict__ t, const double* __restrict__ kt, double* __restrict__ out, int n1,
-                    int batch, int hints) {
+                    int batch, int hints, const int* __restrict__ flags, int flag_need) {
   using C = UCfg<BN>;
   constexpr int kBN = BN, kStages = C::Stages, kStageBytes = C::StageBytes;
   constexpr uint32_t kTmemCols = C::TmemCols;
@@ -207,6 +258,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = l2_policy(hints & 3), pol_b = l2_policy((hints >> 2) & 3);
       for (int tile = cid; tile < tiles; tile += ncl) {
         const int m0 = (tile % mpt) * 2 * kBM + rank * kBM, b0 = (tile / mpt) * kBN + rank * (kBN / 2);
+        // overlapped conversion (k_to_bf16_flagged runs concurrently): the bf16
+        // rows of this tile's 128-row group must be complete
+        if (flags && b0 < batch) wait_group(flags + b0 / kGroupRows, flag_need);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);      // the pair's MMAs are done with this stage
           uint8_t* sa = smem + s * kStageBytes;
@@ -371,7 +425,7 @@ bool umma_half_supported(int64_t n1, int64_t batch) {
 
 template <int BN, int DBG>
 int launch_umma_dbg(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
-                    double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
+                    double* out, int64_t n1, int64_t batch, int sms, const int* flags, cudaStream_t st) {
   static DeviceOnce once;
   if (int rc = once([] {
         CJT_CUDA_TRY(cudaFuncSetAttribute(k_half_inv_umma<BN, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -385,32 +439,64 @@ int launch_umma_dbg(const CUtensorMap& mm, const void* tbf, const CUtensorMap& m
   const unsigned grid = 2 * (unsigned)std::min<int64_t>(tiles, sms / 2);   // CTA pairs
   // L2 policies of the TMA loads: M | vectors << 2 | fp64 t tiles << 4 (0 normal, 1 evict_last, 2 evict_first)
   static const int hints = getenv("CJT_UMMA_HINTS") ? atoi(getenv("CJT_UMMA_HINTS")) : 37;
-  k_half_inv_umma<BN, DBG><<<grid, kThreads, UCfg<BN>::Smem, st>>>(mm, mt, mx, t, k, out, (int)n1, (int)batch, hints);
-  CJT_CUDA_TRY(cudaGetLastError());
+  const int need = (int)(((int64_t)kGroupRows * n1 + kUnitElems - 1) / kUnitElems);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = UCfg<BN>::Smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;   // start while the conversion kernel runs
+  cfg.attrs = attr;
+  cfg.numAttrs = flags ? 1 : 0;
+  CJT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_half_inv_umma<BN, DBG>, mm, mt, mx, t, k, out, (int)n1, (int)batch, hints,
+                                  flags, need));
   return CJT_OK;
 }
 
 template <int BN>
 int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, const double* t, const double* k,
-                double* out, int64_t n1, int64_t batch, int sms, cudaStream_t st) {
+                double* out, int64_t n1, int64_t batch, int sms, const int* flags, cudaStream_t st) {
   // $CJT_UMMA_DBG (timing experiments): 1 = epilogue without HBM traffic;
   // builds with -DCJT_UMMA_DBG_BUILD also have the partial epilogues (bit mask, see the kernel)
   static const int dbg = getenv("CJT_UMMA_DBG") ? atoi(getenv("CJT_UMMA_DBG")) : 0;
   switch (dbg) {
-#define CJT_UD(D) case D: return launch_umma_dbg<BN, D>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+#define CJT_UD(D) case D: return launch_umma_dbg<BN, D>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
     CJT_UD(1)
 #ifdef CJT_UMMA_DBG_BUILD
     CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10)
 #endif
 #undef CJT_UD
-    default: return launch_umma_dbg<BN, 0>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+    default: return launch_umma_dbg<BN, 0>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
   }
 }
 
-int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, const void* tbf,
-                      const double* k, cudaStream_t st) {
+bool umma_overlap_enabled() {
+  // opt-in: measured slower on B200 (config 3: 0.420 vs 0.382 ms per step) -- the
+  // conversion's HBM traffic slows the GEMM's operand and epilogue streams by
+  // more than the 46 us it hides
+  static const bool on = getenv("CJT_HALF_OVERLAP") && atoi(getenv("CJT_HALF_OVERLAP")) == 1;
+  return on;
+}
+
+// flags != nullptr: tbf is NOT converted yet -- the conversion runs here,
+// overlapped with the GEMM (flags: one int per 128 vectors, scratch)
+int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, const void* Mrow, void* tbf,
+                      const double* k, int* flags, cudaStream_t st) {
   if (batch <= 0) return CJT_OK;
   if (((uintptr_t)t & 15) != 0) return fail(CJT_EINVAL, "umma_half_inverse: input must be 16-byte aligned");
+  if (flags) {
+    const int64_t ngroups = (batch + kGroupRows - 1) / kGroupRows;
+    CJT_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)ngroups * sizeof(int), st));
+    int dev0 = 0, sms0 = 148;
+    CJT_CUDA_TRY(cudaGetDevice(&dev0));
+    CJT_CUDA_TRY(cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0));
+    const int64_t nunits = ngroups * (((int64_t)kGroupRows * n1 + kUnitElems - 1) / kUnitElems);
+    k_to_bf16_flagged<<<(unsigned)std::min<int64_t>(nunits, 2 * sms0), 256, 0, st>>>(
+        t, reinterpret_cast<__nv_bfloat16*>(tbf), n1, batch, flags);
+    CJT_CUDA_TRY(cudaGetLastError());
+  }
   CUtensorMap mm, mx;
   if (int rc = make_map(&mm, Mrow, n1, n1, kBM)) return rc;
   if (int rc = make_map_f64(&mx, t, batch, n1, kTRows, kTW)) return rc;
@@ -425,8 +511,8 @@ int umma_half_inverse(const double* t, double* out, int64_t n1, int64_t batch, c
   const int64_t cost256 = 2 * ((mpt * ((batch + 255) / 256) + pairs - 1) / pairs);
   const int64_t cost128 = (mpt * ((batch + 127) / 128) + pairs - 1) / pairs;
   if (cost128 < cost256 && !getenv("CJT_UMMA_BN256"))
-    return launch_umma<128>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
-  return launch_umma<256>(mm, tbf, mx, t, k, out, n1, batch, sms, st);
+    return launch_umma<128>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
+  return launch_umma<256>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
 }
 
 }  // namespace cjt
