@@ -476,8 +476,8 @@ bool umma_overlap_enabled() {
   // opt-in: measured slower on B200 (config 3: 0.420 vs 0.382 ms per step) -- the
   // conversion's HBM traffic slows the GEMM's operand and epilogue streams by
   // more than the 46 us it hides
-  static const bool on = getenv("CJT_HALF_OVERLAP") && atoi(getenv("CJT_HALF_OVERLAP")) == 1;
-  return on;
+  const char* e = getenv("CJT_HALF_OVERLAP");   // (read per call: tests switch it)
+  return e && atoi(e) == 1;
 }
 
 // flags != nullptr: tbf is NOT converted yet -- the conversion runs here,

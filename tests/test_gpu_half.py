@@ -127,3 +127,22 @@ def test_tcgen05_inverse_tile_width_invariance(cuda, monkeypatch):
     monkeypatch.setenv("CJT_UMMA_BN256", "1")
     b = cj.inverse_batched(ip, t)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n,batch", [(1023, 37), (4095, 300), (4095, 1100)])
+def test_tcgen05_inverse_overlapped_conversion(cuda, n, batch, monkeypatch):
+    """$CJT_HALF_OVERLAP=1: the fp64 -> bf16 conversion runs concurrently with
+    the tcgen05 GEMM (programmatic dependent launch; the GEMM's TMA producers
+    wait on per-128-vector progress counters).  Same arithmetic, so the
+    results are bit-identical to the convert-then-multiply default, also on
+    repeated executions (the counters are reset per execution)."""
+    import torch
+    p = cj.JacobiParameters(0.5, 0.5)
+    ip = cj.plan("inverse", p, n)
+    t = torch.from_numpy(np.stack([O.seeded_vector(3, v, n) for v in range(batch)])).to(cuda)
+    monkeypatch.delenv("CJT_HALF_OVERLAP", raising=False)
+    a = cj.inverse_batched(ip, t)
+    monkeypatch.setenv("CJT_HALF_OVERLAP", "1")
+    for _ in range(3):
+        b = cj.inverse_batched(ip, t)
+        assert torch.equal(a, b)
