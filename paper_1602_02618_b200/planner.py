@@ -688,16 +688,28 @@ FUSED_MAX = 8192        # largest Bluestein length kept entirely in one CTA's sh
 # with register column passes (L <= 2^17), ~29 ps with shared-memory columns
 # (config-4 launch lists).
 _TILE_COST = {4096: (9.7, 6.5), 8192: (10.9, 7.1)}   # (forward, inverse)
+_MULTIPASS_COST = (18.5, 29.0)                       # register / shared-memory column passes
+
+
+def _cost_overrides():
+    """$CJT_TILE_COST="f4096,i4096,f8192,i8192,mp_reg,mp_smem" (experiments)."""
+    import os
+    e = os.environ.get("CJT_TILE_COST")
+    if not e:
+        return _TILE_COST, _MULTIPASS_COST
+    v = [float(x) for x in e.split(",")]
+    return {4096: (v[0], v[1]), 8192: (v[2], v[3])}, (v[4], v[5])
 
 
 def _cost(length: int, n_in: int, n_out: int) -> float:
+    tile, mp = _cost_overrides()
     if length <= FUSED_MAX:
-        fwd, inv = _TILE_COST[max(4096, length)]
+        fwd, inv = tile[max(4096, length)]
         return n_out * length * (fwd * n_in + inv)
     # multi-pass: half the per-point cost per FFT; tiled multi-pass runs one
     # forward FFT per input tile and one inverse FFT per output tile (input
     # spectra summed, or one forward spectrum shared by the output tiles)
-    return length * (18.5 if length <= 1 << 17 else 29.0) * 0.5 * (n_in + n_out)
+    return length * (mp[0] if length <= 1 << 17 else mp[1]) * 0.5 * (n_in + n_out)
 
 
 def _spectrum(g: int, p0: int, width: int, q0: int, count: int, length: int) -> np.ndarray:
