@@ -655,8 +655,11 @@ __device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* _
 
 // TM (tiling mode): 0 untiled, 1 input tiles, 2 output tiles (separate
 // instantiations keep the untiled kernel's register allocation unchanged)
+#ifndef CJT_ROWS_MINB
+#define CJT_ROWS_MINB 2
+#endif
 template <int LOG2, int TM>
-__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 12) ? 2 : 1)
+__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 11) ? CJT_ROWS_MINB : (LOG2 <= 12) ? 2 : 1)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ twg, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
   extern __shared__ double2 smem[];

@@ -17,7 +17,7 @@ for c in 3 2; do
         python bench.py --config $c --profile-stage $st --warmup 1 > $out/traffic_c${c}_$st.log 2>&1
   done
 done
-timeout 900 ncu --set full --import-source on --clock-control none --kernel-name regex:"k_half_fwd_warp|k_to_bf16|k_half_inv_umma" -c 3 -o $out/full_c3 \
+timeout 900 ncu --set full --import-source on --clock-control none --kernel-name regex:"k_half_fwd_warp|k_half_inv_umma" -c 2 -o $out/full_c3 \
     python bench.py --config 3 --profile --steps 1 --warmup 1 > $out/full_c3.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none \
     --kernel-name regex:"k_chirpz_fused|k_chirpz_rows|k_chirpz_cols|k_rec_inverse_ws|k_rec_forward_ws" -c 10 -o $out/full_c2 \

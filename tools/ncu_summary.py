@@ -18,6 +18,7 @@ METRICS = [
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_%", 1.0),
     ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "dmma_%", 1.0),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "dmma_inst_%", 1.0),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pipe_%", 1.0),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%", 1.0),
     ("launch__registers_per_thread", "regs", 1.0),
     ("launch__grid_size", "grid", 1.0),
