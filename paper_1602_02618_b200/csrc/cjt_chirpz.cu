@@ -1055,7 +1055,7 @@ int launch_chirpz(const ChirpZDev& cz, const double2* tw8192, const double* x, i
       default: return fail(CJT_EINVAL, "chirp-z length below 16");
     }
   }
-  if (lg <= 17 && cluster_enabled()) {
+  if (lg <= 17 && cz.n_in == 1 && cz.n_out == 1 && cluster_enabled()) {   // (tiled products keep the multi-pass layout)
     *launches += 1;
     switch (lg) {
       case 14: return run_cluster<12, 4>(cz, tw8192, x, ldx, out, ldo, batch, st);

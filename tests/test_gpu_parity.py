@@ -134,3 +134,35 @@ def test_parity_folding_full_size_forward(cuda, monkeypatch):
     torch.cuda.synchronize()
     d = (f_fold - f_flat).abs().max(dim=1).values / c.abs().sum(dim=1)
     assert float(d.max()) <= 1e-14
+
+
+def test_cluster_chirpz_path_golden():
+    """$CJT_CLUSTER=1 (opt-in): untiled Bluestein products of 2^14..2^17 points
+    run in thread-block clusters over distributed shared memory; tiled products
+    keep the multi-pass kernels.  Checked in a child process (the switch is read
+    once per process) against the reference's golden outputs of config 2."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path[:0] = [%r, %r, %r]\n"
+        "import numpy as np, torch\n"
+        "import cjt_oracle as O, paper_1602_02618_b200 as cj\n"
+        "from conftest import load_golden\n"
+        "worst = 0.0\n"
+        "for name in ('cfg2_full', 'cfg5_d'):\n"
+        "    g = load_golden(name)\n"
+        "    p = cj.JacobiParameters(float(g['alpha']), float(g['beta'])); n = int(g['n'])\n"
+        "    fp, ip = cj.plan('forward', p, n), cj.plan('inverse', p, n)\n"
+        "    f = cj.forward_batched(fp, torch.from_numpy(g['c']).cuda()).cpu().numpy()\n"
+        "    i = cj.inverse_batched(ip, torch.from_numpy(g['fwd']).cuda()).cpu().numpy()\n"
+        "    for v in range(g['c'].shape[0]):\n"
+        "        worst = max(worst, O.parity(f[v], g['fwd'][v], g['c'][v]), O.parity(i[v], g['inv'][v], g['c'][v]))\n"
+        "print('WORST', worst)\n"
+    ) % (root, os.path.join(root, "oracle"), os.path.join(root, "tests"))
+    env = dict(os.environ, CJT_CLUSTER="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    worst = float(out.stdout.strip().split("WORST")[-1])
+    assert worst <= TOL, worst
