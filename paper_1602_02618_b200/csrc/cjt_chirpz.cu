@@ -45,7 +45,11 @@ struct FusedCfg {
   // latency of the fused first / last passes better than radix-32 with 8 warps
   static constexpr int LEPT = LOGL == 13 ? CJT_FUSED13_LEPT : 4;
   static constexpr int EPT = 1 << LEPT;             // elements per thread
-  static constexpr int E = (L >= 4096) ? L : 4096;  // complex elements per CTA
+#ifndef CJT_FUSED_LOGEMIN
+#define CJT_FUSED_LOGEMIN 12
+#endif
+  static constexpr int EMIN = 1 << CJT_FUSED_LOGEMIN;
+  static constexpr int E = (L >= EMIN) ? L : EMIN;  // complex elements per CTA
   static constexpr int NG = E / L;                  // vectors per CTA
   static constexpr int T = E / EPT;                 // threads per CTA
   // 8192: the FFT buffer and accumulator leave ~23 KB of L1, less than the
@@ -283,7 +287,7 @@ __device__ __forceinline__ void fused_streamk(const ChirpZDev& cz, const TW& tw,
 
 // grid: direct (groups, n_out) or stream-K (P); see FusedSched.
 template <int LOGL, bool MULTI>
-__global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 2 : 1)
+__global__ void __launch_bounds__(FusedCfg<LOGL>::T, (LOGL <= 12) ? 512 / FusedCfg<LOGL>::T : 1)
     k_chirpz_fused(ChirpZDev cz, const double2* __restrict__ tw, const double* __restrict__ x,
                    int64_t ldx, double* __restrict__ out, int64_t ldo, int64_t batch,
                    double* __restrict__ part, double2* __restrict__ spec, FusedSched sk) {
@@ -630,7 +634,10 @@ struct RowCfg {
   static constexpr int L2 = 1 << LOG2;
   static constexpr int LEPT = (LOG2 == 13 && !fft2_used(LOG2)) ? 5 : 4;   // Fft2: 16 per thread
   static constexpr int EPT = 1 << LEPT;
-  static constexpr int E = (L2 >= 4096) ? L2 : 4096;
+#ifndef CJT_ROWS_EMIN
+#define CJT_ROWS_EMIN 1024
+#endif
+  static constexpr int E = (L2 >= CJT_ROWS_EMIN) ? L2 : CJT_ROWS_EMIN;   // complex elements per CTA
   static constexpr int NR = E / L2;
   static constexpr int T = E / EPT;
   // (4096 / 8192-point rows only: A/B on configs 2, 4, 5 -- the 1024 / 2048
@@ -659,7 +666,7 @@ __device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* _
 #define CJT_ROWS_MINB 2
 #endif
 template <int LOG2, int TM>
-__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 11) ? CJT_ROWS_MINB : (LOG2 <= 12) ? 2 : 1)
+__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 11) ? CJT_ROWS_MINB * 256 / RowCfg<LOG2>::T : (LOG2 <= 12) ? 2 : 1)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ twg, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
   extern __shared__ double2 smem[];
@@ -865,13 +872,15 @@ int set_smem(K kernel, int bytes) {
   return CJT_OK;
 }
 
-int fused_groups(int lg) { return lg >= 12 ? 1 : (1 << (12 - lg)); }
+int fused_groups(int lg) { return lg >= CJT_FUSED_LOGEMIN ? 1 : (1 << (CJT_FUSED_LOGEMIN - lg)); }
+// resident CTAs per SM (128 registers per thread: 512 threads)
+int fused_ctas_per_sm(int lg) { return lg > 12 ? 1 : 512 / (((1 << lg) * fused_groups(lg)) / 16); }
 
 // direct unless stream-K shortens the modelled critical path by > 10 %
 // (time in forward-FFT units, inverse FFT ~ one unit; partial traffic ignored)
 FusedSched fused_sched(const ChirpZDev& cz, int64_t batch) {
   const int ng = fused_groups(cz.log2len);
-  const int64_t slots = 148 * (cz.log2len <= 12 ? 2 : 1);
+  const int64_t slots = 148 * fused_ctas_per_sm(cz.log2len);
   const int64_t gn = (batch + ng - 1) / ng * cz.n_out;
   FusedSched sk{0, gn * cz.m_count, gn * cz.m_count * cz.n_in, 0, 0};
   const int64_t t_direct = (gn + slots - 1) / slots * cz.m_count * (cz.n_in + 1);
@@ -898,7 +907,7 @@ template <int LOGL>
 int run_fused(const ChirpZDev& cz, const double2* tw, const double* x, int64_t ldx, double* out,
               int64_t ldo, int64_t batch, double* part, double2* spec, cudaStream_t st, int* launches) {
   using Cfg = FusedCfg<LOGL>;
-  static_assert(Cfg::NG == (LOGL >= 12 ? 1 : (1 << (12 - LOGL))), "fused_groups out of sync");
+  static_assert(Cfg::NG == (LOGL >= CJT_FUSED_LOGEMIN ? 1 : (1 << (CJT_FUSED_LOGEMIN - LOGL))), "fused_groups out of sync");
   static DeviceOnce once_;
   if (int rc_ = once_([&]() -> int {
     if (int rc = set_smem(k_chirpz_fused<LOGL, false>, Cfg::SMEM)) return rc;
