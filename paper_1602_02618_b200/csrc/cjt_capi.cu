@@ -291,13 +291,16 @@ inline void unit_root(int64_t num, int64_t den, double* re, double* im) {
 // L = 8192: exp(-2 pi i u / 8192), u < 8192 (+ packed power tables); multi-pass L: the hi table
 // exp(-2 pi i a 4096 / L), a < max(1, L / 4096), followed by the lo table
 // exp(-2 pi i b / L), b < 4096.
-int shared_twiddles(int64_t L, const double2** out) {
+// col_log1 > 0 (multi-pass L with register column passes): followed by the
+// column twiddles [p][n2] = exp(-2 pi i n2 2^p / L), p < col_log1, n2 < L >> col_log1
+// (coalesced per-lane loads in k_chirpz_cols_fwd_reg)
+int shared_twiddles(int64_t L, const double2** out, int col_log1 = 0) {
   static std::map<std::pair<int, int64_t>, void*> cache;
   static std::mutex mu;
   int dev = 0;
   CJT_CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find({dev, L});
+  auto it = cache.find({dev, L * 64 + col_log1});
   if (it == cache.end()) {
     std::vector<double2> tw;
     if (L == 8192) {
@@ -312,11 +315,20 @@ int shared_twiddles(int64_t L, const double2** out) {
       tw.resize((size_t)(nhi + 4096));
       for (int64_t a = 0; a < nhi; ++a) unit_root(a * 4096, L, &tw[a].x, &tw[a].y);
       for (int64_t b = 0; b < 4096; ++b) unit_root(b, L, &tw[nhi + b].x, &tw[nhi + b].y);
+      if (col_log1 > 0) {
+        const int64_t L2 = L >> col_log1;
+        tw.resize((size_t)(nhi + 4096 + col_log1 * L2));
+        for (int p = 0; p < col_log1; ++p)
+          for (int64_t n2 = 0; n2 < L2; ++n2) {
+            double2& w = tw[(size_t)(nhi + 4096 + p * L2 + n2)];
+            unit_root((n2 << p) % L, L, &w.x, &w.y);
+          }
+      }
     }
     void* p = nullptr;
     CJT_CUDA_TRY(cudaMalloc(&p, tw.size() * sizeof(double2)));
     CJT_CUDA_TRY(cudaMemcpy(p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
-    it = cache.emplace(std::make_pair(dev, L), p).first;
+    it = cache.emplace(std::make_pair(dev, L * 64 + col_log1), p).first;
   }
   *out = (const double2*)it->second;
   return CJT_OK;
@@ -419,9 +431,11 @@ int build_chirpz(cjt_plan* P, const cjt_chirpz_desc& d, ChirpZDev* out) {
   }
   if (lg >= 14) {
     const double2* t = nullptr;
-    if (int rc = shared_twiddles(d.length, &t)) return rc;
+    const int col_log1 = (!cluster && cz.log1 <= 5) ? cz.log1 : 0;
+    if (int rc = shared_twiddles(d.length, &t, col_log1)) return rc;
     cz.tw_hi = t;
     cz.tw_lo = t + std::max<int64_t>(1, d.length / 4096);
+    cz.tw_col = col_log1 ? cz.tw_lo + 4096 : nullptr;
   }
   if (lg >= 14 && !cluster) {
     // one slot per input or output tile per (vector, term)

@@ -531,8 +531,11 @@ constexpr int COLR_T = 128;
 template <int R>
 __device__ __forceinline__ void column_twiddles(const ChirpZDev& cz, int64_t n2, double2* w) {
   w[0] = make_double2(1.0, 0.0);
+  // W_L^{n2 2^p} from the per-length column table: consecutive threads read
+  // consecutive entries (the two-level table costs a cache line per lane)
+  const int64_t L2 = (int64_t)1 << cz.log2;
 #pragma unroll
-  for (int j = 1; j < R; j <<= 1) w[j] = twiddle_L(cz, n2 * j);
+  for (int j = 1, p = 0; j < R; j <<= 1, ++p) w[j] = __ldg(cz.tw_col + p * L2 + n2);
 #pragma unroll
   for (int k = 3; k < R; ++k) {
     if ((k & (k - 1)) != 0) {

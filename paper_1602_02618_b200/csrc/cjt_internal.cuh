@@ -602,6 +602,7 @@ struct ChirpZDev {
   const double2* khat;      // fused: natural order; multipass: [k1][k2] = khat[k1 + L1 k2]
   const double2* tw_hi;     // multipass: exp(-2 pi i (a 4096) / L)
   const double2* tw_lo;     // multipass: exp(-2 pi i b / L), b < 4096
+  const double2* tw_col;    // multipass, register columns (log1 <= 5): [p][n2] = exp(-2 pi i n2 2^p / L), p < log1
   int32_t n_in, n_out;      // tiling (fused path only; 1 x 1 otherwise)
   int64_t count_max;        // largest output tile
   const int64_t* tin;       // [n_in][2] (offset, width)
