@@ -233,7 +233,8 @@ int cjt_kernel_plan_destroy(cjt_kernel_plan* plan);
  * angle phi_p of the point the reference's recurrence evaluates (interior:
  * acos(x_p); near +-1: from the half-angle x-+1 value xm_p), computed in
  * binary128, as inv_sin[p] = 1/sin(phi_p) and delta_over_sin[p] =
- * (phi_p - pi p/G)/sin(phi_p) (endpoint rows p = 0, G: 0).  Host only. */
+ * (phi_p - pi p/G)/sin(phi_p) (endpoint rows p = 0, G: 0).  With inv_sin ==
+ * delta_over_sin == NULL only k is computed (forward plans).  Host only. */
 int cjt_host_half_exact(const double* x, const double* xm, const int8_t* regions, int64_t G, int64_t n,
                         double* k, double* inv_sin, double* delta_over_sin);
 

@@ -40,13 +40,17 @@ __float128 effective_angle(double x, double xm, int8_t region) {
 
 extern "C" int cjt_host_half_exact(const double* x, const double* xm, const int8_t* regions, int64_t G,
                                    int64_t n, double* k, double* inv_sin, double* delta_over_sin) {
-  if (G < 1 || n < 0 || !x || !xm || !regions || !k || !inv_sin || !delta_over_sin) return CJT_EINVAL;
+  // inv_sin == delta_over_sin == nullptr: only k (the forward plan needs no row tables)
+  const bool want_rows = inv_sin || delta_over_sin;
+  if (n < 0 || !k) return CJT_EINVAL;
+  if (want_rows && (G < 1 || !x || !xm || !regions || !inv_sin || !delta_over_sin)) return CJT_EINVAL;
   // P_m(1) = Gamma(m + 3/2) / (Gamma(3/2) m!): P_m(1) = P_{m-1}(1) (m + 1/2) / m
   __float128 p1 = kOne;
   for (int64_t m = 0; m <= n; ++m) {
     if (m > 0) p1 = p1 * ((__float128)m + kHalf) / (__float128)m;
     k[m] = (double)(p1 / (__float128)(m + 1));
   }
+  if (!want_rows) return CJT_OK;
   auto rows = [&](int64_t p0, int64_t p1) {
     for (int64_t p = p0; p < p1; ++p) {
       if (p == 0 || p == G) {

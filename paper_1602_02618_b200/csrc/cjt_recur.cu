@@ -268,7 +268,32 @@ __global__ void __launch_bounds__(128) k_checkpoints(RecRowsDev rows, RecTablesD
     }
     __syncthreads();
     const int64_t n1 = min(n0 + CKW, nc - 1);
-    for (int64_t n = n0; n < n1; ++n) {
+    int64_t n = n0;
+    // whole checkpoint intervals: CK steps fully unrolled (table reads hoisted
+    // off the dependent chain, no per-step bounds or checkpoint tests); same
+    // operations in the same order as the tail loop below (bit-identical)
+    for (; n + CK <= n1; n += CK) {
+      const int kb = (int)(n - n0);
+      if (reg == 0) {
+#pragma unroll
+        for (int k = 0; k < CK; ++k) {
+          const double pn = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(w[0][kb + k], x), w[1][kb + k]), s1),
+                                      __dmul_rn(w[2][kb + k], s0));
+          s0 = s1;
+          s1 = pn;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < CK; ++k) {
+          const double d = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(w[0][kb + k], xm), s0), __dmul_rn(w[2][kb + k], s1)),
+                                     rfi_t[kb + k]);
+          s0 = __dmul_rn(__dadd_rn(s0, d), rf_t[kb + k]);
+          s1 = d;
+        }
+      }
+      out[(n + CK) / CK - 1] = make_double2(s0, s1);
+    }
+    for (; n < n1; ++n) {
       const int k = (int)(n - n0);
       const double a = w[0][k], c = w[2][k];
       if (reg == 0) {

@@ -839,6 +839,15 @@ def half_exact_enabled(p: JacobiParameters) -> bool:
     return p.alpha == 0.5 and p.beta == 0.5 and os.environ.get("CJT_HALF_EXACT", "1") != "0"
 
 
+def half_exact_k(n: int) -> np.ndarray:
+    """k_m = P_m(1)/(m+1), m <= n, in binary128 (all the forward plan needs)."""
+    from . import _native as nat
+    k = np.empty(n + 1)
+    nat.check(nat.lib().cjt_host_half_exact(None, None, None, 0, n, k.ctypes.data, None, None),
+              "cjt_host_half_exact")
+    return k
+
+
 def half_exact_tables(thetas: np.ndarray, regions: np.ndarray, g: int, n: int):
     """(k, inv_sin, delta_over_sin): k_m = P_m(1)/(m+1) (m <= n), and per grid
     row p the angle phi_p of the point the reference's recurrence evaluates
@@ -924,7 +933,10 @@ def _build_half_exact(hp: HostPlan) -> HostPlan:
     rows): forward = U -> T conversion with k_n, inverse = synthesis + one
     chirp-z (half_exact_inverse)."""
     g, n = hp.grid_n, hp.n
-    k, inv_sin, dos = half_exact_tables(hp.thetas, hp.regions, g, n)
+    if hp.direction == "inverse":
+        k, inv_sin, dos = half_exact_tables(hp.thetas, hp.regions, g, n)
+    else:
+        k = half_exact_k(n)     # the row tables (binary128, ~1 us per row) are the inverse's
     hp.half_k = k
     hp.exec_cuts = np.zeros(g + 1, dtype=np.int64)
     if hp.direction == "inverse":

@@ -59,7 +59,12 @@ class RaggedPlan:
             top[(a, b)] = max(top.get((a, b), 0), n)
         with cf.ThreadPoolExecutor(max_workers=threads) as ex:
             list(ex.map(lambda kv: planner.prewarm(JacobiParameters(*kv[0]), kv[1], m_terms), top.items()))
-            self.plans = list(ex.map(build, keys))
+            # largest degrees first (their plans take longest: no long tail)
+            by_cost = sorted(range(len(keys)), key=lambda i: -keys[i][2])
+            built = list(ex.map(build, [keys[i] for i in by_cost]))
+            self.plans = [None] * len(keys)
+            for i, pair in zip(by_cost, built):
+                self.plans[i] = pair
         # packed layout: group g occupies [offsets[g], offsets[g] + B_g (N_g + 1))
         lens = [b * (n + 1) for (a, bb, n), b in zip(keys, self.sizes)]
         self.offsets = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
