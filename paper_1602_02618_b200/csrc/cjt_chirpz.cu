@@ -668,8 +668,11 @@ __device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* _
 #ifndef CJT_ROWS_MINB
 #define CJT_ROWS_MINB 2
 #endif
+#ifndef CJT_ROWS12_MINB
+#define CJT_ROWS12_MINB 2
+#endif
 template <int LOG2, int TM>
-__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 11) ? CJT_ROWS_MINB * 256 / RowCfg<LOG2>::T : (LOG2 <= 12) ? 2 : 1)
+__global__ void __launch_bounds__(RowCfg<LOG2>::T, (LOG2 <= 11) ? CJT_ROWS_MINB * 256 / RowCfg<LOG2>::T : (LOG2 <= 12) ? CJT_ROWS12_MINB : 1)
     k_chirpz_rows(ChirpZDev cz, const double2* __restrict__ twg, double2* __restrict__ buf) {
   using Cfg = RowCfg<LOG2>;
   extern __shared__ double2 smem[];

@@ -14,7 +14,11 @@ data = json.loads(out.read_text()) if out.exists() else {}
 args = sys.argv[2:]
 for stage, path in zip(args[0::2], args[1::2]):
     rows = list(csv.reader(open(path)))
-    hdr = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+    hdr = next((i for i, r in enumerate(rows) if "Metric Name" in r), None)
+    if hdr is None:   # the stage launches no kernel in this configuration
+        data.setdefault(f"config{cfg}", {})[stage] = {"bytes": 0.0, "read": 0.0, "write": 0.0, "kernels": 0,
+                                                      "ncu_us": 0.0, "source": path}
+        continue
     h = rows[hdr]
     mi, vi, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
