@@ -371,7 +371,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           double tm = 1.0, hi = 2.0;
           if constexpr (!(DBG & 4)) {
             tm = xr[j * kTW + ml];
-            hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
+            if constexpr (DBG & 32) {   // experiment: t_{m+2} from lane + 2 (shuffle), shared memory for the last two lanes
+              const double hs = __shfl_down_sync(0xffffffffu, tm, 2);
+              hi = hs;
+              if (lane >= 30) hi = xr[j * kTW + ml + 2];
+            } else {
+              hi = xr[j * kTW + ml + 2];   // zero past N+1 (TMA fill)
+            }
           }
           double r;
           if constexpr (DBG & 8)
@@ -465,7 +471,7 @@ int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, c
 #define CJT_UD(D) case D: return launch_umma_dbg<BN, D>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
     CJT_UD(1)
 #ifdef CJT_UMMA_DBG_BUILD
-    CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10)
+    CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10) CJT_UD(32)
 #endif
 #undef CJT_UD
     default: return launch_umma_dbg<BN, 0>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
