@@ -330,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           "r"(smem_u32(br)), "l"(pol_x)
           : "memory");
     };
-    if (leader && !(DBG & 5)) issue_x(0);
+    if (leader && !(DBG & (5 | 64))) issue_x(0);
     int it = 0, sq = 0;
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       const int acc = it & 1;
@@ -355,7 +355,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c0 = kTRows * grp; c0 < kBN; c0 += kTRows * kEpiGroups, ++sq) {
         // (DBG bits, timing experiments only: 2 no result stores, 4 no t tiles,
         // 8 no fp64 arithmetic, 16 no accumulator loads)
-        if (leader && !(DBG & 4)) issue_x(sq + 1);         // its buffer was released by the barrier below
+        if (leader && !(DBG & (4 | 64))) issue_x(sq + 1);         // its buffer was released by the barrier below
+        double gt[kTRows], gh[kTRows];
+        if constexpr (DBG & 64) {   // experiment: t rows straight from global memory into registers
+#pragma unroll
+          for (int j = 0; j < kTRows; ++j) {
+            const int b = b0 + c0 + j;
+            const double* tp = t + (int64_t)b * n1 + m;
+            gt[j] = (mv && b < batch) ? __ldg(tp) : 0.0;
+            gh[j] = (m + 2 < n1 && b < batch) ? __ldg(tp + 2) : 0.0;
+          }
+        }
         float v[kTRows];
         if constexpr (DBG & 16) {
 #pragma unroll
@@ -363,13 +373,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         } else {
           tmem_ld8(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN + c0), v);
         }
-        if constexpr (!(DBG & 4)) mbar_wait(&xbar[grp][sq & 1], (uint32_t)((sq >> 1) & 1));
+        if constexpr (!(DBG & (4 | 64))) mbar_wait(&xbar[grp][sq & 1], (uint32_t)((sq >> 1) & 1));
         const double* xr = xb + (sq & 1) * (kTRows * kTW);
 #pragma unroll
         for (int j = 0; j < kTRows; ++j) {
           const int b = b0 + c0 + j;
           double tm = 1.0, hi = 2.0;
-          if constexpr (!(DBG & 4)) {
+          if constexpr (DBG & 64) {
+            tm = gt[j];
+            hi = gh[j];
+          } else if constexpr (!(DBG & 4)) {
             tm = xr[j * kTW + ml];
             if constexpr (DBG & 32) {   // experiment: t_{m+2} from lane + 2 (shuffle), shared memory for the last two lanes
               const double hs = __shfl_down_sync(0xffffffffu, tm, 2);
@@ -391,7 +404,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (mv && b < batch) __stcs(out + (int64_t)b * n1 + m, r);
           }
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group is done with this buffer
+        if constexpr (!(DBG & 64))
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group is done with this buffer
       }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);   // the leader may reuse this accumulator (both CTAs)
@@ -471,7 +485,7 @@ int launch_umma(const CUtensorMap& mm, const void* tbf, const CUtensorMap& mx, c
 #define CJT_UD(D) case D: return launch_umma_dbg<BN, D>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
     CJT_UD(1)
 #ifdef CJT_UMMA_DBG_BUILD
-    CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10) CJT_UD(32)
+    CJT_UD(2) CJT_UD(4) CJT_UD(6) CJT_UD(8) CJT_UD(12) CJT_UD(14) CJT_UD(16) CJT_UD(30) CJT_UD(10) CJT_UD(32) CJT_UD(64)
 #endif
 #undef CJT_UD
     default: return launch_umma_dbg<BN, 0>(mm, tbf, mx, t, k, out, n1, batch, sms, flags, st);
