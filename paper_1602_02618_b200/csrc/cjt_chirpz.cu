@@ -52,8 +52,9 @@ struct FusedCfg {
   static constexpr int E = (L >= EMIN) ? L : EMIN;  // complex elements per CTA
   static constexpr int NG = E / L;                  // vectors per CTA
   static constexpr int T = E / EPT;                 // threads per CTA
-  // 8192: the FFT buffer and accumulator leave ~23 KB of L1, less than the
-  // global twiddle table's working set -> twiddles from shared memory
+  // (build option, off: 8192-point tiles with the shared-memory twiddle table;
+  // the packed global tables' coalesced loads win although only ~23 KB of L1
+  // remain next to the FFT buffer and accumulator)
   static constexpr bool TW_SMEM = CJT_FUSED13_TWSMEM && LOGL == 13;
   static constexpr int SMEM = NG * padded_len(L) * 16 + E * 8 + (TW_SMEM ? 1024 * 16 : 0);
 };
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
   }
 }
 
-// column FFT twiddles from the shared-memory table (see CJT_ROWS_TWSMEM)
+// (build option, off: column FFT twiddles from the shared-memory table, see CJT_ROWS_TWSMEM)
 #ifndef CJT_COLS_TWSMEM
 #define CJT_COLS_TWSMEM 0
 #endif
@@ -626,9 +627,10 @@ __global__ void __launch_bounds__(COLR_T, (LOG1 <= 4) ? 4 : 1)
   }
 }
 
-// row FFT twiddles from a 1024-entry shared-memory table (TwSmem) instead
-// of the 8192-entry global table: the global table's scattered per-lane
-// loads cost L1 sectors the row kernels are short of
+// (build option, off: row FFT twiddles from a 1024-entry shared-memory table
+// (TwSmem).  It was the answer to the 8192-entry global table's scattered
+// per-lane loads, but its strided reads are 8-way bank conflicts; the packed
+// per-period tables (tw_pow, cjt_internal.cuh) are coalesced and faster)
 #ifndef CJT_ROWS_TWSMEM
 #define CJT_ROWS_TWSMEM 0
 #endif
