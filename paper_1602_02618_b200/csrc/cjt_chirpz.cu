@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(ClusterCfg<LOGQ, P>::T, 1)
 template <int LOG1>
 struct ColCfg {
   static constexpr int L1 = 1 << LOG1;
-  static constexpr int E = (L1 >= 4096) ? L1 : 4096;
+#ifndef CJT_COLS_EMIN
+#define CJT_COLS_EMIN 2048
+#endif
+  static constexpr int E = (L1 >= CJT_COLS_EMIN) ? L1 : CJT_COLS_EMIN;   // complex elements per CTA
   static constexpr int NC = E / L1;                  // columns per CTA
   static constexpr int T = E / 16;
   static constexpr int CS = padded_len(L1) + 1;      // odd column stride (conflict-free transpose)
@@ -459,7 +462,7 @@ struct ColCfg {
 
 // pass 1: x (real slice) * pre_m -> column FFTs over n1 -> * W_L^{n2 k1} -> buf[b][m][k1][n2]
 template <int LOG1>
-__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
+__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 512 / ColCfg<LOG1>::T)
     k_chirpz_cols_fwd(ChirpZDev cz, const double2* __restrict__ twg, const double* __restrict__ x,
                       int64_t ldx, double2* __restrict__ buf) {
   using Cfg = ColCfg<LOG1>;
@@ -805,7 +808,7 @@ __device__ __forceinline__ void rows_impl(ChirpZDev cz, const TW& tw, double2* _
 
 // pass 3: columns n2: * W_L^{-n2 k1} -> inverse FFT over k1 -> sum_m Re(post_m * y) -> out
 template <int LOG1>
-__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 2)
+__global__ void __launch_bounds__(ColCfg<LOG1>::T, (ColCfg<LOG1>::T >= 512) ? 1 : 512 / ColCfg<LOG1>::T)
     k_chirpz_cols_inv(ChirpZDev cz, const double2* __restrict__ twg,
                       const double2* __restrict__ buf, double* __restrict__ out, int64_t ldo) {
   using Cfg = ColCfg<LOG1>;
